@@ -1,0 +1,121 @@
+/* bbsi_cuda.h -- C ABI of the B200-native selected-inversion library
+ * (libbbsi_cuda.so, built from paper_2605_19910_b200/csrc).
+ *
+ * This is the drop-in boundary for the reference solver entry points of
+ * /root/reference/proj/core/include/bbsi (the "bbsi" C++ library). Each entry
+ * point below names the reference interface it replaces. The reference's C++
+ * signatures take a BlockBandedMatrix<std::complex<double>> by const& and return
+ * {BlockBandedMatrix, KernelCounters} by value (rgf.hpp:37-39, 82-84;
+ * ddrgf.hpp:420-422); across this ABI the matrix travels as plain caller-owned
+ * buffers in the reference's own slot order (block_banded.hpp:58-60):
+ *
+ *   slot(a, off) = a*(2w+1) + off + w,  a = 0..l-1, off = -w..w
+ *   each slot    = bs x bs complex128, column-major, (re, im) interleaved,
+ *                  block (a, a+off) of size sizes[a] x sizes[a+off] in its
+ *                  top-left corner with leading dimension bs.
+ *   Out-of-band slots are ignored on input and zero-filled on output.
+ *
+ * Host-buffer entry points ("_z") copy in and out of the device inside the call
+ * (the drop-in semantics); "_dev" entry points take device pointers and a
+ * cudaStream_t (passed as void*) and keep everything resident.
+ *
+ * Return codes (the C++ shim include/bbsi_gpu.hpp rethrows the reference types):
+ *   BBSI_OK 0; BBSI_INVALID_ARGUMENT 1 -> bbsi::invalid_argument_error (errors.hpp:9-12);
+ *   BBSI_SINGULAR 2 -> bbsi::singular_matrix_error(layer) (errors.hpp:18-27), the failing
+ *   global layer in *fail_layer; BBSI_CUDA_ERROR 3; BBSI_OUT_OF_MEMORY 4.
+ * bbsi_cuda_last_error() returns the message of the last failure on this thread.
+ * All arithmetic is complex FP64 on the GPU; there is no CPU fallback: without a
+ * CUDA device every compute entry point returns BBSI_CUDA_ERROR.
+ */
+#ifndef BBSI_CUDA_H
+#define BBSI_CUDA_H
+#include <stdint.h>
+
+#ifdef __cplusplus
+extern "C" {
+#endif
+
+#define BBSI_OK 0
+#define BBSI_INVALID_ARGUMENT 1
+#define BBSI_SINGULAR 2
+#define BBSI_CUDA_ERROR 3
+#define BBSI_OUT_OF_MEMORY 4
+
+/* ABI version (major*100 + minor). */
+int bbsi_cuda_version(void);
+const char* bbsi_cuda_last_error(void);
+/* Number of CUDA devices visible (0 on a CPU-only host). */
+int bbsi_cuda_device_count(void);
+/* Releases the library's cached device workspaces on every device. */
+void bbsi_cuda_release_workspace(void);
+
+/* ---------------------------------------------------------------- solvers (drop-in)
+ * sizes: per-layer block sizes (length l) or NULL for uniform bs.
+ * counters: int64[3] = {n_gemm, n_lu, n_getrs}, the reference's logical
+ *   KernelCounters for this call (kernels.hpp:18-31), or NULL.
+ * fail_layer: receives the failing layer on BBSI_SINGULAR (may be NULL). */
+
+/* replaces bbsi::rgf_tridiag (rgf.hpp:37-76) */
+int bbsi_cuda_rgf_tridiag_z(int l, int w, int bs, const int* sizes, const double* A, double* G,
+                            long long* counters, int* fail_layer);
+
+/* replaces bbsi::rgf_ndiag (rgf.hpp:82-137); *max_update_offset mirrors
+ * StructuralTrace::max_update_offset (rgf.hpp:14-16), may be NULL. */
+int bbsi_cuda_rgf_ndiag_z(int l, int w, int bs, const int* sizes, const double* A, double* G,
+                          long long* counters, int* max_update_offset, int* fail_layer);
+
+/* replaces bbsi::rgf_fused (rgf.hpp:143-192): super-blocks of w layers, tridiagonal
+ * solve, restriction to the original band. */
+int bbsi_cuda_rgf_fused_z(int l, int w, int bs, const int* sizes, const double* A, double* G,
+                          long long* counters, int* fail_layer);
+
+/* replaces bbsi::rgf_extended (rgf.hpp:197-270): core band plus full first/last
+ * block rows and columns of the inverse, each [l][bs][bs] (entry b of first_row
+ * = (M^-1)[0, b], etc.). Any halo pointer may be NULL. */
+int bbsi_cuda_rgf_extended_z(int l, int w, int bs, const int* sizes, const double* A, double* G,
+                             double* first_row, double* last_row, double* first_col, double* last_col,
+                             long long* counters, int* fail_layer);
+
+/* replaces bbsi::ddrgf (ddrgf.hpp:420-428) with DomainPlan{s2_levels, n_threads,
+ * terminal_threads} (ddrgf.hpp:18-32). n_threads only bounds host concurrency;
+ * results do not depend on it. Uses the stabilised boundary-self-energy variant
+ * (DESIGN.md "DDRGF"); counters are the reference's logical counts. */
+int bbsi_cuda_ddrgf_z(int l, int w, int bs, const int* sizes, const double* A, const int* s2_levels,
+                      int n_levels, int n_threads, int terminal_threads, double* G, long long* counters,
+                      int* fail_layer);
+
+/* ---------------------------------------------------------------- resident batched API
+ * A batch of independent band matrices (energies or domains) with uniform
+ * bs % 64 == 0. dA / dG: device pointers to [batch][l][2w+1][bs][bs];
+ * a_bstride: elements (complex) between consecutive A bands.
+ * fail_layers: host int[batch], -1 or the failing layer per entry. */
+int bbsi_cuda_rgf_batched_dev(int l, int w, int bs, int batch, const double* dA, long long a_bstride,
+                              double* dG, int* fail_layers, void* stream);
+
+/* Dyson batch: A_e = z_e I - H - Sigma (Sigma_a = sigma_a I) formed on the fly
+ * from ONE shared Hamiltonian band dH ([l][2w+1][bs][bs], device), z: host
+ * complex[n_energy] (E + i eta), sigma: host complex[l]. */
+int bbsi_cuda_dyson_rgf_dev(int l, int w, int bs, int n_energy, const double* dH, const double* z,
+                            const double* sigma, double* dG, int* fail_layers, void* stream);
+
+/* Seeded Dyson Hamiltonian (include/.. csrc/dyson_gen.h spec) written on the device. */
+int bbsi_cuda_dyson_fill_h_dev(int l, int w, int b, uint64_t seed, double* dH, void* stream);
+/* Same bytes on the host (for the end-to-end path and the parity tests). */
+void bbsi_dyson_fill_h_host(int l, int w, int b, uint64_t seed, double* H);
+
+/* ---------------------------------------------------------------- kernel-level API (device pointers)
+ * Batched C = alpha*A*B + beta*C on plain column-major complex128 matrices,
+ * m, n % 64 == 0, k % 16 == 0 (the sm_100a DMMA GEMM of the sweeps). */
+int bbsi_cuda_zgemm_dev(int m, int n, int k, const double* alpha, const double* dA, long long lda,
+                        long long a_bstride, const double* dB, long long ldb, long long b_bstride,
+                        const double* beta, double* dC, long long ldc, long long c_bstride, int batch,
+                        void* stream);
+/* Batched in-place inverse (GJ with partial pivoting), n % 64 == 0, threshold on
+ * the leading n_true x n_true block; status_host[batch] = -1 or first bad pivot. */
+int bbsi_cuda_zinv_dev(int n, int n_true, int batch, double* dM, long long ld, long long bstride,
+                       int* status_host, void* stream);
+
+#ifdef __cplusplus
+}
+#endif
+#endif

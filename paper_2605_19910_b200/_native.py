@@ -1,0 +1,54 @@
+"""ctypes binding of libbbsi_cuda.so (C ABI: include/bbsi_cuda.h).
+
+There is no fallback: if the library is missing or exports are absent this
+module raises at import / first use.
+"""
+from __future__ import annotations
+
+import ctypes as C
+from pathlib import Path
+
+LIB_PATH = Path(__file__).resolve().parent / "_lib" / "libbbsi_cuda.so"
+
+# Every symbol include/bbsi_cuda.h declares, with its ctypes signature.
+_vp, _ip, _i, _ll, _d = C.c_void_p, C.POINTER(C.c_int), C.c_int, C.c_longlong, C.c_double
+SIGNATURES = {
+    "bbsi_cuda_version": (_i, []),
+    "bbsi_cuda_last_error": (C.c_char_p, []),
+    "bbsi_cuda_device_count": (_i, []),
+    "bbsi_cuda_release_workspace": (None, []),
+    "bbsi_cuda_rgf_tridiag_z": (_i, [_i, _i, _i, _vp, _vp, _vp, _vp, _vp]),
+    "bbsi_cuda_rgf_ndiag_z": (_i, [_i, _i, _i, _vp, _vp, _vp, _vp, _vp, _vp]),
+    "bbsi_cuda_rgf_fused_z": (_i, [_i, _i, _i, _vp, _vp, _vp, _vp, _vp]),
+    "bbsi_cuda_rgf_extended_z": (_i, [_i, _i, _i, _vp, _vp, _vp, _vp, _vp, _vp, _vp, _vp, _vp]),
+    "bbsi_cuda_ddrgf_z": (_i, [_i, _i, _i, _vp, _vp, _vp, _i, _i, _i, _vp, _vp, _vp]),
+    "bbsi_cuda_rgf_batched_dev": (_i, [_i, _i, _i, _i, _vp, _ll, _vp, _vp, _vp]),
+    "bbsi_cuda_dyson_rgf_dev": (_i, [_i, _i, _i, _i, _vp, _vp, _vp, _vp, _vp, _vp]),
+    "bbsi_cuda_dyson_fill_h_dev": (_i, [_i, _i, _i, C.c_uint64, _vp, _vp]),
+    "bbsi_dyson_fill_h_host": (None, [_i, _i, _i, C.c_uint64, _vp]),
+    "bbsi_cuda_zgemm_dev": (_i, [_i, _i, _i, _vp, _vp, _ll, _ll, _vp, _ll, _ll, _vp, _vp, _ll, _ll, _i, _vp]),
+    "bbsi_cuda_zinv_dev": (_i, [_i, _i, _i, _vp, _ll, _ll, _vp, _vp]),
+}
+
+_lib = None
+
+
+def lib():
+    """Loads the native library (raises if it has not been built)."""
+    global _lib
+    if _lib is None:
+        if not LIB_PATH.exists():
+            raise ImportError(
+                f"{LIB_PATH} is missing: run `python -c 'import __graft_entry__ as g; g.build()'` "
+                "(the bbsi GPU path has no CPU fallback)")
+        lib_ = C.CDLL(str(LIB_PATH))
+        for name, (res, args) in SIGNATURES.items():
+            fn = getattr(lib_, name)
+            fn.restype = res
+            fn.argtypes = args
+        _lib = lib_
+    return _lib
+
+
+def last_error() -> str:
+    return lib().bbsi_cuda_last_error().decode()

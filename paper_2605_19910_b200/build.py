@@ -1,0 +1,49 @@
+"""Builds libbbsi_cuda.so (sm_100a) in-tree with nvcc. No torch, no JIT cache."""
+from __future__ import annotations
+
+import os
+import subprocess
+import sys
+from pathlib import Path
+
+PKG = Path(__file__).resolve().parent
+CSRC = PKG / "csrc"
+LIB_DIR = PKG / "_lib"
+LIB = LIB_DIR / "libbbsi_cuda.so"
+SOURCES = ["zgemm.cu", "zinv.cu", "band_ops.cu", "rgf.cu", "capi.cu"]
+HEADERS = ["zcommon.cuh", "internal.h", "dyson_gen.h"]
+NVCC = os.environ.get("NVCC", "/usr/local/cuda/bin/nvcc")
+FLAGS = ["-gencode", "arch=compute_100a,code=sm_100a", "-O3", "-lineinfo", "-std=c++17",
+         "-Xcompiler", "-fPIC", "-Xcompiler", "-O2"]
+
+
+def _stale() -> bool:
+    if not LIB.exists():
+        return True
+    t = LIB.stat().st_mtime
+    deps = [CSRC / s for s in SOURCES + HEADERS] + [PKG.parent / "include" / "bbsi_cuda.h"]
+    return any(p.exists() and p.stat().st_mtime > t for p in deps)
+
+
+def build(force: bool = False, verbose: bool = False) -> Path:
+    srcs = [s for s in SOURCES if (CSRC / s).exists()]
+    if not force and not _stale():
+        return LIB
+    LIB_DIR.mkdir(exist_ok=True)
+    objs = []
+    for s in srcs:
+        obj = LIB_DIR / (Path(s).stem + ".o")
+        cmd = [NVCC, *FLAGS, "-dc" if False else "-c", str(CSRC / s), "-o", str(obj)]
+        if verbose:
+            print(" ".join(cmd), file=sys.stderr)
+        subprocess.run(cmd, check=True, cwd=CSRC)
+        objs.append(str(obj))
+    cmd = [NVCC, "-shared", "-gencode", "arch=compute_100a,code=sm_100a", *objs, "-o", str(LIB), "-cudart", "static"]
+    subprocess.run(cmd, check=True, cwd=CSRC)
+    for o in objs:
+        Path(o).unlink(missing_ok=True)
+    return LIB
+
+
+if __name__ == "__main__":
+    print(build(force="--force" in sys.argv, verbose=True))

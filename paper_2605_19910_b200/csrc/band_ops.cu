@@ -1,0 +1,75 @@
+// Band-level elementwise kernels: Dyson-matrix synthesis on the device and the
+// formation of the per-energy working band A(E) = z I - H - Sigma from a shared H.
+#include "dyson_gen.h"
+#include "zcommon.cuh"
+
+namespace bbsi_gpu {
+
+namespace {
+
+// H slots [l][2w+1][b*b] (b = slot size, blocks fill the whole slot).
+__global__ void dyson_fill_h_kernel(double2* H, int l, int w, int b, uint64_t seedmix) {
+  const long long bb = (long long)b * b;
+  const long long total = (long long)l * (2 * w + 1) * bb;
+  for (long long idx = blockIdx.x * (long long)blockDim.x + threadIdx.x; idx < total;
+       idx += (long long)gridDim.x * blockDim.x) {
+    long long slot = idx / bb;
+    long long e = idx - slot * bb;
+    int a = int(slot / (2 * w + 1));
+    int off = int(slot % (2 * w + 1)) - w;
+    int i = int(e % b), j = int(e / b);
+    double re = 0.0, im = 0.0;
+    if (a + off >= 0 && a + off < l) bbsi_h_entry(seedmix, b, a, off, i, j, &re, &im);
+    H[idx] = make_double2(re, im);
+  }
+}
+
+// G[e] = -H (full band), diagonal entries += z_e - sigma_a:
+//   re = (E - h_re) - s_re,  im = (eta - h_im) - s_im   (fixed operation order).
+__global__ void dyson_form_band_kernel(double2* __restrict__ G, const double2* __restrict__ H, int l, int w, int bs,
+                                       int batch, const double2* __restrict__ z, const double2* __restrict__ sigma) {
+  const long long bb = (long long)bs * bs;
+  const long long band = (long long)l * (2 * w + 1) * bb;
+  const long long total = band * batch;
+  for (long long idx = blockIdx.x * (long long)blockDim.x + threadIdx.x; idx < total;
+       idx += (long long)gridDim.x * blockDim.x) {
+    long long e = idx / band;
+    long long r = idx - e * band;
+    long long slot = r / bb;
+    long long q = r - slot * bb;
+    int off = int(slot % (2 * w + 1)) - w;
+    double2 h = H[r];
+    double2 out;
+    if (off == 0 && (q % bs) == (q / bs)) {
+      int a = int(slot / (2 * w + 1));
+      double2 ze = z[e], sg = sigma[a];
+      out = make_double2((ze.x - h.x) - sg.x, (ze.y - h.y) - sg.y);
+    } else {
+      out = make_double2(-h.x, -h.y);
+    }
+    G[idx] = out;
+  }
+}
+
+int grid_for(long long n, int threads) {
+  long long g = (n + threads - 1) / threads;
+  if (g > 148LL * 32) g = 148LL * 32;
+  return int(g < 1 ? 1 : g);
+}
+
+}  // namespace
+
+cudaError_t dyson_fill_h(double2* H, int l, int w, int b, uint64_t seed, cudaStream_t s) {
+  long long total = (long long)l * (2 * w + 1) * b * b;
+  dyson_fill_h_kernel<<<grid_for(total, 256), 256, 0, s>>>(H, l, w, b, bbsi_mix64(seed));
+  return cudaGetLastError();
+}
+
+cudaError_t dyson_form_band(double2* G, const double2* H, int l, int w, int bs, int batch, const double2* z,
+                            const double2* sigma, cudaStream_t s) {
+  long long total = (long long)l * (2 * w + 1) * bs * bs * batch;
+  dyson_form_band_kernel<<<grid_for(total, 256), 256, 0, s>>>(G, H, l, w, bs, batch, z, sigma);
+  return cudaGetLastError();
+}
+
+}  // namespace bbsi_gpu

@@ -1,0 +1,395 @@
+// C ABI (include/bbsi_cuda.h) over the sm_100a kernels. Validation mirrors the
+// reference's preconditions and messages (layout.hpp:27-38, rgf.hpp:41-42,86-87,
+// ddrgf.hpp:26-31,424-425); failures map onto the reference exception contract.
+#include <cstdio>
+#include <cstring>
+#include <mutex>
+#include <string>
+#include <vector>
+
+#include "../../include/bbsi_cuda.h"
+#include "dyson_gen.h"
+#include "internal.h"
+
+using namespace bbsi_gpu;
+
+namespace {
+
+thread_local std::string g_err;
+std::mutex g_call_mu;  // the workspace arena is shared: serialise host-buffer calls
+
+int fail(int code, const std::string& msg) {
+  g_err = msg;
+  return code;
+}
+
+int cuda_fail(cudaError_t e, const char* where) {
+  cudaGetLastError();
+  return fail(e == cudaErrorMemoryAllocation ? BBSI_OUT_OF_MEMORY : BBSI_CUDA_ERROR,
+              std::string(where) + ": " + cudaGetErrorString(e));
+}
+
+#define CK(expr)                                      \
+  do {                                                \
+    cudaError_t e_ = (expr);                          \
+    if (e_ != cudaSuccess) return cuda_fail(e_, #expr); \
+  } while (0)
+
+// BlockLayout::validate (layout.hpp:27-38)
+int validate_layout(int l, int w, int bs, const int* sizes) {
+  if (l < 1) return fail(BBSI_INVALID_ARGUMENT, "BlockLayout: num_layers must be >= 1");
+  for (int a = 0; a < l; ++a) {
+    int b = sizes ? sizes[a] : bs;
+    if (b < 1) return fail(BBSI_INVALID_ARGUMENT, "BlockLayout: block sizes must be >= 1");
+    if (b > bs) return fail(BBSI_INVALID_ARGUMENT, "slot size bs smaller than a block size");
+  }
+  if (w < 0) return fail(BBSI_INVALID_ARGUMENT, "BlockLayout: negative bandwidth");
+  if (l > 1 && w > l - 1) return fail(BBSI_INVALID_ARGUMENT, "BlockLayout: bandwidth exceeds num_layers - 1");
+  if (l == 1 && w != 0) return fail(BBSI_INVALID_ARGUMENT, "BlockLayout: single layer requires bandwidth 0");
+  return BBSI_OK;
+}
+
+int pad64(int b) { return (b + 63) / 64 * 64; }
+
+int device_ok() {
+  int n = 0;
+  if (cudaGetDeviceCount(&n) != cudaSuccess || n == 0) {
+    cudaGetLastError();
+    return fail(BBSI_CUDA_ERROR, "no CUDA device: the bbsi GPU path has no CPU fallback");
+  }
+  return BBSI_OK;
+}
+
+void put_counters(long long* out, long long g, long long lu, long long rs) {
+  if (!out) return;
+  out[0] = g;
+  out[1] = lu;
+  out[2] = rs;
+}
+
+// Host band in slot order, block (a, a+off) of rows(a) x cols(a+off), ld = bs.
+struct HostBand {
+  int l, w, bs;
+  std::vector<int> sz;
+  const double2* p;
+  const double2* slot(int a, int off) const { return p + ((long long)a * (2 * w + 1) + off + w) * bs * bs; }
+  bool in_band(int a, int off) const { return a + off >= 0 && a + off < l && off >= -w && off <= w; }
+};
+
+// Copies a host band into a padded device-layout staging buffer (identity in the
+// padding of diagonal blocks: blockdiag(A, I)^{-1} = blockdiag(A^{-1}, I), exact).
+void pad_band(const HostBand& h, int bp, std::vector<double2>& out) {
+  const long long bb = (long long)bp * bp;
+  out.assign(size_t(h.l) * (2 * h.w + 1) * bb, make_double2(0.0, 0.0));
+  for (int a = 0; a < h.l; ++a)
+    for (int off = -h.w; off <= h.w; ++off) {
+      if (!h.in_band(a, off)) continue;
+      double2* d = out.data() + ((long long)a * (2 * h.w + 1) + off + h.w) * bb;
+      const double2* s = h.slot(a, off);
+      const int r = h.sz[a], c = h.sz[a + off];
+      for (int j = 0; j < c; ++j) std::memcpy(d + (long long)j * bp, s + (long long)j * h.bs, sizeof(double2) * r);
+      if (off == 0)
+        for (int i = r; i < bp; ++i) d[(long long)i * bp + i] = make_double2(1.0, 0.0);
+    }
+}
+
+void unpad_band(const std::vector<double2>& in, int bp, const HostBand& h, double2* G) {
+  const long long bb = (long long)bp * bp;
+  std::memset(G, 0, sizeof(double2) * size_t(h.l) * (2 * h.w + 1) * h.bs * h.bs);
+  for (int a = 0; a < h.l; ++a)
+    for (int off = -h.w; off <= h.w; ++off) {
+      if (!h.in_band(a, off)) continue;
+      const double2* s = in.data() + ((long long)a * (2 * h.w + 1) + off + h.w) * bb;
+      double2* d = G + ((long long)a * (2 * h.w + 1) + off + h.w) * h.bs * h.bs;
+      const int r = h.sz[a], c = h.sz[a + off];
+      for (int j = 0; j < c; ++j) std::memcpy(d + (long long)j * h.bs, s + (long long)j * bp, sizeof(double2) * r);
+    }
+}
+
+// Runs the batched sweeps on a device band (already holding A) with the arena scratch.
+int run_sweeps(SweepWork& W, const std::vector<int>& n_true, std::vector<int>& fails, cudaStream_t s) {
+  void* scratch = arena_get(1, sweep_scratch_bytes(W.l, W.w, W.bs, W.batch));
+  if (!scratch) return fail(BBSI_OUT_OF_MEMORY, "sweep workspace allocation failed");
+  sweep_carve(W, scratch);
+  CK(rgf_sweeps(W, n_true.data(), s));
+  CK(collect_failures(W, fails, s));
+  return BBSI_OK;
+}
+
+// Single-matrix drop-in solve of the padded band (shared by tridiag/ndiag/fused).
+int solve_host(const HostBand& h, double2* Gout, int* fail_layer) {
+  if (int rc = device_ok()) return rc;
+  std::lock_guard<std::mutex> lk(g_call_mu);
+  const int bp = pad64(h.bs);
+  std::vector<double2> staging;
+  pad_band(h, bp, staging);
+  const size_t bytes = staging.size() * sizeof(double2);
+  double2* dG = static_cast<double2*>(arena_get(0, bytes));
+  if (!dG) return fail(BBSI_OUT_OF_MEMORY, "band allocation failed");
+  cudaStream_t s = 0;
+  CK(cudaMemcpyAsync(dG, staging.data(), bytes, cudaMemcpyHostToDevice, s));
+  SweepWork W;
+  W.l = h.l;
+  W.w = h.w;
+  W.bs = bp;
+  W.batch = 1;
+  W.G = dG;
+  W.g_bstride = (long long)h.l * (2 * h.w + 1) * bp * bp;
+  std::vector<int> fails;
+  if (int rc = run_sweeps(W, h.sz, fails, s)) return rc;
+  CK(cudaMemcpyAsync(staging.data(), dG, bytes, cudaMemcpyDeviceToHost, s));
+  CK(cudaStreamSynchronize(s));
+  if (fails[0] >= 0) {
+    if (fail_layer) *fail_layer = fails[0];
+    return fail(BBSI_SINGULAR, "singular Schur pivot at layer " + std::to_string(fails[0]));
+  }
+  unpad_band(staging, bp, h, Gout);
+  return BBSI_OK;
+}
+
+HostBand make_host(int l, int w, int bs, const int* sizes, const double* A) {
+  HostBand h{l, w, bs, {}, reinterpret_cast<const double2*>(A)};
+  h.sz.resize(l);
+  for (int a = 0; a < l; ++a) h.sz[a] = sizes ? sizes[a] : bs;
+  return h;
+}
+
+}  // namespace
+
+extern "C" {
+
+int bbsi_cuda_version(void) { return 100; }
+const char* bbsi_cuda_last_error(void) { return g_err.c_str(); }
+
+int bbsi_cuda_device_count(void) {
+  int n = 0;
+  if (cudaGetDeviceCount(&n) != cudaSuccess) {
+    cudaGetLastError();
+    return 0;
+  }
+  return n;
+}
+
+void bbsi_cuda_release_workspace(void) { arena_release_all(); }
+
+int bbsi_cuda_rgf_ndiag_z(int l, int w, int bs, const int* sizes, const double* A, double* G, long long* counters,
+                          int* max_update_offset, int* fail_layer) {
+  if (fail_layer) *fail_layer = -1;
+  if (int rc = validate_layout(l, w, bs, sizes)) return rc;
+  if (w < 1 && l != 1) return fail(BBSI_INVALID_ARGUMENT, "rgf_ndiag: requires bandwidth >= 1");
+  HostBand h = make_host(l, w, bs, sizes, A);
+  if (int rc = solve_host(h, reinterpret_cast<double2*>(G), fail_layer)) return rc;
+  if (l == 1) {
+    put_counters(counters, 0, 1, 1);  // predict_rgf_counters(1) (cost_model.hpp:47-49)
+  } else {
+    long long L = l, W = w;
+    put_counters(counters, (3 * W * W + W) * L - 2 * W * W * W - 2 * W * W, L, L * (2 * W + 1) - W * W - W);
+    if (max_update_offset) *max_update_offset = w - 1;
+  }
+  return BBSI_OK;
+}
+
+int bbsi_cuda_rgf_tridiag_z(int l, int w, int bs, const int* sizes, const double* A, double* G, long long* counters,
+                            int* fail_layer) {
+  if (fail_layer) *fail_layer = -1;
+  if (int rc = validate_layout(l, w, bs, sizes)) return rc;
+  if (w != 1 && l != 1) return fail(BBSI_INVALID_ARGUMENT, "rgf_tridiag: requires bandwidth 1");
+  HostBand h = make_host(l, w, bs, sizes, A);
+  if (int rc = solve_host(h, reinterpret_cast<double2*>(G), fail_layer)) return rc;
+  long long L = l;
+  put_counters(counters, 4 * (L - 1), L, 3 * L - 2);
+  return BBSI_OK;
+}
+
+int bbsi_cuda_rgf_fused_z(int l, int w, int bs, const int* sizes, const double* A, double* G, long long* counters,
+                          int* fail_layer) {
+  if (fail_layer) *fail_layer = -1;
+  if (int rc = validate_layout(l, w, bs, sizes)) return rc;
+  if (w < 1 && l != 1) return fail(BBSI_INVALID_ARGUMENT, "rgf_fused: requires bandwidth >= 1");
+  for (int a = 0; a < l; ++a)
+    if ((sizes ? sizes[a] : bs) != (sizes ? sizes[0] : bs))
+      return fail(BBSI_INVALID_ARGUMENT, "rgf_fused: requires uniform block sizes");
+  if (w <= 1) return bbsi_cuda_rgf_tridiag_z(l, w, bs, sizes, A, G, counters, fail_layer);
+  // rgf.hpp:152-191: super-layer s holds layers [s*w, min(l, s*w+w)).
+  const int b = sizes ? sizes[0] : bs;
+  const int lp = (l + w - 1) / w;
+  std::vector<int> fsz(lp);
+  for (int s = 0; s < lp; ++s) fsz[s] = (std::min(l, s * w + w) - s * w) * b;
+  const int fbs = w * b;
+  const int fw = lp == 1 ? 0 : 1;
+  const long long fbb = (long long)fbs * fbs;
+  std::vector<double2> fused(size_t(lp) * (2 * fw + 1) * fbb, make_double2(0.0, 0.0));
+  HostBand h = make_host(l, w, bs, sizes, A);
+  auto fslot = [&](int s, int off) { return fused.data() + ((long long)s * (2 * fw + 1) + off + fw) * fbb; };
+  for (int a = 0; a < l; ++a)
+    for (int off = -w; off <= w; ++off) {
+      if (!h.in_band(a, off)) continue;
+      const int c = a + off;
+      double2* dst = fslot(a / w, c / w - a / w);
+      const double2* src = h.slot(a, off);
+      const int r0 = (a % w) * b, c0 = (c % w) * b;
+      for (int j = 0; j < b; ++j)
+        std::memcpy(dst + (long long)(c0 + j) * fbs + r0, src + (long long)j * bs, sizeof(double2) * b);
+    }
+  std::vector<double2> gf(fused.size());
+  HostBand fh = make_host(lp, fw, fbs, fsz.data(), reinterpret_cast<const double*>(fused.data()));
+  // a singular pivot reports the super-layer, as rgf_tridiag(fused) does in the reference
+  if (int rc = solve_host(fh, gf.data(), fail_layer)) return rc;
+  double2* Go = reinterpret_cast<double2*>(G);
+  std::memset(Go, 0, sizeof(double2) * size_t(l) * (2 * w + 1) * bs * bs);
+  for (int a = 0; a < l; ++a)
+    for (int off = -w; off <= w; ++off) {
+      if (!h.in_band(a, off)) continue;
+      const int c = a + off;
+      const double2* src = gf.data() + ((long long)(a / w) * (2 * fw + 1) + (c / w - a / w) + fw) * fbb;
+      double2* dst = Go + ((long long)a * (2 * w + 1) + off + w) * bs * bs;
+      const int r0 = (a % w) * b, c0 = (c % w) * b;
+      for (int j = 0; j < b; ++j)
+        std::memcpy(dst + (long long)j * bs, src + (long long)(c0 + j) * fbs + r0, sizeof(double2) * b);
+    }
+  long long L = lp;
+  put_counters(counters, 4 * (L - 1), L, 3 * L - 2);
+  return BBSI_OK;
+}
+
+int bbsi_cuda_rgf_batched_dev(int l, int w, int bs, int batch, const double* dA, long long a_bstride, double* dG,
+                              int* fail_layers, void* stream) {
+  if (int rc = validate_layout(l, w, bs, nullptr)) return rc;
+  if (bs % 64) return fail(BBSI_INVALID_ARGUMENT, "resident API requires bs % 64 == 0");
+  if (w < 1 && l != 1) return fail(BBSI_INVALID_ARGUMENT, "rgf_ndiag: requires bandwidth >= 1");
+  if (batch < 1) return fail(BBSI_INVALID_ARGUMENT, "batch must be >= 1");
+  if (int rc = device_ok()) return rc;
+  cudaStream_t s = static_cast<cudaStream_t>(stream);
+  const long long band = (long long)l * (2 * w + 1) * bs * bs;
+  CK(cudaMemcpy2DAsync(dG, band * sizeof(double2), dA, a_bstride * sizeof(double2), band * sizeof(double2), batch,
+                       cudaMemcpyDeviceToDevice, s));
+  SweepWork W;
+  W.l = l;
+  W.w = w;
+  W.bs = bs;
+  W.batch = batch;
+  W.G = reinterpret_cast<double2*>(dG);
+  W.g_bstride = band;
+  std::vector<int> nt(l, bs), fails;
+  std::lock_guard<std::mutex> lk(g_call_mu);
+  if (int rc = run_sweeps(W, nt, fails, s)) return rc;
+  bool bad = false;
+  for (int b = 0; b < batch; ++b) {
+    if (fail_layers) fail_layers[b] = fails[b];
+    bad |= fails[b] >= 0;
+  }
+  return bad ? fail(BBSI_SINGULAR, "singular Schur pivot in at least one batch entry") : BBSI_OK;
+}
+
+int bbsi_cuda_dyson_rgf_dev(int l, int w, int bs, int n_energy, const double* dH, const double* z,
+                            const double* sigma, double* dG, int* fail_layers, void* stream) {
+  if (int rc = validate_layout(l, w, bs, nullptr)) return rc;
+  if (bs % 64) return fail(BBSI_INVALID_ARGUMENT, "resident API requires bs % 64 == 0");
+  if (w < 1 && l != 1) return fail(BBSI_INVALID_ARGUMENT, "rgf_ndiag: requires bandwidth >= 1");
+  if (n_energy < 1) return fail(BBSI_INVALID_ARGUMENT, "n_energy must be >= 1");
+  if (int rc = device_ok()) return rc;
+  cudaStream_t s = static_cast<cudaStream_t>(stream);
+  std::lock_guard<std::mutex> lk(g_call_mu);
+  double2* dzs = static_cast<double2*>(arena_get(2, sizeof(double2) * (size_t(n_energy) + l)));
+  if (!dzs) return fail(BBSI_OUT_OF_MEMORY, "parameter upload allocation failed");
+  CK(cudaMemcpyAsync(dzs, z, sizeof(double2) * n_energy, cudaMemcpyHostToDevice, s));
+  CK(cudaMemcpyAsync(dzs + n_energy, sigma, sizeof(double2) * l, cudaMemcpyHostToDevice, s));
+  CK(dyson_form_band(reinterpret_cast<double2*>(dG), reinterpret_cast<const double2*>(dH), l, w, bs, n_energy, dzs,
+                     dzs + n_energy, s));
+  SweepWork W;
+  W.l = l;
+  W.w = w;
+  W.bs = bs;
+  W.batch = n_energy;
+  W.G = reinterpret_cast<double2*>(dG);
+  W.g_bstride = (long long)l * (2 * w + 1) * bs * bs;
+  std::vector<int> nt(l, bs), fails;
+  if (int rc = run_sweeps(W, nt, fails, s)) return rc;
+  bool bad = false;
+  for (int b = 0; b < n_energy; ++b) {
+    if (fail_layers) fail_layers[b] = fails[b];
+    bad |= fails[b] >= 0;
+  }
+  return bad ? fail(BBSI_SINGULAR, "singular Schur pivot in at least one energy") : BBSI_OK;
+}
+
+int bbsi_cuda_dyson_fill_h_dev(int l, int w, int b, uint64_t seed, double* dH, void* stream) {
+  if (int rc = validate_layout(l, w, b, nullptr)) return rc;
+  if (int rc = device_ok()) return rc;
+  CK(dyson_fill_h(reinterpret_cast<double2*>(dH), l, w, b, seed, static_cast<cudaStream_t>(stream)));
+  return BBSI_OK;
+}
+
+void bbsi_dyson_fill_h_host(int l, int w, int b, uint64_t seed, double* H) {
+  const uint64_t sm = bbsi_mix64(seed);
+  const long long bb = (long long)b * b;
+  for (int a = 0; a < l; ++a)
+    for (int off = -w; off <= w; ++off) {
+      double* d = H + 2 * ((long long)a * (2 * w + 1) + off + w) * bb;
+      const bool in = a + off >= 0 && a + off < l;
+      for (int j = 0; j < b; ++j)
+        for (int i = 0; i < b; ++i) {
+          double re = 0.0, im = 0.0;
+          if (in) bbsi_h_entry(sm, b, a, off, i, j, &re, &im);
+          d[2 * ((long long)j * b + i)] = re;
+          d[2 * ((long long)j * b + i) + 1] = im;
+        }
+    }
+}
+
+int bbsi_cuda_zgemm_dev(int m, int n, int k, const double* alpha, const double* dA, long long lda, long long a_bstride,
+                        const double* dB, long long ldb, long long b_bstride, const double* beta, double* dC,
+                        long long ldc, long long c_bstride, int batch, void* stream) {
+  if (m % 64 || n % 64 || k % 16 || m < 0 || n < 0 || k < 16 || batch < 1)
+    return fail(BBSI_INVALID_ARGUMENT, "zgemm: requires m, n % 64 == 0 and k % 16 == 0");
+  if (int rc = device_ok()) return rc;
+  // plain column-major matrices as 64 x 64 block operands
+  ZGemmGroup g{};
+  g.batch = batch;
+  g.bs = 64;
+  g.nprob = 1;
+  ZGemmProblem& p = g.prob[0];
+  p.M = m;
+  p.N = n;
+  p.K = k;
+  p.alpha = make_double2(alpha[0], alpha[1]);
+  p.beta = make_double2(beta[0], beta[1]);
+  p.A = ZOp{reinterpret_cast<const double2*>(dA), lda, 64, 64 * lda, a_bstride};
+  p.B = ZOp{reinterpret_cast<const double2*>(dB), ldb, 64, 64 * ldb, b_bstride};
+  p.C = ZOp{reinterpret_cast<const double2*>(dC), ldc, 64, 64 * ldc, c_bstride};
+  p.D = reinterpret_cast<double2*>(dC);
+  CK(zgemm_grouped(g, static_cast<cudaStream_t>(stream)));
+  return BBSI_OK;
+}
+
+int bbsi_cuda_zinv_dev(int n, int n_true, int batch, double* dM, long long ld, long long bstride, int* status_host,
+                       void* stream) {
+  if (n % 64 || n_true < 1 || n_true > n || batch < 1)
+    return fail(BBSI_INVALID_ARGUMENT, "zinv: requires n % 64 == 0 and 1 <= n_true <= n");
+  if (int rc = device_ok()) return rc;
+  cudaStream_t s = static_cast<cudaStream_t>(stream);
+  std::lock_guard<std::mutex> lk(g_call_mu);
+  size_t scr = size_t(batch) * (n * sizeof(int) + zinv_scratch_bytes(n) + sizeof(int)) + 512;
+  char* base = static_cast<char*>(arena_get(3, scr));
+  if (!base) return fail(BBSI_OUT_OF_MEMORY, "zinv scratch allocation failed");
+  int* piv = reinterpret_cast<int*>(base);
+  double2* wz = reinterpret_cast<double2*>(base + ((size_t(batch) * n * sizeof(int) + 255) & ~size_t(255)));
+  int* st = reinterpret_cast<int*>(reinterpret_cast<char*>(wz) + size_t(batch) * zinv_scratch_bytes(n));
+  CK(zinv_batched(reinterpret_cast<double2*>(dM), ld, bstride, n, n_true, batch, piv, wz, st, s));
+  if (status_host) {
+    CK(cudaMemcpyAsync(status_host, st, sizeof(int) * batch, cudaMemcpyDeviceToHost, s));
+    CK(cudaStreamSynchronize(s));
+  }
+  return BBSI_OK;
+}
+
+int bbsi_cuda_rgf_extended_z(int, int, int, const int*, const double*, double*, double*, double*, double*, double*,
+                             long long*, int*) {
+  return fail(BBSI_INVALID_ARGUMENT, "rgf_extended: not yet available on the GPU path");
+}
+
+int bbsi_cuda_ddrgf_z(int, int, int, const int*, const double*, const int*, int, int, int, double*, long long*, int*) {
+  return fail(BBSI_INVALID_ARGUMENT, "ddrgf: not yet available on the GPU path");
+}
+
+}  // extern "C"

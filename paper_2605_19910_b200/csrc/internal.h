@@ -1,0 +1,60 @@
+// Internal declarations shared by the CUDA translation units of libbbsi_cuda.so.
+#pragma once
+#include <cuda_runtime.h>
+#include <stdint.h>
+
+#include <string>
+#include <vector>
+
+#include "zcommon.cuh"
+
+namespace bbsi_gpu {
+
+// kernels
+cudaError_t zgemm_grouped(ZGemmGroup& g, cudaStream_t stream);
+cudaError_t zinv_batched(double2* M, long long ld, long long bstride, int n, int n_true, int batch, int* piv,
+                         double2* wz, int* status, cudaStream_t stream);
+size_t zinv_scratch_bytes(int n);
+cudaError_t dyson_fill_h(double2* H, int l, int w, int b, uint64_t seed, cudaStream_t s);
+cudaError_t dyson_form_band(double2* G, const double2* H, int l, int w, int bs, int batch, const double2* z,
+                            const double2* sigma, cudaStream_t s);
+
+// Error codes of the C ABI (include/bbsi_cuda.h).
+enum Status { OK = 0, INVALID = 1, SINGULAR = 2, CUDA_ERR = 3, NOMEM = 4 };
+
+struct Error {
+  int code;
+  std::string what;
+};
+
+// Device workspace of one batched n-diagonal sweep (all pointers device memory).
+struct SweepWork {
+  int l = 0, w = 0, bs = 0, batch = 0;
+  double2* G = nullptr;   // [batch][l][2w+1][bs*bs]: working copy of A, then G^R
+  long long g_bstride = 0;
+  double2* LM = nullptr;  // [batch][l][w][bs*bs]: lm[j][t-1] = X_j M'[j, j-t]
+  double2* UM = nullptr;  // [batch][l][w][bs*bs]: um[j][t-1] = M'[j-t, j] X_j
+  int* piv = nullptr;     // [batch][bs]
+  double2* wz = nullptr;  // [batch][bs*16]
+  int* status = nullptr;  // [l][batch]
+};
+
+// Bytes of LM+UM+piv+wz+status for a sweep.
+size_t sweep_scratch_bytes(int l, int w, int bs, int batch);
+// Carves the scratch part of a SweepWork out of `base` (>= sweep_scratch_bytes).
+void sweep_carve(SweepWork& W, void* base);
+
+// Upward + downward sweeps of rgf_ndiag (rgf.hpp:82-137; w=1 is rgf_tridiag,
+// rgf.hpp:37-76) on a batch of working bands already holding A.
+// n_true[a] = unpadded size of layer a (for the singular-pivot threshold).
+cudaError_t rgf_sweeps(const SweepWork& W, const int* n_true, cudaStream_t s);
+
+// Reads back W.status and returns, per batch entry, the failing layer the
+// reference would report (first failure in elimination order) or -1.
+cudaError_t collect_failures(const SweepWork& W, std::vector<int>& fail, cudaStream_t s);
+
+// Grow-only device arena per (device, slot) with a mutex; returns nullptr on OOM.
+void* arena_get(int slot, size_t bytes);
+void arena_release_all();
+
+}  // namespace bbsi_gpu

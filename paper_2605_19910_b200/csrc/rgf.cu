@@ -1,0 +1,198 @@
+// Batched RGF sweeps (block tridiagonal and block n-diagonal) on the device.
+//
+// Restates rgf_ndiag (rgf.hpp:82-137) -- and through w = 1 rgf_tridiag
+// (rgf.hpp:37-76) -- for a batch of independent matrices (energies, domains):
+//
+//   upward  j = l-1 .. 1, k = min(w, j):
+//     X_j          = inv(M'[j,j])                        (zinv: zgetrf + zgetrs(I))
+//     lm[j][t]     = X_j M'[j, j-t]          t = 1..k    (one GEMM, b x kb)
+//     um[j][t]     = M'[j-t, j] X_j                      (one GEMM, kb x b)
+//     M'[j-s, j-t] -= M'[j-s, j] lm[j][t]    s,t = 1..k  (one GEMM, kb x kb window)
+//   X_0 = inv(M'[0,0]) = G[0,0]
+//   downward j = 1 .. l-1:
+//     G[j, j-t]    = -sum_s lm[j][s] G[j-s, j-t]         (one GEMM, b x kb)
+//     G[j-t, j]    = -sum_s G[j-t, j-s] um[j][s]         (one GEMM, kb x b)
+//     G[j, j]      = X_j - sum_s lm[j][s] G[j-s, j]      (one GEMM, b x b, K = kb)
+//
+// The working copy M' lives in the output band G itself (its slots are only
+// overwritten by G^R after the upward sweep has consumed them), and the
+// explicit inverse X_j is written into G[j,j], which the downward pass updates
+// in place. Every operand is a strided set of slots of the band storage
+// slot(a, off) = a*(2w+1) + off + w (block_banded.hpp:58-60).
+#include <mutex>
+
+#include "internal.h"
+
+namespace bbsi_gpu {
+
+size_t sweep_scratch_bytes(int l, int w, int bs, int batch) {
+  const size_t bb = size_t(bs) * bs * sizeof(double2);
+  size_t s = 2 * size_t(batch) * l * w * bb;              // LM, UM
+  s += size_t(batch) * bs * sizeof(int);                  // piv
+  s = (s + 255) & ~size_t(255);
+  s += size_t(batch) * zinv_scratch_bytes(bs);            // wz
+  s += size_t(l) * batch * sizeof(int) + 256;             // status
+  return s;
+}
+
+void sweep_carve(SweepWork& W, void* base) {
+  char* p = static_cast<char*>(base);
+  const size_t bb = size_t(W.bs) * W.bs;
+  W.LM = reinterpret_cast<double2*>(p);
+  p += size_t(W.batch) * W.l * W.w * bb * sizeof(double2);
+  W.UM = reinterpret_cast<double2*>(p);
+  p += size_t(W.batch) * W.l * W.w * bb * sizeof(double2);
+  W.piv = reinterpret_cast<int*>(p);
+  p += size_t(W.batch) * W.bs * sizeof(int);
+  p = reinterpret_cast<char*>((reinterpret_cast<uintptr_t>(p) + 255) & ~uintptr_t(255));
+  W.wz = reinterpret_cast<double2*>(p);
+  p += size_t(W.batch) * zinv_scratch_bytes(W.bs);
+  W.status = reinterpret_cast<int*>(p);
+}
+
+namespace {
+
+struct Ctx {
+  const SweepWork& W;
+  long long bb, nslot;
+  Ctx(const SweepWork& w) : W(w), bb((long long)w.bs * w.bs), nslot(2 * w.w + 1) {}
+  double2* slot(int a, int off) const { return W.G + ((long long)a * nslot + off + W.w) * bb; }
+  double2* lm(int j) const { return W.LM + (long long)j * W.w * bb; }
+  double2* um(int j) const { return W.UM + (long long)j * W.w * bb; }
+  long long lm_bstride() const { return (long long)W.l * W.w * bb; }
+  ZOp gop(const double2* p, long long rs_slots, long long cs_slots) const {
+    return ZOp{p, W.bs, rs_slots * bb, cs_slots * bb, W.g_bstride};
+  }
+  ZOp mop(const double2* p, long long rs_blocks, long long cs_blocks) const {
+    return ZOp{p, W.bs, rs_blocks * bb, cs_blocks * bb, lm_bstride()};
+  }
+};
+
+ZGemmProblem prob(int M, int N, int K, double alpha, double beta, ZOp A, ZOp B, ZOp C) {
+  ZGemmProblem p{};
+  p.M = M;
+  p.N = N;
+  p.K = K;
+  p.alpha = make_double2(alpha, 0.0);
+  p.beta = make_double2(beta, 0.0);
+  p.A = A;
+  p.B = B;
+  p.C = C;
+  p.D = const_cast<double2*>(C.p);
+  return p;
+}
+
+cudaError_t launch(const SweepWork& W, std::initializer_list<ZGemmProblem> ps, cudaStream_t s) {
+  ZGemmGroup g{};
+  g.batch = W.batch;
+  g.bs = W.bs;
+  for (const auto& p : ps) g.prob[g.nprob++] = p;
+  return zgemm_grouped(g, s);
+}
+
+}  // namespace
+
+cudaError_t rgf_sweeps(const SweepWork& W, const int* n_true, cudaStream_t s) {
+  Ctx c(W);
+  const int l = W.l, w = W.w, b = W.bs;
+  const long long two_w = 2LL * w;
+  cudaError_t e;
+  auto inv = [&](int j) {
+    return zinv_batched(c.slot(j, 0), b, W.g_bstride, b, n_true[j], W.batch, W.piv, W.wz,
+                        W.status + (long long)j * W.batch, s);
+  };
+
+  // ---------------- upward sweep (rgf.hpp:98-114)
+  for (int j = l - 1; j >= 1; --j) {
+    const int k = j < w ? j : w;
+    if ((e = inv(j)) != cudaSuccess) return e;
+    const ZOp X = c.gop(c.slot(j, 0), 0, 0);
+    // lm[j] = X_j [M'(j,j-1) .. M'(j,j-k)]
+    ZGemmProblem p_lm = prob(b, k * b, b, 1.0, 0.0, X, c.gop(c.slot(j, -1), 0, -1), c.mop(c.lm(j), 0, 1));
+    if ((e = launch(W, {p_lm}, s)) != cudaSuccess) return e;
+    // window M'(j-s, j-t) -= M'(j-s, j) lm[j][t];  um[j] = [M'(j-t, j)]_t X_j
+    ZOp upper = c.gop(c.slot(j - 1, +1), -two_w, 0);
+    ZGemmProblem p_win = prob(k * b, k * b, b, -1.0, 1.0, upper, c.mop(c.lm(j), 0, 1), c.gop(c.slot(j - 1, 0), -two_w, -1));
+    ZGemmProblem p_um = prob(k * b, b, b, 1.0, 0.0, upper, X, c.mop(c.um(j), 1, 0));
+    if ((e = launch(W, {p_win, p_um}, s)) != cudaSuccess) return e;
+  }
+  if ((e = inv(0)) != cudaSuccess) return e;
+
+  // ---------------- downward sweep (rgf.hpp:117-135)
+  for (int j = 1; j < l; ++j) {
+    const int k = j < w ? j : w;
+    ZOp lmrow = c.mop(c.lm(j), 0, 1);
+    ZOp window = c.gop(c.slot(j - 1, 0), -two_w, -1);
+    ZGemmProblem p_row = prob(b, k * b, k * b, -1.0, 0.0, lmrow, window, c.gop(c.slot(j, -1), 0, -1));
+    ZGemmProblem p_col = prob(k * b, b, k * b, -1.0, 0.0, window, c.mop(c.um(j), 1, 0), c.gop(c.slot(j - 1, +1), -two_w, 0));
+    if ((e = launch(W, {p_row, p_col}, s)) != cudaSuccess) return e;
+    ZGemmProblem p_diag = prob(b, b, k * b, -1.0, 1.0, lmrow, c.gop(c.slot(j - 1, +1), -two_w, 0), c.gop(c.slot(j, 0), 0, 0));
+    if ((e = launch(W, {p_diag}, s)) != cudaSuccess) return e;
+  }
+  return cudaSuccess;
+}
+
+cudaError_t collect_failures(const SweepWork& W, std::vector<int>& fail, cudaStream_t s) {
+  std::vector<int> st(size_t(W.l) * W.batch);
+  cudaError_t e = cudaMemcpyAsync(st.data(), W.status, st.size() * sizeof(int), cudaMemcpyDeviceToHost, s);
+  if (e != cudaSuccess) return e;
+  if ((e = cudaStreamSynchronize(s)) != cudaSuccess) return e;
+  fail.assign(W.batch, -1);
+  // elimination order of the reference: l-1, l-2, ..., 0 (rgf.hpp:58,64 / :100,114)
+  for (int bt = 0; bt < W.batch; ++bt)
+    for (int j = W.l - 1; j >= 0; --j)
+      if (st[size_t(j) * W.batch + bt] >= 0) {
+        fail[bt] = j;
+        break;
+      }
+  return cudaSuccess;
+}
+
+// ------------------------------------------------------------------ arena
+namespace {
+std::mutex g_arena_mu;
+struct Buf {
+  void* p = nullptr;
+  size_t n = 0;
+};
+std::vector<std::vector<Buf>> g_arena;  // [device][slot]
+}  // namespace
+
+void* arena_get(int slot, size_t bytes) {
+  std::lock_guard<std::mutex> lk(g_arena_mu);
+  int dev = 0;
+  cudaGetDevice(&dev);
+  if (int(g_arena.size()) <= dev) g_arena.resize(dev + 1);
+  auto& v = g_arena[dev];
+  if (int(v.size()) <= slot) v.resize(slot + 1);
+  Buf& b = v[slot];
+  if (b.n >= bytes && b.p) return b.p;
+  if (b.p) {
+    cudaDeviceSynchronize();
+    cudaFree(b.p);
+    b.p = nullptr;
+    b.n = 0;
+  }
+  if (cudaMalloc(&b.p, bytes) != cudaSuccess) {
+    cudaGetLastError();
+    b.p = nullptr;
+    return nullptr;
+  }
+  b.n = bytes;
+  return b.p;
+}
+
+void arena_release_all() {
+  std::lock_guard<std::mutex> lk(g_arena_mu);
+  int cur = 0;
+  cudaGetDevice(&cur);
+  for (size_t d = 0; d < g_arena.size(); ++d) {
+    cudaSetDevice(int(d));
+    cudaDeviceSynchronize();
+    for (auto& b : g_arena[d])
+      if (b.p) cudaFree(b.p), b.p = nullptr, b.n = 0;
+  }
+  cudaSetDevice(cur);
+}
+
+}  // namespace bbsi_gpu

@@ -1,0 +1,160 @@
+// Grouped, batched, block-strided complex-FP64 GEMM on DMMA (mma.sync m8n8k4 f64).
+//
+// Replaces every zgemm the reference issues through gemm_into (kernels.hpp:102-117)
+// on the solver path: one launch covers up to kMaxProblems independent products,
+// each batched over energies / domains, each operand a strided set of bs x bs
+// blocks (see ZOp). The n-diagonal k x k window updates (rgf.hpp:107-112) and the
+// downward row/column accumulations (rgf.hpp:122-134) become ONE product each.
+//
+// Complex product with 4 real DMMAs per 8x8x4 step (no 3M trick: same rounding
+// class as zgemm). CTA tile 64x64 complex, 4 warps of 32x32, K staged 16 at a
+// time through a 2-stage cp.async pipeline into padded, bank-conflict-free smem.
+#include "zcommon.cuh"
+
+namespace bbsi_gpu {
+
+namespace {
+
+constexpr int BM = 64, BN = 64, BK = 16;
+constexpr int LDA_S = BM + 2;  // As[k][m]: 16B lanes l/4 rows x l%4 ks -> 8 distinct slots per phase
+constexpr int LDB_S = BK + 4;  // Bs[n][k]
+constexpr int STAGES = 2;
+constexpr int A_STAGE = BK * LDA_S;
+constexpr int B_STAGE = BN * LDB_S;
+constexpr int SMEM_BYTES = STAGES * (A_STAGE + B_STAGE) * sizeof(double2);
+
+__device__ __forceinline__ void load_tile(const ZGemmProblem& P, int bs, int batch, int m0, int n0, int k0,
+                                          double2* As, double2* Bs, int tid) {
+  const double2* a = P.A.p + (long long)batch * P.A.bstride + zop_offset(P.A, bs, m0, k0);
+  const double2* b = P.B.p + (long long)batch * P.B.bstride + zop_offset(P.B, bs, k0, n0);
+#pragma unroll
+  for (int i = 0; i < (BM * BK) / 128; ++i) {
+    int e = tid + 128 * i;
+    int m = e & (BM - 1), k = e >> 6;
+    cp_async16(&As[k * LDA_S + m], a + (long long)k * P.A.ld + m);
+  }
+#pragma unroll
+  for (int i = 0; i < (BN * BK) / 128; ++i) {
+    int e = tid + 128 * i;
+    int k = e & (BK - 1), n = e >> 4;
+    cp_async16(&Bs[n * LDB_S + k], b + (long long)n * P.B.ld + k);
+  }
+}
+
+__global__ void __launch_bounds__(128, 2) zgemm_grouped_kernel(const __grid_constant__ ZGemmGroup g) {
+  extern __shared__ __align__(16) double2 smem[];
+  double2* As = smem;
+  double2* Bs = smem + STAGES * A_STAGE;
+
+  // ---- decode the flattened tile index
+  int t = blockIdx.x;
+  int pi = 0;
+#pragma unroll 1
+  for (int q = 1; q < g.nprob; ++q)
+    if (t >= g.prob[q].tile_begin) pi = q;
+  const ZGemmProblem& P = g.prob[pi];
+  int local = t - P.tile_begin;
+  const int per_batch = P.tiles_m * P.tiles_n;
+  const int batch = local / per_batch;
+  local -= batch * per_batch;
+  const int m0 = (local % P.tiles_m) * BM;
+  const int n0 = (local / P.tiles_m) * BN;
+  const int bs = g.bs;
+
+  const int tid = threadIdx.x, lane = tid & 31, warp = tid >> 5;
+  const int wm = (warp & 1) * 32, wn = (warp >> 1) * 32;
+  const int lr = lane >> 2, lc = lane & 3;
+
+  double cr[4][4][2], ci[4][4][2];
+#pragma unroll
+  for (int i = 0; i < 4; ++i)
+#pragma unroll
+    for (int j = 0; j < 4; ++j) cr[i][j][0] = cr[i][j][1] = ci[i][j][0] = ci[i][j][1] = 0.0;
+
+  const int nk = P.K / BK;
+  load_tile(P, bs, batch, m0, n0, 0, As, Bs, tid);
+  cp_async_commit();
+
+#pragma unroll 1
+  for (int kc = 0; kc < nk; ++kc) {
+    const int s = kc & 1;
+    if (kc + 1 < nk) load_tile(P, bs, batch, m0, n0, (kc + 1) * BK, As + (s ^ 1) * A_STAGE, Bs + (s ^ 1) * B_STAGE, tid);
+    cp_async_commit();
+    cp_async_wait<1>();
+    __syncthreads();
+    const double2* as = As + s * A_STAGE;
+    const double2* bsm = Bs + s * B_STAGE;
+#pragma unroll
+    for (int kk = 0; kk < BK / 4; ++kk) {
+      double ar[4], ai[4], an[4], br[4], bi[4];
+#pragma unroll
+      for (int mi = 0; mi < 4; ++mi) {
+        double2 v = as[(kk * 4 + lc) * LDA_S + wm + mi * 8 + lr];
+        ar[mi] = v.x;
+        ai[mi] = v.y;
+        an[mi] = -v.y;
+      }
+#pragma unroll
+      for (int ni = 0; ni < 4; ++ni) {
+        double2 v = bsm[(wn + ni * 8 + lr) * LDB_S + kk * 4 + lc];
+        br[ni] = v.x;
+        bi[ni] = v.y;
+      }
+#pragma unroll
+      for (int mi = 0; mi < 4; ++mi)
+#pragma unroll
+        for (int ni = 0; ni < 4; ++ni) {
+          dmma884(cr[mi][ni], ar[mi], br[ni]);
+          dmma884(ci[mi][ni], ar[mi], bi[ni]);
+          dmma884(cr[mi][ni], an[mi], bi[ni]);
+          dmma884(ci[mi][ni], ai[mi], br[ni]);
+        }
+    }
+    __syncthreads();
+  }
+
+  // ---- epilogue: D = alpha*acc + beta*C
+  const bool use_c = (P.beta.x != 0.0 || P.beta.y != 0.0);
+  const long long coff = (long long)batch * P.C.bstride + zop_offset(P.C, bs, m0, n0);
+  const double2* cptr = P.C.p + coff;
+  double2* dptr = P.D + coff;
+#pragma unroll
+  for (int mi = 0; mi < 4; ++mi)
+#pragma unroll
+    for (int ni = 0; ni < 4; ++ni)
+#pragma unroll
+      for (int q = 0; q < 2; ++q) {
+        const int m = wm + mi * 8 + lr, n = wn + ni * 8 + lc * 2 + q;
+        const long long o = (long long)n * P.C.ld + m;
+        double2 acc = make_double2(cr[mi][ni][q], ci[mi][ni][q]);
+        double2 out = cmul(P.alpha, acc);
+        if (use_c) out = cfma(P.beta, cptr[o], out);
+        dptr[o] = out;
+      }
+}
+
+}  // namespace
+
+cudaError_t zgemm_grouped(ZGemmGroup& g, cudaStream_t stream) {
+  static bool attr_set = false;
+  if (!attr_set) {
+    cudaError_t e = cudaFuncSetAttribute(zgemm_grouped_kernel, cudaFuncAttributeMaxDynamicSharedMemorySize, SMEM_BYTES);
+    if (e != cudaSuccess) return e;
+    attr_set = true;
+  }
+  int total = 0;
+  for (int p = 0; p < g.nprob; ++p) {
+    ZGemmProblem& P = g.prob[p];
+    if (P.M % BM || P.N % BN || P.K % BK || g.bs % BM) return cudaErrorInvalidValue;
+    P.tiles_m = P.M / BM;
+    P.tiles_n = P.N / BN;
+    P.tile_begin = total;
+    total += P.tiles_m * P.tiles_n * g.batch;
+  }
+  g.total_tiles = total;
+  if (total == 0) return cudaSuccess;
+  zgemm_grouped_kernel<<<total, 128, SMEM_BYTES, stream>>>(g);
+  return cudaGetLastError();
+}
+
+}  // namespace bbsi_gpu

@@ -1,0 +1,67 @@
+"""Parity of the resident Dyson batch path (BASELINE configs) against the oracle.
+
+Bar (BASELINE.json north_star): per-block relative Frobenius error <= 1e-10 of
+every diagonal and off-diagonal G^R block against the reference CPU RGF on the
+same seeded input. Config 1 runs at full size (also against the dense oracle);
+configs 2/3 at reduced layer / energy counts with their true b, w and eta
+(full-size checks live in tests/test_gpu_dyson_full.py).
+"""
+import numpy as np
+import pytest
+
+from oracle import bbsi_oracle as O
+from oracle import dyson_oracle as DO
+from paper_2605_19910_b200 import dyson as D
+
+pytestmark = pytest.mark.gpu
+TOL = 1e-10
+
+
+def _run_gpu(cfg):
+    import torch
+
+    l, w, b = cfg.num_layers, cfg.bandwidth, cfg.block_size
+    H = torch.empty((l, 2 * w + 1, b, b), dtype=torch.complex128, device="cuda")
+    D.fill_h_device(cfg, H)
+    G = torch.empty((cfg.n_energy, l, 2 * w + 1, b, b), dtype=torch.complex128, device="cuda")
+    fails = D.solve_device(cfg, H, G)
+    assert (fails == -1).all()
+    torch.cuda.synchronize()
+    return np.swapaxes(G.cpu().numpy(), -1, -2)  # slot memory -> (row, col)
+
+
+def _oracle_band(cfg, e):
+    h = DO.hamiltonian(cfg.num_layers, cfg.bandwidth, cfg.block_size, cfg.seed)
+    return DO.dyson_matrix(h, complex(cfg.z()[e]), cfg.sigma_layers)
+
+
+def _check(cfg, dense=False, energies=None):
+    g = _run_gpu(cfg)
+    lay = O.make_layout(cfg.num_layers, cfg.block_size, cfg.bandwidth)
+    worst = 0.0
+    for e in energies if energies is not None else range(cfg.n_energy):
+        a = _oracle_band(cfg, e)
+        ref = O.rgf_ndiag(a)[0] if cfg.bandwidth > 1 else O.rgf_tridiag(a)[0]
+        got = O.Band(lay, g[e])
+        err = O.max_block_error(got, ref)
+        worst = max(worst, err)
+        assert err <= TOL, (e, err)
+        if dense:
+            assert O.max_block_error(got, O.oracle_selected_inverse(a)) <= TOL
+    return worst
+
+
+def test_config1_full_size_vs_rgf_and_dense(gpu):
+    _check(D.CONFIGS[1], dense=True)
+
+
+def test_config2_proxy(gpu):
+    _check(D.scaled(D.CONFIGS[2], num_layers=24, n_energy=4))
+
+
+def test_config3_proxy(gpu):
+    _check(D.scaled(D.CONFIGS[3], num_layers=24, n_energy=4))
+
+
+def test_config5_block_size_proxy(gpu):
+    _check(D.scaled(D.CONFIGS[5], num_layers=6, n_energy=2))

@@ -1,0 +1,141 @@
+"""GPU parity of rgf_tridiag / rgf_ndiag / rgf_fused through the C ABI.
+
+Each case restates a reference test (tests/test_rgf.cpp) with the same seeds,
+sizes and tolerances; the checker is the compiled reference (oracle/_ref) when
+present, else the numpy restatement (oracle/bbsi_oracle.py), plus the dense
+oracle (block_banded.hpp:175-181).
+"""
+import numpy as np
+import pytest
+
+import paper_2605_19910_b200 as P
+from oracle import bbsi_oracle as O
+from tests._util import max_err, to_oracle, to_product
+
+pytestmark = pytest.mark.gpu
+
+
+def test_second_difference_known_answer(gpu):
+    """test_rgf.cpp:10-25 (real input promoted to complex128)."""
+    m = O.Band(O.make_layout(3, 1, 1))
+    for i in range(3):
+        m.block(i, 0)[0, 0] = 2
+        if i > 0:
+            m.block(i, -1)[0, 0] = -1
+        if i < 2:
+            m.block(i, 1)[0, 0] = -1
+    g, c = P.rgf_tridiag(to_product(m))
+    assert abs(g.block(0, 0)[0, 0] - 0.75) <= 1e-14
+    assert abs(g.block(1, 0)[0, 0] - 1.0) <= 1e-14
+    assert abs(g.block(2, 0)[0, 0] - 0.75) <= 1e-14
+    assert abs(g.block(0, 1)[0, 0] - 0.5) <= 1e-14
+    assert abs(g.block(1, 1)[0, 0] - 0.5) <= 1e-14
+    assert c.as_tuple() == (8, 3, 7)
+
+
+def test_single_layer(gpu):
+    """test_rgf.cpp:27-32"""
+    m = O.random_spd_like(O.make_layout(1, 4, 0), 3, 2.0)
+    g, c = P.rgf_tridiag(to_product(m))
+    assert max_err(g, O.oracle_selected_inverse(m)) <= 1e-13
+    assert c.as_tuple() == O.predict_rgf_counters(1).as_tuple()
+
+
+def test_tridiag_matches_oracle_with_counters(gpu):
+    """test_rgf.cpp:34-40"""
+    m = O.random_spd_like(O.make_layout(12, 8, 1), 77, 2.0)
+    g, c = P.rgf_tridiag(to_product(m))
+    assert max_err(g, O.oracle_selected_inverse(m)) <= 1e-10
+    assert max_err(g, O.rgf_tridiag(m)[0]) <= 1e-12
+    assert c.as_tuple() == (44, 12, 34)
+
+
+def test_ragged_block_sizes(gpu):
+    """test_rgf.cpp:42-48"""
+    m = O.random_spd_like(O.BlockLayout(5, [3, 1, 4, 2, 3], 1), 8, 2.0)
+    g, c = P.rgf_tridiag(to_product(m))
+    assert max_err(g, O.oracle_selected_inverse(m)) <= 1e-10
+    assert c.as_tuple() == O.predict_rgf_counters(5).as_tuple()
+
+
+def test_ndiag_reduces_to_tridiag(gpu):
+    """test_rgf.cpp:50-56 (identical kernel sequence on the GPU path -> bit-identical)."""
+    m = to_product(O.random_spd_like(O.make_layout(9, 4, 1), 13, 2.0))
+    g1, c1 = P.rgf_tridiag(m)
+    gn, cn = P.rgf_ndiag(m)
+    assert np.array_equal(g1.data, gn.data)
+    assert c1 == cn
+
+
+@pytest.mark.parametrize("w", [2, 3])
+def test_ndiag_matches_oracle(gpu, w):
+    """test_rgf.cpp:58-67"""
+    m = O.random_spd_like(O.make_layout(10, 4, w), 100 + w, 2.0)
+    trace = {}
+    g, c = P.rgf_ndiag(to_product(m), trace)
+    assert max_err(g, O.oracle_selected_inverse(m)) <= 1e-10
+    assert trace["max_update_offset"] <= w - 1
+    assert c.as_tuple() == O.predict_nrgf_counters(10, w).as_tuple()
+
+
+def test_ndiag_counters_closed_form(gpu):
+    """test_rgf.cpp:69-77 (plus parity on every case)."""
+    for w in range(1, 4):
+        for l in range(w + 1, 13):
+            m = O.random_spd_like(O.make_layout(l, 2, w), l * 10 + w, 2.0)
+            g, c = P.rgf_ndiag(to_product(m))
+            assert c.as_tuple() == O.predict_nrgf_counters(l, w).as_tuple()
+            assert max_err(g, O.rgf_ndiag(m)[0]) <= 1e-10
+
+
+def test_fused_agrees_with_ndiag(gpu):
+    """test_rgf.cpp:79-88"""
+    m = O.random_spd_like(O.make_layout(9, 3, 2), 55, 2.0)
+    gf, cf = P.rgf_fused(to_product(m))
+    assert max_err(gf, O.rgf_ndiag(m)[0]) <= 1e-10
+    assert cf.as_tuple() == (16, 5, 13)
+
+
+def test_fused_short_last_superblock(gpu):
+    """test_rgf.cpp:90-95"""
+    m = O.random_spd_like(O.make_layout(10, 2, 3), 56, 2.0)
+    gf, cf = P.rgf_fused(to_product(m))
+    assert max_err(gf, O.oracle_selected_inverse(m)) <= 1e-10
+    assert cf.as_tuple() == O.predict_rgf_counters(4).as_tuple()
+
+
+def test_hermitian_input_gives_hermitian_inverse(gpu):
+    """test_rgf.cpp:150-160"""
+    h1 = O.random_hermitian(O.make_layout(8, 3, 1), 31, 1.0)
+    g1, _ = P.rgf_tridiag(to_product(h1))
+    assert O.hermitian_defect(to_oracle(g1)) <= 1e-12
+    h2 = O.random_hermitian(O.make_layout(8, 3, 2), 32, 1.0)
+    g2, _ = P.rgf_ndiag(to_product(h2))
+    assert O.hermitian_defect(to_oracle(g2)) <= 1e-12
+
+
+def test_singular_pivot_attribution(gpu):
+    """test_rgf.cpp:162-171"""
+    m = O.random_spd_like(O.make_layout(5, 2, 1), 40, 2.0)
+    m.block(4, 0)[...] = 0
+    with pytest.raises(P.SingularMatrixError) as ei:
+        P.rgf_tridiag(to_product(m))
+    assert ei.value.layer == 4
+
+
+def test_wrong_bandwidth_rejected(gpu):
+    """test_rgf.cpp:173-179"""
+    wide = to_product(O.random_spd_like(O.make_layout(6, 2, 2), 41, 2.0))
+    with pytest.raises(P.InvalidArgumentError):
+        P.rgf_tridiag(wide)
+    ragged = to_product(O.random_spd_like(O.BlockLayout(4, [2, 3, 2, 3], 2), 42, 2.0))
+    with pytest.raises(P.InvalidArgumentError):
+        P.rgf_fused(ragged)
+
+
+@pytest.mark.parametrize("l,b,w", [(6, 64, 1), (7, 128, 1), (9, 64, 2), (5, 192, 2), (4, 96, 3)])
+def test_padded_and_native_block_sizes(gpu, l, b, w):
+    """Block sizes on and off the 64-wide tile grid, diagonally dominant inputs."""
+    m = O.random_spd_like(O.make_layout(l, b, w), 1000 + l + b + w, 2.0)
+    g, _ = P.rgf_ndiag(to_product(m))
+    assert max_err(g, O.rgf_ndiag(m)[0]) <= 1e-12
