@@ -1,0 +1,355 @@
+#!/usr/bin/env python
+"""Benchmark: batched selected inversion of the BASELINE Dyson matrices on B200.
+
+Workload (N=1 default): BASELINE.json configs[1] -- block-tridiagonal RGF, N_b=256,
+b=256, complex128, 64 energies in [-1.5, 1.5], eta=1e-4, seed 1 (synthetic, seeded;
+BASELINE names no dataset). A "step" is the selected inversion of all 64 energies
+(diagonal + off-diagonal G^R blocks). Energies shard contiguously across ranks
+(strong scaling, no data-path collective).
+
+  python bench.py [--gpus N] [--steps K] [--warmup W] [--config 2] [--impl ours|reference]
+
+Prints ONE JSON line (rank 0). Keys beyond the driver contract:
+  roofline      dominant kernel (the DMMA GEMM) vs the FP64 DMMA peak measured live
+  cpu_baseline  compiled reference rgf_tridiag (oracle/_ref) on a bounded sample, host cores
+  e2e           same metric through the host-buffer C ABI (H2D of H, D2H of every G band)
+"""
+from __future__ import annotations
+
+import argparse
+import ctypes as C
+import json
+import os
+import statistics
+import subprocess
+import sys
+import threading
+import time
+from pathlib import Path
+
+import numpy as np
+
+ROOT = Path(__file__).resolve().parent
+sys.path.insert(0, str(ROOT))
+
+METRIC = "selected inversions/s (energy pts x blocks / s)"
+UNIT = "energy_pts*blocks/s"
+
+
+def parse():
+    p = argparse.ArgumentParser()
+    p.add_argument("--gpus", type=int, default=1)
+    p.add_argument("--steps", type=int, default=3)
+    p.add_argument("--warmup", type=int, default=3)
+    p.add_argument("--config", type=int, default=2)
+    p.add_argument("--impl", default="ours", choices=["ours", "reference"])
+    p.add_argument("--no-e2e", action="store_true")
+    p.add_argument("--no-cpu-baseline", action="store_true")
+    p.add_argument("--chunk", type=int, default=0, help="energy chunk of the e2e path (0 = n/4)")
+    return p.parse_args()
+
+
+# ---------------------------------------------------------------------------- clocks
+class ClockSampler:
+    """nvidia-smi clocks + throttle reasons sampled every 200 ms during the timed region."""
+
+    Q = ("clocks.sm,clocks.max.sm,clocks_event_reasons.hw_slowdown,clocks_event_reasons.hw_thermal_slowdown,"
+         "clocks_event_reasons.sw_thermal_slowdown,clocks_event_reasons.sw_power_cap")
+
+    def __init__(self, index: int):
+        self.index = index
+        self.rows = []
+        self._stop = threading.Event()
+        self._t = None
+
+    def _run(self):
+        while not self._stop.is_set():
+            try:
+                out = subprocess.run(["nvidia-smi", "-i", str(self.index), f"--query-gpu={self.Q}",
+                                      "--format=csv,noheader,nounits"], capture_output=True, text=True,
+                                     timeout=5).stdout.strip()
+                if out:
+                    self.rows.append([x.strip() for x in out.split(",")])
+            except Exception:
+                pass
+            self._stop.wait(0.2)
+
+    def __enter__(self):
+        self._t = threading.Thread(target=self._run, daemon=True)
+        self._t.start()
+        return self
+
+    def __exit__(self, *a):
+        self._stop.set()
+        self._t.join(timeout=10)
+
+    def summary(self):
+        if not self.rows:
+            return {"sm_mhz": None, "sm_max_mhz": None, "reasons": ["nvidia-smi unavailable"]}
+        sm = [float(r[0]) for r in self.rows if r[0].replace(".", "").isdigit()]
+        mx = [float(r[1]) for r in self.rows if r[1].replace(".", "").isdigit()]
+        names = ["hw_slowdown", "hw_thermal_slowdown", "sw_thermal_slowdown", "sw_power_cap"]
+        reasons = sorted({names[i] for r in self.rows for i in range(4) if len(r) > 2 + i and "Active" in r[2 + i]
+                          and "Not" not in r[2 + i]})
+        return {"sm_mhz": statistics.median(sm) if sm else None, "sm_max_mhz": max(mx) if mx else None,
+                "reasons": reasons, "samples": len(self.rows)}
+
+
+# ---------------------------------------------------------------------------- CPU reference
+def cpu_reference(cfg, n_energies: int, threads_per_energy: int, nproc: int):
+    """Times the compiled, unmodified reference rgf_tridiag / rgf_ndiag (oracle/_ref) on
+    n_energies energies of cfg, each with threads_per_energy BLAS threads, run
+    concurrently on host threads. Returns (seconds, energies)."""
+    from oracle import ref_lib as R
+    from paper_2605_19910_b200 import dyson as D
+
+    L = R.lib()
+    l, w, b = cfg.num_layers, cfg.bandwidth, cfg.block_size
+    h = D.fill_h_host(cfg)  # slot memory [a, off, col, row]
+    zs = cfg.z()
+    sig = cfg.sigma()
+    idx = np.arange(b)
+    fn = L.ref_rgf_tridiag if w == 1 else L.ref_rgf_ndiag
+    L.ref_set_threads(C.c_int(threads_per_energy))
+    inputs = []
+    for e in range(n_energies):
+        a = -h
+        z = zs[e % len(zs)]
+        for layer in range(l):
+            d = a[layer, w]
+            hd = h[layer, w][idx, idx]
+            d[idx, idx] = ((z.real - hd.real) - sig[layer].real) + 1j * ((z.imag - hd.imag) - sig[layer].imag)
+        inputs.append(a)
+    outs = [np.empty_like(h) for _ in range(n_energies)]
+    errs = []
+
+    def run(e):
+        fail = C.c_int(-1)
+        args = [l, w, b, None, inputs[e].ctypes.data_as(C.c_void_p), outs[e].ctypes.data_as(C.c_void_p), None]
+        if w != 1:
+            args.append(None)
+        rc = fn(*args, C.byref(fail))
+        if rc != 0:
+            errs.append(rc)
+
+    t0 = time.perf_counter()
+    ths = [threading.Thread(target=run, args=(e,)) for e in range(n_energies)]
+    for t in ths:
+        t.start()
+    for t in ths:
+        t.join()
+    dt = time.perf_counter() - t0
+    if errs:
+        raise RuntimeError(f"reference solve failed: {errs}")
+    return dt, n_energies
+
+
+def cpu_baseline_block(cfg, nproc: int):
+    """Best of (i) energy-parallel, 1 BLAS thread per energy and (ii) one energy with
+    nproc BLAS threads."""
+    n_par = nproc
+    t_par, e_par = cpu_reference(cfg, n_par, 1, nproc)
+    t_one, e_one = cpu_reference(cfg, 1, nproc, nproc)
+    r_par, r_one = e_par / t_par, e_one / t_one
+    if r_par >= r_one:
+        rate, sample, cores = r_par, f"{e_par} energies of {cfg.name}, one per host thread, 1 BLAS thread each", n_par
+    else:
+        rate, sample, cores = r_one, f"1 energy of {cfg.name}, {nproc} BLAS threads", nproc
+    return {"value": rate * cfg.num_layers, "unit": UNIT, "cores": cores, "kind": "reference",
+            "sample": sample, "seconds": {"energy_parallel": round(t_par, 3), "threaded_blas": round(t_one, 3)},
+            "energies_per_s": rate}
+
+
+# ---------------------------------------------------------------------------- reference arm
+def run_reference(args, rank, world):
+    from paper_2605_19910_b200 import dyson as D
+
+    if rank != 0:
+        return
+    cfg = D.CONFIGS[args.config]
+    nproc = os.cpu_count() or 1
+    for _ in range(args.warmup):
+        cpu_reference(cfg, nproc, 1, nproc)
+    times = []
+    for _ in range(args.steps):
+        dt, ne = cpu_reference(cfg, nproc, 1, nproc)
+        times.append(dt)
+    tot = sum(times)
+    value = args.steps * nproc * cfg.num_layers / tot
+    line = {"impl": "reference", "metric": METRIC, "value": value, "unit": UNIT, "n_gpus": args.gpus,
+            "steps": args.steps, "warmup": args.warmup, "ms_per_step": 1e3 * tot / args.steps,
+            "higher_is_better": True, "scaling": "strong", "vs_baseline": None, "dtype": "c128 (f64)",
+            "data": "synthetic (seeded Dyson generator, csrc/dyson_gen.h)",
+            "config": {"workload": cfg.name, "num_layers": cfg.num_layers, "block_size": cfg.block_size,
+                       "bandwidth": cfg.bandwidth, "energies": cfg.n_energy, "eta": cfg.eta, "seed": cfg.seed,
+                       "solver": "reference rgf_tridiag (oracle/_ref, OpenBLAS 0.3.15)"},
+            "cpu_baseline": {"value": value, "unit": UNIT, "cores": nproc, "kind": "reference",
+                             "sample": f"{nproc} energies of {cfg.name} per step, one per host thread, 1 BLAS "
+                                       f"thread each"},
+            "e2e": {"value": value, "unit": UNIT, "h2d_bytes_per_step": 0, "d2h_bytes_per_step": 0}}
+    print(json.dumps(line), flush=True)
+
+
+# ---------------------------------------------------------------------------- our arm
+def run_ours(args, rank, world, local_rank):
+    import torch
+    import torch.distributed as dist
+
+    from paper_2605_19910_b200 import dyson as D
+    from paper_2605_19910_b200._native import lib
+
+    L = lib()
+    dev = torch.device("cuda", local_rank)
+    torch.cuda.set_device(dev)
+    cfg = D.CONFIGS[args.config]
+    l, w, b = cfg.num_layers, cfg.bandwidth, cfg.block_size
+    zs_all = cfg.z()
+    n_all = len(zs_all)
+    lo, hi = rank * n_all // world, (rank + 1) * n_all // world
+    zs = zs_all[lo:hi]
+    n_loc = len(zs)
+
+    H = torch.empty((l, 2 * w + 1, b, b), dtype=torch.complex128, device=dev)
+    D.fill_h_device(cfg, H)
+    G = torch.empty((n_loc, l, 2 * w + 1, b, b), dtype=torch.complex128, device=dev)
+    stream = torch.cuda.current_stream()
+
+    def step():
+        D.solve_device(cfg, H, G, z=zs, stream=stream)
+
+    def barrier():
+        if world > 1:
+            dist.barrier()
+
+    for _ in range(max(3, args.warmup)):
+        step()
+    torch.cuda.synchronize()
+    barrier()
+    torch.cuda.synchronize()
+    n0 = L.bbsi_cuda_launch_count()
+    e0, e1 = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
+    with ClockSampler(local_rank) as clocks:
+        e0.record(stream)
+        for _ in range(args.steps):
+            step()
+        e1.record(stream)
+        torch.cuda.synchronize()
+    barrier()
+    ms = e0.elapsed_time(e1)
+    launches = L.bbsi_cuda_launch_count() - n0
+    ms_max = ms
+    if world > 1:
+        t = torch.tensor([ms], device=dev, dtype=torch.float64)
+        dist.all_reduce(t, op=dist.ReduceOp.MAX)
+        ms_max = float(t.item())
+    ms_step = ms_max / args.steps
+    value = n_all * l / (ms_step * 1e-3)
+    flops_energy = D.algorithmic_flops(cfg)
+    tflops = n_all * flops_energy / (ms_step * 1e-3) / 1e12
+
+    # ---- per-kernel breakdown of one step (CUDA events around every library launch)
+    L.bbsi_cuda_profile_enable(1)
+    step()
+    torch.cuda.synchronize()
+    L.bbsi_cuda_profile_enable(0)
+    prof = np.zeros(12)
+    L.bbsi_cuda_profile_collect(prof.ctypes.data_as(C.c_void_p), 3)
+    cats = {}
+    for i, name in enumerate(["zgemm_dmma", "zinv_gj", "band_ops"]):
+        cnt, tms, fl, by = prof[4 * i: 4 * i + 4]
+        cats[name] = {"launches": int(cnt), "ms": round(tms, 3),
+                      "tflops": round(fl / (tms * 1e-3) / 1e12, 3) if tms > 0 else None,
+                      "gbs": round(by / (tms * 1e-3) / 1e9, 1) if tms > 0 else None}
+    peak = L.bbsi_cuda_fp64_peak_tflops(50.0, 5)
+    g = cats["zgemm_dmma"]
+    step_kernel_ms = sum(c["ms"] for c in cats.values())
+    roofline = {"bound": "tensor", "kernel": "zgemm_grouped_kernel (DMMA f64)", "achieved": g["tflops"],
+                "peak": round(peak, 2), "unit": "TFLOP/s", "frac": round(g["tflops"] / peak, 4) if peak > 0 else None,
+                "traffic": None,
+                "peak_source": "FP64 DMMA peak measured live in this run (bbsi_cuda_fp64_peak_tflops; "
+                               "MEASURED_PEAKS.json has no FP64 entry)",
+                "share_of_step": round(g["ms"] / step_kernel_ms, 3) if step_kernel_ms else None,
+                "step_algorithmic_tflops": round(tflops / world, 3),
+                "step_frac_of_peak": round(tflops / world / peak, 4) if peak > 0 else None,
+                "kernels": cats}
+
+    # ---- end to end through the host-buffer C ABI
+    e2e = None
+    if not args.no_e2e:
+        band = l * (2 * w + 1) * b * b
+        Hh = torch.from_numpy(D.fill_h_host(cfg)).pin_memory()
+        Gh = torch.empty((n_loc, l, 2 * w + 1, b, b), dtype=torch.complex128).pin_memory()
+        zz = np.ascontiguousarray(zs, dtype=np.complex128)
+        sig = cfg.sigma()
+        fails = np.zeros(n_loc, dtype=np.int32)
+
+        def e2e_step():
+            rc = L.bbsi_cuda_dyson_rgf_z(l, w, b, n_loc, C.c_void_p(Hh.data_ptr()), zz.ctypes.data_as(C.c_void_p),
+                                         sig.ctypes.data_as(C.c_void_p), C.c_void_p(Gh.data_ptr()),
+                                         fails.ctypes.data_as(C.c_void_p), args.chunk)
+            if rc != 0:
+                raise RuntimeError(L.bbsi_cuda_last_error().decode())
+
+        e2e_step()
+        torch.cuda.synchronize()
+        barrier()
+        t0 = time.perf_counter()
+        for _ in range(args.steps):
+            e2e_step()
+        torch.cuda.synchronize()
+        dt = (time.perf_counter() - t0) / args.steps
+        if world > 1:
+            t = torch.tensor([dt], device=dev, dtype=torch.float64)
+            dist.all_reduce(t, op=dist.ReduceOp.MAX)
+            dt = float(t.item())
+        e2e = {"value": n_all * l / dt, "unit": UNIT, "ms_per_step": round(dt * 1e3, 2),
+               "h2d_bytes_per_step": int(16 * band + 16 * n_loc + 16 * l) * world,
+               "d2h_bytes_per_step": int(16 * band * n_loc + 4 * n_loc) * world,
+               "path": "bbsi_cuda_dyson_rgf_z (host H in, every G band out, pinned host memory)"}
+        del Hh, Gh
+
+    cpu = None
+    if rank == 0 and world == 1 and not args.no_cpu_baseline:
+        try:
+            cpu = cpu_baseline_block(cfg, os.cpu_count() or 1)
+        except Exception as ex:  # the GPU number stands without it
+            cpu = {"error": str(ex)}
+
+    if rank == 0:
+        line = {"metric": METRIC, "value": value, "unit": UNIT, "n_gpus": world, "steps": args.steps,
+                "warmup": max(3, args.warmup), "ms_per_step": ms_step, "higher_is_better": True, "scaling": "strong",
+                "vs_baseline": None, "dtype": "c128 (f64)", "data": "synthetic (seeded Dyson generator, "
+                "csrc/dyson_gen.h)",
+                "config": {"workload": cfg.name, "num_layers": l, "block_size": b, "bandwidth": w,
+                           "energies": n_all, "eta": cfg.eta, "seed": cfg.seed, "solver": "rgf (batched sweeps)",
+                           "parallelism": f"energy shards x{world}", "l2": "inputs larger than L2 (G band "
+                           f"{16 * l * (2 * w + 1) * b * b * n_all / 2**30:.1f} GiB)"},
+                "energies_per_s": n_all / (ms_step * 1e-3), "tflops_algorithmic": tflops,
+                "gpu_launches": int(launches), "clocks": clocks.summary(), "roofline": roofline,
+                "e2e": e2e, "cpu_baseline": cpu}
+        print(json.dumps(line), flush=True)
+
+
+def main():
+    args = parse()
+    world = int(os.environ.get("WORLD_SIZE", "1"))
+    rank = int(os.environ.get("RANK", "0"))
+    local_rank = int(os.environ.get("LOCAL_RANK", "0"))
+    if args.impl == "reference":
+        run_reference(args, rank, world)
+        return
+    if world > 1:
+        import torch
+        import torch.distributed as dist
+
+        torch.cuda.set_device(local_rank)
+        dist.init_process_group("nccl", device_id=torch.device("cuda", local_rank))
+    run_ours(args, rank, world, local_rank)
+    if world > 1:
+        import torch.distributed as dist
+
+        dist.destroy_process_group()
+
+
+if __name__ == "__main__":
+    main()

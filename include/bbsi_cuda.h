@@ -98,6 +98,12 @@ int bbsi_cuda_rgf_batched_dev(int l, int w, int bs, int batch, const double* dA,
 int bbsi_cuda_dyson_rgf_dev(int l, int w, int bs, int n_energy, const double* dH, const double* z,
                             const double* sigma, double* dG, int* fail_layers, void* stream);
 
+/* Same solve end to end from HOST buffers (the drop-in form): H host [l][2w+1][bs][bs],
+ * G host [n_energy][l][2w+1][bs][bs]. Energies run in chunks of `chunk` (<= 0: n/4);
+ * finished chunks stream back to G while the next computes (pin G for overlap). */
+int bbsi_cuda_dyson_rgf_z(int l, int w, int bs, int n_energy, const double* H, const double* z,
+                          const double* sigma, double* G, int* fail_layers, int chunk);
+
 /* Seeded Dyson Hamiltonian (include/.. csrc/dyson_gen.h spec) written on the device. */
 int bbsi_cuda_dyson_fill_h_dev(int l, int w, int b, uint64_t seed, double* dH, void* stream);
 /* Same bytes on the host (for the end-to-end path and the parity tests). */
@@ -114,6 +120,18 @@ int bbsi_cuda_zgemm_dev(int m, int n, int k, const double* alpha, const double* 
  * the leading n_true x n_true block; status_host[batch] = -1 or first bad pivot. */
 int bbsi_cuda_zinv_dev(int n, int n_true, int batch, double* dM, long long ld, long long bstride,
                        int* status_host, void* stream);
+
+/* ---------------------------------------------------------------- instrumentation
+ * Number of library kernel launches since load (all entry points). */
+long long bbsi_cuda_launch_count(void);
+/* When enabled, every library kernel launch is bracketed by CUDA events on its
+ * stream; collect() synchronises and returns, per category (0 GEMM, 1 inversion,
+ * 2 band ops), {launches, total ms, algorithmic FLOPs, algorithmic bytes} and
+ * clears the records. */
+void bbsi_cuda_profile_enable(int on);
+int bbsi_cuda_profile_collect(double* out, int ncat);
+/* Measured FP64 DMMA (mma.sync f64) peak of device 0 in TFLOP/s (best of reps). */
+double bbsi_cuda_fp64_peak_tflops(double duration_ms, int reps);
 
 #ifdef __cplusplus
 }

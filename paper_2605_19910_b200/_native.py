@@ -28,6 +28,11 @@ SIGNATURES = {
     "bbsi_dyson_fill_h_host": (None, [_i, _i, _i, C.c_uint64, _vp]),
     "bbsi_cuda_zgemm_dev": (_i, [_i, _i, _i, _vp, _vp, _ll, _ll, _vp, _ll, _ll, _vp, _vp, _ll, _ll, _i, _vp]),
     "bbsi_cuda_zinv_dev": (_i, [_i, _i, _i, _vp, _ll, _ll, _vp, _vp]),
+    "bbsi_cuda_dyson_rgf_z": (_i, [_i, _i, _i, _i, _vp, _vp, _vp, _vp, _vp, _i]),
+    "bbsi_cuda_launch_count": (_ll, []),
+    "bbsi_cuda_profile_enable": (None, [_i]),
+    "bbsi_cuda_profile_collect": (_i, [_vp, _i]),
+    "bbsi_cuda_fp64_peak_tflops": (_d, [_d, _i]),
 }
 
 _lib = None

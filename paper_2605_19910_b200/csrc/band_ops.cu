@@ -1,7 +1,7 @@
 // Band-level elementwise kernels: Dyson-matrix synthesis on the device and the
 // formation of the per-energy working band A(E) = z I - H - Sigma from a shared H.
 #include "dyson_gen.h"
-#include "zcommon.cuh"
+#include "internal.h"
 
 namespace bbsi_gpu {
 
@@ -61,6 +61,7 @@ int grid_for(long long n, int threads) {
 
 cudaError_t dyson_fill_h(double2* H, int l, int w, int b, uint64_t seed, cudaStream_t s) {
   long long total = (long long)l * (2 * w + 1) * b * b;
+  ProfScope prof(s, PROF_BAND, 0.0, 16.0 * total);
   dyson_fill_h_kernel<<<grid_for(total, 256), 256, 0, s>>>(H, l, w, b, bbsi_mix64(seed));
   return cudaGetLastError();
 }
@@ -68,6 +69,7 @@ cudaError_t dyson_fill_h(double2* H, int l, int w, int b, uint64_t seed, cudaStr
 cudaError_t dyson_form_band(double2* G, const double2* H, int l, int w, int bs, int batch, const double2* z,
                             const double2* sigma, cudaStream_t s) {
   long long total = (long long)l * (2 * w + 1) * bs * bs * batch;
+  ProfScope prof(s, PROF_BAND, 0.0, 16.0 * (total + (long long)l * (2 * w + 1) * bs * bs));
   dyson_form_band_kernel<<<grid_for(total, 256), 256, 0, s>>>(G, H, l, w, bs, batch, z, sigma);
   return cudaGetLastError();
 }

@@ -383,6 +383,108 @@ int bbsi_cuda_zinv_dev(int n, int n_true, int batch, double* dM, long long ld, l
   return BBSI_OK;
 }
 
+long long bbsi_cuda_launch_count(void) { return launch_count(); }
+
+void bbsi_cuda_profile_enable(int on) { prof_enable(on != 0); }
+
+int bbsi_cuda_profile_collect(double* out, int ncat) {
+  if (!out || ncat < 1) return fail(BBSI_INVALID_ARGUMENT, "profile_collect: bad output buffer");
+  return prof_collect(out, ncat);
+}
+
+double bbsi_cuda_fp64_peak_tflops(double duration_ms, int reps) {
+  if (device_ok()) return -1.0;
+  return fp64_dmma_peak(duration_ms, reps < 1 ? 1 : reps);
+}
+
+// End-to-end Dyson batch from HOST buffers: H2D of H, energy chunks computed on
+// one stream while the finished chunks' G bands stream back to the host on a
+// second stream (pinned G_host gives full overlap).
+int bbsi_cuda_dyson_rgf_z(int l, int w, int bs, int n_energy, const double* H, const double* z, const double* sigma,
+                          double* G, int* fail_layers, int chunk) {
+  if (int rc = validate_layout(l, w, bs, nullptr)) return rc;
+  if (bs % 64) return fail(BBSI_INVALID_ARGUMENT, "Dyson batch requires bs % 64 == 0");
+  if (w < 1 && l != 1) return fail(BBSI_INVALID_ARGUMENT, "rgf_ndiag: requires bandwidth >= 1");
+  if (n_energy < 1) return fail(BBSI_INVALID_ARGUMENT, "n_energy must be >= 1");
+  if (int rc = device_ok()) return rc;
+  std::lock_guard<std::mutex> lk(g_call_mu);
+  if (chunk <= 0) chunk = (n_energy + 3) / 4;
+  if (chunk > n_energy) chunk = n_energy;
+  const int nchunk = (n_energy + chunk - 1) / chunk;
+  const long long band = (long long)l * (2 * w + 1) * bs * bs;
+  const size_t band_b = size_t(band) * sizeof(double2);
+  const size_t scr_b = sweep_scratch_bytes(l, w, bs, chunk);
+  size_t free_b = 0, total_b = 0;
+  CK(cudaMemGetInfo(&free_b, &total_b));
+  int nbuf = nchunk;
+  while (nbuf > 2 && (size_t(nbuf) * chunk * band_b + band_b + scr_b) > free_b * 9 / 10) --nbuf;
+  double2* dH = static_cast<double2*>(arena_get(4, band_b));
+  double2* dG = static_cast<double2*>(arena_get(5, size_t(nbuf) * chunk * band_b));
+  double2* dzs = static_cast<double2*>(arena_get(2, sizeof(double2) * (size_t(n_energy) + l)));
+  void* scratch = arena_get(1, scr_b);
+  if (!dH || !dG || !dzs || !scratch) return fail(BBSI_OUT_OF_MEMORY, "Dyson batch workspace allocation failed");
+  cudaStream_t sc = nullptr, sd = nullptr;
+  CK(cudaStreamCreateWithFlags(&sc, cudaStreamNonBlocking));
+  CK(cudaStreamCreateWithFlags(&sd, cudaStreamNonBlocking));
+  std::vector<cudaEvent_t> done(nchunk), freed(nbuf);
+  for (auto& e : done) CK(cudaEventCreateWithFlags(&e, cudaEventDisableTiming));
+  for (auto& e : freed) CK(cudaEventCreateWithFlags(&e, cudaEventDisableTiming));
+  std::vector<int> status(size_t(l) * n_energy, -1);
+  int rc = BBSI_OK;
+  auto body = [&]() -> int {
+    CK(cudaMemcpyAsync(dH, H, band_b, cudaMemcpyHostToDevice, sc));
+    CK(cudaMemcpyAsync(dzs, z, sizeof(double2) * n_energy, cudaMemcpyHostToDevice, sc));
+    CK(cudaMemcpyAsync(dzs + n_energy, sigma, sizeof(double2) * l, cudaMemcpyHostToDevice, sc));
+    std::vector<int> nt(l, bs);
+    for (int c = 0; c < nchunk; ++c) {
+      const int e0 = c * chunk, ne = std::min(chunk, n_energy - e0), buf = c % nbuf;
+      if (c >= nbuf) CK(cudaStreamWaitEvent(sc, freed[buf], 0));
+      double2* g = dG + size_t(buf) * chunk * band;
+      CK(dyson_form_band(g, dH, l, w, bs, ne, dzs + e0, dzs + n_energy, sc));
+      SweepWork W;
+      W.l = l;
+      W.w = w;
+      W.bs = bs;
+      W.batch = ne;
+      W.G = g;
+      W.g_bstride = band;
+      sweep_carve(W, scratch);
+      CK(rgf_sweeps(W, nt.data(), sc));
+      // status rows [layer][ne] of this chunk -> host (pageable; tiny)
+      std::vector<int> st(size_t(l) * ne);
+      CK(cudaMemcpyAsync(st.data(), W.status, st.size() * sizeof(int), cudaMemcpyDeviceToHost, sc));
+      CK(cudaEventRecord(done[c], sc));
+      CK(cudaStreamWaitEvent(sd, done[c], 0));
+      CK(cudaMemcpyAsync(G + 2 * size_t(e0) * band, g, size_t(ne) * band_b, cudaMemcpyDeviceToHost, sd));
+      CK(cudaEventRecord(freed[buf], sd));
+      CK(cudaEventSynchronize(done[c]));  // st is filled (pageable copy); keeps the host one chunk ahead
+      for (int j = 0; j < l; ++j)
+        for (int e = 0; e < ne; ++e) status[size_t(j) * n_energy + e0 + e] = st[size_t(j) * ne + e];
+    }
+    CK(cudaStreamSynchronize(sd));
+    CK(cudaStreamSynchronize(sc));
+    return BBSI_OK;
+  };
+  rc = body();
+  for (auto& e : done) cudaEventDestroy(e);
+  for (auto& e : freed) cudaEventDestroy(e);
+  cudaStreamDestroy(sc);
+  cudaStreamDestroy(sd);
+  if (rc) return rc;
+  bool bad = false;
+  for (int e = 0; e < n_energy; ++e) {
+    int f = -1;
+    for (int j = l - 1; j >= 0; --j)
+      if (status[size_t(j) * n_energy + e] >= 0) {
+        f = j;
+        break;
+      }
+    if (fail_layers) fail_layers[e] = f;
+    bad |= f >= 0;
+  }
+  return bad ? fail(BBSI_SINGULAR, "singular Schur pivot in at least one energy") : BBSI_OK;
+}
+
 int bbsi_cuda_rgf_extended_z(int, int, int, const int*, const double*, double*, double*, double*, double*, double*,
                              long long*, int*) {
   return fail(BBSI_INVALID_ARGUMENT, "rgf_extended: not yet available on the GPU path");

@@ -53,6 +53,25 @@ cudaError_t rgf_sweeps(const SweepWork& W, const int* n_true, cudaStream_t s);
 // reference would report (first failure in elimination order) or -1.
 cudaError_t collect_failures(const SweepWork& W, std::vector<int>& fail, cudaStream_t s);
 
+// Launch accounting / optional event timing around one kernel launch (prof.cu).
+enum ProfCat { PROF_GEMM = 0, PROF_INV = 1, PROF_BAND = 2, PROF_NCAT = 3 };
+class ProfScope {
+ public:
+  ProfScope(cudaStream_t s, int cat, double flops, double bytes);
+  ~ProfScope();
+
+ private:
+  cudaStream_t s_;
+  void* a_;
+  void* b_ = nullptr;
+  int cat_ = 0;
+  double flops_ = 0, bytes_ = 0;
+};
+long long launch_count();
+void prof_enable(bool on);
+int prof_collect(double* out, int ncat);
+double fp64_dmma_peak(double duration_ms, int reps);
+
 // Grow-only device arena per (device, slot) with a mutex; returns nullptr on OOM.
 void* arena_get(int slot, size_t bytes);
 void arena_release_all();

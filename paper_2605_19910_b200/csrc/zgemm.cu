@@ -9,7 +9,7 @@
 // Complex product with 4 real DMMAs per 8x8x4 step (no 3M trick: same rounding
 // class as zgemm). CTA tile 64x64 complex, 4 warps of 32x32, K staged 16 at a
 // time through a 2-stage cp.async pipeline into padded, bank-conflict-free smem.
-#include "zcommon.cuh"
+#include "internal.h"
 
 namespace bbsi_gpu {
 
@@ -153,6 +153,14 @@ cudaError_t zgemm_grouped(ZGemmGroup& g, cudaStream_t stream) {
   }
   g.total_tiles = total;
   if (total == 0) return cudaSuccess;
+  double fl = 0, by = 0;
+  for (int p = 0; p < g.nprob; ++p) {
+    const ZGemmProblem& P = g.prob[p];
+    const bool rc = P.beta.x != 0.0 || P.beta.y != 0.0;
+    fl += 8.0 * P.M * P.N * double(P.K) * g.batch;
+    by += 16.0 * g.batch * (double(P.M) * P.K + double(P.K) * P.N + double(P.M) * P.N * (rc ? 2 : 1));
+  }
+  ProfScope prof(stream, PROF_GEMM, fl, by);
   zgemm_grouped_kernel<<<total, 128, SMEM_BYTES, stream>>>(g);
   return cudaGetLastError();
 }

@@ -23,7 +23,7 @@
 #include <cfloat>
 #include <climits>
 
-#include "zcommon.cuh"
+#include "internal.h"
 
 namespace bbsi_gpu {
 
@@ -340,6 +340,7 @@ cudaError_t zinv_batched(double2* M, long long ld, long long bstride, int n, int
     attr = smem;
   }
   if (batch == 0) return cudaSuccess;
+  ProfScope prof(stream, PROF_INV, 8.0 * double(n) * n * n * batch, 32.0 * double(n) * n * batch);
   zinv_gj_kernel<<<batch, NT, smem, stream>>>(M, ld, bstride, n, n_true, piv, wz, status);
   return cudaGetLastError();
 }
