@@ -108,7 +108,8 @@ void unpad_band(const std::vector<double2>& in, int bp, const HostBand& h, doubl
 
 // Runs the batched sweeps on a device band (already holding A) with the arena scratch.
 int run_sweeps(SweepWork& W, const std::vector<int>& n_true, std::vector<int>& fails, cudaStream_t s) {
-  void* scratch = arena_get(1, sweep_scratch_bytes(W.l, W.w, W.bs, W.batch));
+  W.groups = default_groups(W.batch, W.bs);
+  void* scratch = arena_get(1, sweep_scratch_bytes(W.l, W.w, W.bs, W.batch, W.groups));
   if (!scratch) return fail(BBSI_OUT_OF_MEMORY, "sweep workspace allocation failed");
   sweep_carve(W, scratch);
   CK(rgf_sweeps(W, n_true.data(), s));
@@ -340,8 +341,8 @@ void bbsi_dyson_fill_h_host(int l, int w, int b, uint64_t seed, double* H) {
 int bbsi_cuda_zgemm_dev(int m, int n, int k, const double* alpha, const double* dA, long long lda, long long a_bstride,
                         const double* dB, long long ldb, long long b_bstride, const double* beta, double* dC,
                         long long ldc, long long c_bstride, int batch, void* stream) {
-  if (m % 64 || n % 64 || k % 16 || m < 0 || n < 0 || k < 16 || batch < 1)
-    return fail(BBSI_INVALID_ARGUMENT, "zgemm: requires m, n % 64 == 0 and k % 16 == 0");
+  if (m < 1 || n < 1 || k % 16 || k < 16 || batch < 1)
+    return fail(BBSI_INVALID_ARGUMENT, "zgemm: requires m, n >= 1 and k % 16 == 0");
   if (int rc = device_ok()) return rc;
   // plain column-major matrices as 64 x 64 block operands
   ZGemmGroup g{};
@@ -357,7 +358,7 @@ int bbsi_cuda_zgemm_dev(int m, int n, int k, const double* alpha, const double* 
   p.A = ZOp{reinterpret_cast<const double2*>(dA), lda, 64, 64 * lda, a_bstride};
   p.B = ZOp{reinterpret_cast<const double2*>(dB), ldb, 64, 64 * ldb, b_bstride};
   p.C = ZOp{reinterpret_cast<const double2*>(dC), ldc, 64, 64 * ldc, c_bstride};
-  p.D = reinterpret_cast<double2*>(dC);
+  p.D = p.C;
   CK(zgemm_grouped(g, static_cast<cudaStream_t>(stream)));
   return BBSI_OK;
 }
@@ -369,13 +370,11 @@ int bbsi_cuda_zinv_dev(int n, int n_true, int batch, double* dM, long long ld, l
   if (int rc = device_ok()) return rc;
   cudaStream_t s = static_cast<cudaStream_t>(stream);
   std::lock_guard<std::mutex> lk(g_call_mu);
-  size_t scr = size_t(batch) * (n * sizeof(int) + zinv_scratch_bytes(n) + sizeof(int)) + 512;
+  size_t scr = zinv_scratch_bytes(n, batch) + sizeof(int) * batch + 256;
   char* base = static_cast<char*>(arena_get(3, scr));
   if (!base) return fail(BBSI_OUT_OF_MEMORY, "zinv scratch allocation failed");
-  int* piv = reinterpret_cast<int*>(base);
-  double2* wz = reinterpret_cast<double2*>(base + ((size_t(batch) * n * sizeof(int) + 255) & ~size_t(255)));
-  int* st = reinterpret_cast<int*>(reinterpret_cast<char*>(wz) + size_t(batch) * zinv_scratch_bytes(n));
-  CK(zinv_batched(reinterpret_cast<double2*>(dM), ld, bstride, n, n_true, batch, piv, wz, st, s));
+  int* st = reinterpret_cast<int*>(base + zinv_scratch_bytes(n, batch));
+  CK(zinv_batched(reinterpret_cast<double2*>(dM), ld, bstride, n, n_true, batch, base, st, s));
   if (status_host) {
     CK(cudaMemcpyAsync(status_host, st, sizeof(int) * batch, cudaMemcpyDeviceToHost, s));
     CK(cudaStreamSynchronize(s));
@@ -413,7 +412,8 @@ int bbsi_cuda_dyson_rgf_z(int l, int w, int bs, int n_energy, const double* H, c
   const int nchunk = (n_energy + chunk - 1) / chunk;
   const long long band = (long long)l * (2 * w + 1) * bs * bs;
   const size_t band_b = size_t(band) * sizeof(double2);
-  const size_t scr_b = sweep_scratch_bytes(l, w, bs, chunk);
+  const int groups = default_groups(chunk, bs);
+  const size_t scr_b = sweep_scratch_bytes(l, w, bs, chunk, groups);
   size_t free_b = 0, total_b = 0;
   CK(cudaMemGetInfo(&free_b, &total_b));
   int nbuf = nchunk;
@@ -448,6 +448,7 @@ int bbsi_cuda_dyson_rgf_z(int l, int w, int bs, int n_energy, const double* H, c
       W.batch = ne;
       W.G = g;
       W.g_bstride = band;
+      W.groups = groups;
       sweep_carve(W, scratch);
       CK(rgf_sweeps(W, nt.data(), sc));
       // status rows [layer][ne] of this chunk -> host (pageable; tiny)

@@ -12,9 +12,11 @@ namespace bbsi_gpu {
 
 // kernels
 cudaError_t zgemm_grouped(ZGemmGroup& g, cudaStream_t stream);
-cudaError_t zinv_batched(double2* M, long long ld, long long bstride, int n, int n_true, int batch, int* piv,
-                         double2* wz, int* status, cudaStream_t stream);
-size_t zinv_scratch_bytes(int n);
+// In-place batched inverse (blocked Gauss-Jordan, partial pivoting); scratch of
+// zinv_scratch_bytes(n, batch) bytes; status[b] = -1 or the first negligible pivot.
+cudaError_t zinv_batched(double2* M, long long ld, long long bstride, int n, int n_true, int batch, void* scratch,
+                         int* status, cudaStream_t stream);
+size_t zinv_scratch_bytes(int n, int batch);
 cudaError_t dyson_fill_h(double2* H, int l, int w, int b, uint64_t seed, cudaStream_t s);
 cudaError_t dyson_form_band(double2* G, const double2* H, int l, int w, int bs, int batch, const double2* z,
                             const double2* sigma, cudaStream_t s);
@@ -34,13 +36,15 @@ struct SweepWork {
   long long g_bstride = 0;
   double2* LM = nullptr;  // [batch][l][w][bs*bs]: lm[j][t-1] = X_j M'[j, j-t]
   double2* UM = nullptr;  // [batch][l][w][bs*bs]: um[j][t-1] = M'[j-t, j] X_j
-  int* piv = nullptr;     // [batch][bs]
-  double2* wz = nullptr;  // [batch][bs*16]
+  void* inv = nullptr;    // zinv scratch for `batch` matrices
+  int groups = 1;         // independent batch groups swept concurrently on side streams
   int* status = nullptr;  // [l][batch]
 };
 
 // Bytes of LM+UM+piv+wz+status for a sweep.
-size_t sweep_scratch_bytes(int l, int w, int bs, int batch);
+size_t sweep_scratch_bytes(int l, int w, int bs, int batch, int groups = 1);
+// Default number of concurrent batch groups (env BBSI_GROUPS overrides).
+int default_groups(int batch, int bs);
 // Carves the scratch part of a SweepWork out of `base` (>= sweep_scratch_bytes).
 void sweep_carve(SweepWork& W, void* base);
 

@@ -19,18 +19,27 @@
 // explicit inverse X_j is written into G[j,j], which the downward pass updates
 // in place. Every operand is a strided set of slots of the band storage
 // slot(a, off) = a*(2w+1) + off + w (block_banded.hpp:58-60).
+#include <cstdlib>
 #include <mutex>
 
 #include "internal.h"
 
 namespace bbsi_gpu {
 
-size_t sweep_scratch_bytes(int l, int w, int bs, int batch) {
+int default_groups(int batch, int bs) {
+  if (const char* e = getenv("BBSI_GROUPS")) {
+    int g = atoi(e);
+    if (g >= 1) return g < batch ? g : batch;
+  }
+  (void)bs;
+  int g = batch >= 32 ? 2 : 1;
+  return g;
+}
+
+size_t sweep_scratch_bytes(int l, int w, int bs, int batch, int groups) {
   const size_t bb = size_t(bs) * bs * sizeof(double2);
   size_t s = 2 * size_t(batch) * l * w * bb;              // LM, UM
-  s += size_t(batch) * bs * sizeof(int);                  // piv
-  s = (s + 255) & ~size_t(255);
-  s += size_t(batch) * zinv_scratch_bytes(bs);            // wz
+  s += size_t(groups) * (zinv_scratch_bytes(bs, (batch + groups - 1) / groups) + 256);  // inversion scratch
   s += size_t(l) * batch * sizeof(int) + 256;             // status
   return s;
 }
@@ -42,11 +51,9 @@ void sweep_carve(SweepWork& W, void* base) {
   p += size_t(W.batch) * W.l * W.w * bb * sizeof(double2);
   W.UM = reinterpret_cast<double2*>(p);
   p += size_t(W.batch) * W.l * W.w * bb * sizeof(double2);
-  W.piv = reinterpret_cast<int*>(p);
-  p += size_t(W.batch) * W.bs * sizeof(int);
-  p = reinterpret_cast<char*>((reinterpret_cast<uintptr_t>(p) + 255) & ~uintptr_t(255));
-  W.wz = reinterpret_cast<double2*>(p);
-  p += size_t(W.batch) * zinv_scratch_bytes(W.bs);
+  W.inv = p;
+  const int gs = (W.batch + W.groups - 1) / W.groups;
+  p += size_t(W.groups) * (zinv_scratch_bytes(W.bs, gs) + 256);
   W.status = reinterpret_cast<int*>(p);
 }
 
@@ -78,7 +85,7 @@ ZGemmProblem prob(int M, int N, int K, double alpha, double beta, ZOp A, ZOp B, 
   p.A = A;
   p.B = B;
   p.C = C;
-  p.D = const_cast<double2*>(C.p);
+  p.D = C;
   return p;
 }
 
@@ -92,14 +99,16 @@ cudaError_t launch(const SweepWork& W, std::initializer_list<ZGemmProblem> ps, c
 
 }  // namespace
 
-cudaError_t rgf_sweeps(const SweepWork& W, const int* n_true, cudaStream_t s) {
+namespace {
+
+cudaError_t rgf_sweeps_one(const SweepWork& W, const int* n_true, int* status, int status_stride, cudaStream_t s) {
   Ctx c(W);
   const int l = W.l, w = W.w, b = W.bs;
   const long long two_w = 2LL * w;
   cudaError_t e;
   auto inv = [&](int j) {
-    return zinv_batched(c.slot(j, 0), b, W.g_bstride, b, n_true[j], W.batch, W.piv, W.wz,
-                        W.status + (long long)j * W.batch, s);
+    return zinv_batched(c.slot(j, 0), b, W.g_bstride, b, n_true[j], W.batch, W.inv,
+                        status + (long long)j * status_stride, s);
   };
 
   // ---------------- upward sweep (rgf.hpp:98-114)
@@ -128,6 +137,62 @@ cudaError_t rgf_sweeps(const SweepWork& W, const int* n_true, cudaStream_t s) {
     if ((e = launch(W, {p_row, p_col}, s)) != cudaSuccess) return e;
     ZGemmProblem p_diag = prob(b, b, k * b, -1.0, 1.0, lmrow, c.gop(c.slot(j - 1, +1), -two_w, 0), c.gop(c.slot(j, 0), 0, 0));
     if ((e = launch(W, {p_diag}, s)) != cudaSuccess) return e;
+  }
+  return cudaSuccess;
+}
+
+struct StreamPool {
+  std::vector<cudaStream_t> s;
+  std::vector<cudaEvent_t> ev;
+};
+std::mutex g_pool_mu;
+std::vector<StreamPool> g_pools;
+
+StreamPool& pool_for(int n) {
+  std::lock_guard<std::mutex> lk(g_pool_mu);
+  int dev = 0;
+  cudaGetDevice(&dev);
+  if (int(g_pools.size()) <= dev) g_pools.resize(dev + 1);
+  StreamPool& p = g_pools[dev];
+  while (int(p.s.size()) < n) {
+    cudaStream_t st;
+    cudaStreamCreateWithFlags(&st, cudaStreamNonBlocking);
+    p.s.push_back(st);
+  }
+  while (int(p.ev.size()) < n + 1) {
+    cudaEvent_t e;
+    cudaEventCreateWithFlags(&e, cudaEventDisableTiming);
+    p.ev.push_back(e);
+  }
+  return p;
+}
+
+}  // namespace
+
+cudaError_t rgf_sweeps(const SweepWork& W, const int* n_true, cudaStream_t s) {
+  const int G = W.groups < 1 ? 1 : (W.groups > W.batch ? W.batch : W.groups);
+  if (G == 1) return rgf_sweeps_one(W, n_true, W.status, W.batch, s);
+  // Independent batch groups on side streams: one group's latency-bound pivot
+  // inversions overlap the other groups' GEMMs.
+  StreamPool& P = pool_for(G);
+  cudaError_t e;
+  if ((e = cudaEventRecord(P.ev[G], s))) return e;
+  const int gs = (W.batch + G - 1) / G;
+  const long long bb = (long long)W.bs * W.bs;
+  const size_t inv_b = zinv_scratch_bytes(W.bs, gs) + 256;
+  for (int g = 0; g < G; ++g) {
+    const int e0 = g * gs, ne = std::min(gs, W.batch - e0);
+    if (ne <= 0) break;
+    SweepWork Wg = W;
+    Wg.batch = ne;
+    Wg.G = W.G + (long long)e0 * W.g_bstride;
+    Wg.LM = W.LM + (long long)e0 * W.l * W.w * bb;
+    Wg.UM = W.UM + (long long)e0 * W.l * W.w * bb;
+    Wg.inv = static_cast<char*>(W.inv) + size_t(g) * inv_b;
+    if ((e = cudaStreamWaitEvent(P.s[g], P.ev[G], 0))) return e;
+    if ((e = rgf_sweeps_one(Wg, n_true, W.status + e0, W.batch, P.s[g]))) return e;
+    if ((e = cudaEventRecord(P.ev[g], P.s[g]))) return e;
+    if ((e = cudaStreamWaitEvent(s, P.ev[g], 0))) return e;
   }
   return cudaSuccess;
 }

@@ -22,10 +22,17 @@ struct ZOp {
 };
 
 struct ZGemmProblem {
-  int M, N, K;          // logical sizes, multiples of 64 (M, N) and 16 (K)
+  int M, N, K;          // logical sizes; K % 16 == 0, M/N arbitrary (masked edge tiles)
   double2 alpha, beta;  // D = alpha * A*B + beta * C
   ZOp A, B, C;          // C may be ignored when beta == 0
-  double2* D;           // same strides as C
+  ZOp D;                // output operand (p is written)
+  // optional epilogue remaps (plain single-block operands; used by the blocked
+  // Gauss-Jordan inversion): C row r is read from row rowmap[r]; C is taken as 0
+  // for rows [zr0, zr1) and columns [zc0, zc1); D column c is written to colmap[c].
+  const int* rowmap;
+  const int* colmap;
+  long long map_bstride;
+  int zr0, zr1, zc0, zc1;
   int tiles_m, tiles_n; // filled by the launcher
   int tile_begin;       // first flattened tile index of this problem
 };

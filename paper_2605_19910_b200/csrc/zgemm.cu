@@ -23,24 +23,40 @@ constexpr int A_STAGE = BK * LDA_S;
 constexpr int B_STAGE = BN * LDB_S;
 constexpr int SMEM_BYTES = STAGES * (A_STAGE + B_STAGE) * sizeof(double2);
 
+__device__ __forceinline__ void cp_async16_zfill(void* smem, const void* gmem, bool valid) {
+  unsigned sa = (unsigned)__cvta_generic_to_shared(smem);
+  int n = valid ? 16 : 0;
+  asm volatile("cp.async.cg.shared.global [%0], [%1], 16, %2;\n" ::"r"(sa), "l"(gmem), "r"(n));
+}
+
+template <bool PLAIN>
+__device__ __forceinline__ long long toff(const ZOp& o, int bs, int r, int c) {
+  return PLAIN ? (long long)c * o.ld + r : zop_offset(o, bs, r, c);
+}
+
+template <bool PLAIN>
 __device__ __forceinline__ void load_tile(const ZGemmProblem& P, int bs, int batch, int m0, int n0, int k0,
                                           double2* As, double2* Bs, int tid) {
-  const double2* a = P.A.p + (long long)batch * P.A.bstride + zop_offset(P.A, bs, m0, k0);
-  const double2* b = P.B.p + (long long)batch * P.B.bstride + zop_offset(P.B, bs, k0, n0);
+  const double2* a = P.A.p + (long long)batch * P.A.bstride + toff<PLAIN>(P.A, bs, m0, k0);
+  const double2* b = P.B.p + (long long)batch * P.B.bstride + toff<PLAIN>(P.B, bs, k0, n0);
+  const int mlim = P.M - m0, nlim = P.N - n0;
 #pragma unroll
   for (int i = 0; i < (BM * BK) / 128; ++i) {
     int e = tid + 128 * i;
     int m = e & (BM - 1), k = e >> 6;
-    cp_async16(&As[k * LDA_S + m], a + (long long)k * P.A.ld + m);
+    const bool v = m < mlim;
+    cp_async16_zfill(&As[k * LDA_S + m], v ? a + (long long)k * P.A.ld + m : a, v);
   }
 #pragma unroll
   for (int i = 0; i < (BN * BK) / 128; ++i) {
     int e = tid + 128 * i;
     int k = e & (BK - 1), n = e >> 4;
-    cp_async16(&Bs[n * LDB_S + k], b + (long long)n * P.B.ld + k);
+    const bool v = n < nlim;
+    cp_async16_zfill(&Bs[n * LDB_S + k], v ? b + (long long)n * P.B.ld + k : b, v);
   }
 }
 
+template <bool PLAIN>
 __global__ void __launch_bounds__(128, 2) zgemm_grouped_kernel(const __grid_constant__ ZGemmGroup g) {
   extern __shared__ __align__(16) double2 smem[];
   double2* As = smem;
@@ -66,19 +82,69 @@ __global__ void __launch_bounds__(128, 2) zgemm_grouped_kernel(const __grid_cons
   const int lr = lane >> 2, lc = lane & 3;
 
   double cr[4][4][2], ci[4][4][2];
-#pragma unroll
-  for (int i = 0; i < 4; ++i)
-#pragma unroll
-    for (int j = 0; j < 4; ++j) cr[i][j][0] = cr[i][j][1] = ci[i][j][0] = ci[i][j][1] = 0.0;
-
   const int nk = P.K / BK;
-  load_tile(P, bs, batch, m0, n0, 0, As, Bs, tid);
+  load_tile<PLAIN>(P, bs, batch, m0, n0, 0, As, Bs, tid);
   cp_async_commit();
+
+  // C enters as the accumulator's initial value when beta == 1 and alpha = +-1
+  // (D = alpha*(alpha*C + AB) = C + alpha*AB exactly); all C loads are issued
+  // up front, overlapping the first tile copies, and the epilogue only stores.
+  const bool use_c = (P.beta.x != 0.0 || P.beta.y != 0.0);
+  const bool c_in_acc = use_c && P.beta.x == 1.0 && P.beta.y == 0.0 && P.alpha.y == 0.0 &&
+                        (P.alpha.x == 1.0 || P.alpha.x == -1.0);
+  if (c_in_acc) {
+    // tiles never straddle a bs block: address = tile base + local offset. A row
+    // map is only allowed on plain operands (offset(r, c) = r + c*ld).
+    const int* rmap = P.rowmap ? P.rowmap + (long long)batch * P.map_bstride : nullptr;
+    const double2* __restrict__ cb = P.C.p + (long long)batch * P.C.bstride;
+    const double2* __restrict__ ct = cb + toff<PLAIN>(P.C, bs, m0, n0);
+    const double sg = P.alpha.x;
+    int srow[4];
+    bool rowok[4], colok[4][2];
+#pragma unroll
+    for (int mi = 0; mi < 4; ++mi) {
+      const int m = m0 + wm + mi * 8 + lr;
+      rowok[mi] = m < P.M && !(m >= P.zr0 && m < P.zr1);
+      srow[mi] = rmap ? (m < P.M ? __ldg(&rmap[m]) : 0) : m - m0;
+    }
+#pragma unroll
+    for (int ni = 0; ni < 4; ++ni)
+#pragma unroll
+      for (int q = 0; q < 2; ++q) {
+        const int n = n0 + wn + ni * 8 + lc * 2 + q;
+        colok[ni][q] = n < P.N && !(n >= P.zc0 && n < P.zc1);
+      }
+    const double2* __restrict__ rb = rmap ? cb + (long long)n0 * P.C.ld : ct;
+    double2 cv[4][4][2];
+#pragma unroll
+    for (int mi = 0; mi < 4; ++mi)
+#pragma unroll
+      for (int ni = 0; ni < 4; ++ni)
+#pragma unroll
+        for (int q = 0; q < 2; ++q) {
+          const int nl = wn + ni * 8 + lc * 2 + q;
+          cv[mi][ni][q] = (rowok[mi] && colok[ni][q]) ? rb[(long long)nl * P.C.ld + srow[mi]] : make_double2(0.0, 0.0);
+        }
+#pragma unroll
+    for (int mi = 0; mi < 4; ++mi)
+#pragma unroll
+      for (int ni = 0; ni < 4; ++ni)
+#pragma unroll
+        for (int q = 0; q < 2; ++q) {
+          cr[mi][ni][q] = sg * cv[mi][ni][q].x;
+          ci[mi][ni][q] = sg * cv[mi][ni][q].y;
+        }
+  } else {
+#pragma unroll
+    for (int i = 0; i < 4; ++i)
+#pragma unroll
+      for (int j = 0; j < 4; ++j) cr[i][j][0] = cr[i][j][1] = ci[i][j][0] = ci[i][j][1] = 0.0;
+  }
 
 #pragma unroll 1
   for (int kc = 0; kc < nk; ++kc) {
     const int s = kc & 1;
-    if (kc + 1 < nk) load_tile(P, bs, batch, m0, n0, (kc + 1) * BK, As + (s ^ 1) * A_STAGE, Bs + (s ^ 1) * B_STAGE, tid);
+    if (kc + 1 < nk) load_tile<PLAIN>(P, bs, batch, m0, n0, (kc + 1) * BK, As + (s ^ 1) * A_STAGE, Bs + (s ^ 1) * B_STAGE, tid);
     cp_async_commit();
     cp_async_wait<1>();
     __syncthreads();
@@ -113,24 +179,73 @@ __global__ void __launch_bounds__(128, 2) zgemm_grouped_kernel(const __grid_cons
     __syncthreads();
   }
 
-  // ---- epilogue: D = alpha*acc + beta*C
-  const bool use_c = (P.beta.x != 0.0 || P.beta.y != 0.0);
-  const long long coff = (long long)batch * P.C.bstride + zop_offset(P.C, bs, m0, n0);
-  const double2* cptr = P.C.p + coff;
-  double2* dptr = P.D + coff;
+  // ---- epilogue
+  const int* cmap = P.colmap ? P.colmap + (long long)batch * P.map_bstride : nullptr;
+  double2* __restrict__ dbase = const_cast<double2*>(P.D.p) + (long long)batch * P.D.bstride;
+  if (c_in_acc || !use_c) {  // D = alpha * acc (C already inside acc when c_in_acc)
+    const double2 al = c_in_acc ? make_double2(P.alpha.x, 0.0) : P.alpha;
+    if (!cmap && m0 + BM <= P.M && n0 + BN <= P.N) {
+      double2* __restrict__ dptr = dbase + toff<PLAIN>(P.D, bs, m0, n0);
 #pragma unroll
-  for (int mi = 0; mi < 4; ++mi)
+      for (int mi = 0; mi < 4; ++mi)
 #pragma unroll
-    for (int ni = 0; ni < 4; ++ni)
+        for (int ni = 0; ni < 4; ++ni)
 #pragma unroll
-      for (int q = 0; q < 2; ++q) {
-        const int m = wm + mi * 8 + lr, n = wn + ni * 8 + lc * 2 + q;
-        const long long o = (long long)n * P.C.ld + m;
-        double2 acc = make_double2(cr[mi][ni][q], ci[mi][ni][q]);
-        double2 out = cmul(P.alpha, acc);
-        if (use_c) out = cfma(P.beta, cptr[o], out);
-        dptr[o] = out;
-      }
+          for (int q = 0; q < 2; ++q) {
+            const int m = wm + mi * 8 + lr, n = wn + ni * 8 + lc * 2 + q;
+            dptr[(long long)n * P.D.ld + m] = cmul(al, make_double2(cr[mi][ni][q], ci[mi][ni][q]));
+          }
+    } else {  // edge tile and/or column scatter (plain operand: offset = r + c*ld)
+      double2* __restrict__ dt = dbase + toff<PLAIN>(P.D, bs, m0, n0);
+      long long dcol[4][2];
+#pragma unroll
+      for (int ni = 0; ni < 4; ++ni)
+#pragma unroll
+        for (int q = 0; q < 2; ++q) {
+          const int n = n0 + wn + ni * 8 + lc * 2 + q;
+          dcol[ni][q] = (n < P.N) ? (long long)(cmap ? __ldg(&cmap[n]) - n0 : n - n0) * P.D.ld : 0;
+        }
+#pragma unroll
+      for (int mi = 0; mi < 4; ++mi)
+#pragma unroll
+        for (int ni = 0; ni < 4; ++ni)
+#pragma unroll
+          for (int q = 0; q < 2; ++q) {
+            const int ml = wm + mi * 8 + lr;
+            if (m0 + ml >= P.M || n0 + wn + ni * 8 + lc * 2 + q >= P.N) continue;
+            dt[dcol[ni][q] + ml] = cmul(al, make_double2(cr[mi][ni][q], ci[mi][ni][q]));
+          }
+    }
+  } else {  // general complex alpha / beta: D = alpha*acc + beta*C, C read in two halves
+    const int* rmap = P.rowmap ? P.rowmap + (long long)batch * P.map_bstride : nullptr;
+    const double2* __restrict__ cbase = P.C.p + (long long)batch * P.C.bstride;
+#pragma unroll
+    for (int half = 0; half < 2; ++half) {
+      double2 cv[2][4][2];
+#pragma unroll
+      for (int mh = 0; mh < 2; ++mh)
+#pragma unroll
+        for (int ni = 0; ni < 4; ++ni)
+#pragma unroll
+          for (int q = 0; q < 2; ++q) {
+            const int m = m0 + wm + (half * 2 + mh) * 8 + lr, n = n0 + wn + ni * 8 + lc * 2 + q;
+            const bool z = m >= P.M || n >= P.N || (m >= P.zr0 && m < P.zr1) || (n >= P.zc0 && n < P.zc1);
+            cv[mh][ni][q] = z ? make_double2(0.0, 0.0) : cbase[toff<PLAIN>(P.C, bs, rmap ? __ldg(&rmap[m]) : m, n)];
+          }
+#pragma unroll
+      for (int mh = 0; mh < 2; ++mh)
+#pragma unroll
+        for (int ni = 0; ni < 4; ++ni)
+#pragma unroll
+          for (int q = 0; q < 2; ++q) {
+            const int mi = half * 2 + mh;
+            const int m = m0 + wm + mi * 8 + lr, n = n0 + wn + ni * 8 + lc * 2 + q;
+            if (m >= P.M || n >= P.N) continue;
+            double2 out = cfma(P.beta, cv[mh][ni][q], cmul(P.alpha, make_double2(cr[mi][ni][q], ci[mi][ni][q])));
+            dbase[toff<PLAIN>(P.D, bs, m, cmap ? __ldg(&cmap[n]) : n)] = out;
+          }
+    }
+  }
 }
 
 }  // namespace
@@ -138,18 +253,24 @@ __global__ void __launch_bounds__(128, 2) zgemm_grouped_kernel(const __grid_cons
 cudaError_t zgemm_grouped(ZGemmGroup& g, cudaStream_t stream) {
   static bool attr_set = false;
   if (!attr_set) {
-    cudaError_t e = cudaFuncSetAttribute(zgemm_grouped_kernel, cudaFuncAttributeMaxDynamicSharedMemorySize, SMEM_BYTES);
+    cudaError_t e = cudaFuncSetAttribute(zgemm_grouped_kernel<false>, cudaFuncAttributeMaxDynamicSharedMemorySize,
+                                         SMEM_BYTES);
+    if (e == cudaSuccess)
+      e = cudaFuncSetAttribute(zgemm_grouped_kernel<true>, cudaFuncAttributeMaxDynamicSharedMemorySize, SMEM_BYTES);
     if (e != cudaSuccess) return e;
     attr_set = true;
   }
   int total = 0;
+  bool plain = true;
+  auto is_plain = [&](const ZOp& o) { return o.rs == g.bs && o.cs == (long long)g.bs * o.ld; };
   for (int p = 0; p < g.nprob; ++p) {
     ZGemmProblem& P = g.prob[p];
-    if (P.M % BM || P.N % BN || P.K % BK || g.bs % BM) return cudaErrorInvalidValue;
-    P.tiles_m = P.M / BM;
-    P.tiles_n = P.N / BN;
+    if (P.M < 1 || P.N < 1 || P.K % BK || P.K < BK || g.bs % BM) return cudaErrorInvalidValue;
+    P.tiles_m = (P.M + BM - 1) / BM;
+    P.tiles_n = (P.N + BN - 1) / BN;
     P.tile_begin = total;
     total += P.tiles_m * P.tiles_n * g.batch;
+    plain = plain && is_plain(P.A) && is_plain(P.B) && is_plain(P.C) && is_plain(P.D);
   }
   g.total_tiles = total;
   if (total == 0) return cudaSuccess;
@@ -161,7 +282,10 @@ cudaError_t zgemm_grouped(ZGemmGroup& g, cudaStream_t stream) {
     by += 16.0 * g.batch * (double(P.M) * P.K + double(P.K) * P.N + double(P.M) * P.N * (rc ? 2 : 1));
   }
   ProfScope prof(stream, PROF_GEMM, fl, by);
-  zgemm_grouped_kernel<<<total, 128, SMEM_BYTES, stream>>>(g);
+  if (plain)
+    zgemm_grouped_kernel<true><<<total, 128, SMEM_BYTES, stream>>>(g);
+  else
+    zgemm_grouped_kernel<false><<<total, 128, SMEM_BYTES, stream>>>(g);
   return cudaGetLastError();
 }
 

@@ -31,7 +31,7 @@ def _host(t):
     return np.swapaxes(t.cpu().numpy(), -1, -2)
 
 
-@pytest.mark.parametrize("m,n,k,batch", [(64, 64, 16, 1), (128, 192, 64, 3), (256, 256, 256, 4), (64, 128, 768, 2)])
+@pytest.mark.parametrize("m,n,k,batch", [(64, 64, 16, 1), (128, 192, 64, 3), (256, 256, 256, 4), (64, 128, 768, 2), (32, 96, 48, 2), (100, 70, 32, 1)])
 def test_zgemm_matches_numpy(gpu, m, n, k, batch):
     from paper_2605_19910_b200._native import lib
 
@@ -52,7 +52,7 @@ def test_zgemm_matches_numpy(gpu, m, n, k, batch):
         assert err <= 1e-13, err
 
 
-@pytest.mark.parametrize("n,n_true,batch", [(64, 64, 2), (128, 100, 3), (256, 256, 2), (768, 768, 1)])
+@pytest.mark.parametrize("n,n_true,batch", [(64, 64, 2), (128, 100, 3), (256, 256, 2), (512, 512, 2), (768, 768, 1)])
 def test_zinv_matches_numpy(gpu, n, n_true, batch):
     from paper_2605_19910_b200._native import lib
 
