@@ -72,6 +72,28 @@ __device__ __forceinline__ double2 crcp(double2 a) {
   }
 }
 
+// Division-free reciprocal of a nonzero complex: conj(a) * (1/|a|^2) with |a|^2
+// formed after scaling by a power of two (exact) to avoid over/underflow; 1/x by
+// the MUFU seed plus two Newton steps (~1 ulp). Zero maps to zero.
+__device__ __forceinline__ double rcp_nr(double x) {
+  double y;
+  asm("rcp.approx.ftz.f64 %0, %1;" : "=d"(y) : "d"(x));
+  double e = fma(-x, y, 1.0);
+  y = fma(y, e, y);
+  e = fma(-x, y, 1.0);
+  return fma(y, e, y);
+}
+__device__ __forceinline__ double2 crcp_fast(double2 a) {
+  const double m = fmax(fabs(a.x), fabs(a.y));
+  if (m == 0.0) return make_double2(0.0, 0.0);
+  int ex;
+  frexp(m, &ex);
+  const double sc = ldexp(1.0, -ex);  // power of two: exact scaling
+  const double xr = a.x * sc, xi = a.y * sc;
+  const double inv = rcp_nr(fma(xr, xr, xi * xi)) * sc;
+  return make_double2(xr * inv, -xi * inv);
+}
+
 // DMMA: D(8x8) += A(8x4, row) * B(4x8, col), FP64. One lane holds A[l/4][l%4],
 // B[l%4][l/4] and C[l/4][2*(l%4) + {0,1}].
 __device__ __forceinline__ void dmma884(double (&c)[2], double a, double b) {

@@ -29,10 +29,11 @@
 #include "internal.h"
 
 namespace bbsi_gpu {
+__device__ long long g_zinv_dbg[64];
 
 namespace {
 
-constexpr int PT = 1024;  // panel kernel threads
+constexpr int PT = 256;  // panel kernel threads
 
 struct GjScratch {
   int* rowmap;    // [batch][n]
@@ -84,8 +85,8 @@ __global__ void __launch_bounds__(PT, 1)
     gj_panel_kernel(const double2* __restrict__ cur0, long long ld, long long bstride, int n, int n_true, int k,
                     GjScratch S, int* __restrict__ status) {
   extern __shared__ __align__(16) double2 pn[];  // NB columns x rows (ld = rows + 1), panel in smem
-  __shared__ double cand_v[PT / 32];
-  __shared__ int cand_i[PT / 32];
+  __shared__ double cand_v[2][PT / 32];
+  __shared__ int cand_i[2][PT / 32];
   __shared__ int s_piv[NB];   // pivot row (panel-local) chosen at step j
   __shared__ int s_src[NB];   // source row (global index) of pivot row k+j after interchanges
   __shared__ int s_fail;
@@ -99,26 +100,32 @@ __global__ void __launch_bounds__(PT, 1)
   int* __restrict__ rowmap = S.rowmap + (long long)b * n;
   int* __restrict__ piv = S.piv + (long long)b * n;
 
+#ifdef BBSI_ZINV_DEBUG
+#define DBG(i) if (b == 0 && tid == 0 && k == 32) g_zinv_dbg[i] = clock64();
+#else
+#define DBG(i)
+#endif
+  DBG(0)
   if (tid == 0) s_fail = INT_MAX;
   if (k == 0) {  // threshold eps * n * max|A| over the true block (kernels.hpp:149-158)
     double mx = 0.0;
-    if (tid < n_true) {
+    for (int r = tid; r < n_true; r += PT) {
 #pragma unroll 1
       for (int c0 = 0; c0 < n_true; c0 += 8) {
         double2 v[8];
 #pragma unroll
         for (int u = 0; u < 8; ++u)
-          v[u] = (c0 + u < n_true) ? cur[(long long)(c0 + u) * ld + tid] : make_double2(0.0, 0.0);
+          v[u] = (c0 + u < n_true) ? cur[(long long)(c0 + u) * ld + r] : make_double2(0.0, 0.0);
 #pragma unroll
         for (int u = 0; u < 8; ++u) mx = fmax(mx, hypot(v[u].x, v[u].y));
       }
     }
 #pragma unroll
     for (int o = 16; o; o >>= 1) mx = fmax(mx, __shfl_xor_sync(0xffffffffu, mx, o));
-    if (lane == 0) cand_v[warp] = mx;
+    if (lane == 0) cand_v[1][warp] = mx;
     __syncthreads();
     if (warp == 0) {
-      double m = cand_v[lane];
+      double m = cand_v[1][lane];
 #pragma unroll
       for (int o = 16; o; o >>= 1) m = fmax(m, __shfl_xor_sync(0xffffffffu, m, o));
       if (lane == 0) {
@@ -146,10 +153,18 @@ __global__ void __launch_bounds__(PT, 1)
     }
   }
   __syncthreads();
+  DBG(1)
   const double tol = s_tol;
 
+  // Row interchanges are applied to a logical->physical row permutation (double
+  // buffered by parity) instead of moving data, so one barrier per column
+  // suffices: every warp resolves the pivot redundantly from the published
+  // per-warp candidates (also double buffered).
+  int* perm = reinterpret_cast<int*>(pn + NB * ldp);  // [2][rows]
+  for (int r = tid; r < rows; r += PT) perm[r] = r;
+
   // warp-level argmax of |re|+|im| over the rows this thread offers; lane 0 publishes
-  auto publish = [&](double bv, int bi) {
+  auto publish = [&](int par, double bv, int bi) {
 #pragma unroll
     for (int o = 16; o; o >>= 1) {
       double v2 = __shfl_xor_sync(0xffffffffu, bv, o);
@@ -157,69 +172,205 @@ __global__ void __launch_bounds__(PT, 1)
       argmax_merge(bv, bi, v2, i2);
     }
     if (lane == 0) {
-      cand_v[warp] = bv;
-      cand_i[warp] = bi;
+      cand_v[par][warp] = bv;
+      cand_i[par][warp] = bi;
     }
   };
   {  // candidates for column 0
-    const int r = tid;
-    const bool on = r < rows;
-    publish(on ? cabs1(pn[r]) : -1.0, on ? r : INT_MAX);
+    double bv = -1.0;
+    int bi = INT_MAX;
+    for (int r = tid; r < rows; r += PT) {
+      const double a = cabs1(pn[r]);
+      if (a > bv) {
+        bv = a;
+        bi = r;
+      }
+    }
+    publish(0, bv, bi);
   }
 
-  // ---- right-looking LU with partial pivoting, 3 barriers per column:
-  //   B1 candidates visible -> warp 0 resolves the pivot, swaps rows j/p and
-  //      publishes 1/pivot
-  //   B2 -> multipliers of column j
-  //   B3 -> rank-1 update of the trailing block by a 256 (rows) x 4 (column
-  //         groups) thread grid; column j+1's updaters publish its candidates.
-  __shared__ double2 s_inv;
-  const int nwarp_rows = (rows + 31) / 32 < 8 ? (rows + 31) / 32 : 8;
-  const int rt = tid & 255, cg = tid >> 8;
+  const int nwarp_rows = (rows + 31) / 32 < PT / 32 ? (rows + 31) / 32 : PT / 32;
+  // The register-resident variant measured slower than the shared-memory one on
+  // B200 (4.6k vs 3.9k cycles per column at n = 256); kept for experiments.
+  constexpr bool kRegPath = false;
+  const bool reg = kRegPath && rows <= PT;
+  if (reg) {
+    // ---- register path: physical row t is owned by thread t and kept in
+    // registers; interchanges only relabel logical indices. Per column: one
+    // barrier; each warp's best candidate lane publishes its whole row, every
+    // warp resolves the pivot redundantly and reads the winning row.
+    __shared__ double2 cand_row[2][PT / 32][NB];
+    __shared__ int cand_ph[2][PT / 32];
+    const int t = tid;
+    const bool own = t < rows;
+    double2 a[NB];
+#pragma unroll
+    for (int c = 0; c < NB; ++c) a[c] = own ? pn[c * ldp + t] : make_double2(0.0, 0.0);
+    int mylog = t;
+    auto publish_reg = [&](int par, double bv, int blog) {
+      int bph = t;
+#pragma unroll
+      for (int o = 16; o; o >>= 1) {
+        double v2 = __shfl_xor_sync(0xffffffffu, bv, o);
+        int i2 = __shfl_xor_sync(0xffffffffu, blog, o);
+        int p2 = __shfl_xor_sync(0xffffffffu, bph, o);
+        if (v2 > bv || (v2 == bv && i2 < blog)) {
+          bv = v2;
+          blog = i2;
+          bph = p2;
+        }
+      }
+      if (bph == t && blog != INT_MAX) {
+#pragma unroll
+        for (int c = 0; c < NB; ++c) cand_row[par][warp][c] = a[c];
+      }
+      if (lane == 0) {
+        cand_v[par][warp] = bv;
+        cand_i[par][warp] = blog;
+        cand_ph[par][warp] = bph;
+      }
+    };
+    __syncthreads();  // everyone has consumed the smem-path candidates of column 0
+    publish_reg(0, own ? cabs1(a[0]) : -1.0, own ? t : INT_MAX);
 #pragma unroll 1
-  for (int j = 0; j < NB; ++j) {
-    __syncthreads();  // B1
-    if (warp == 0) {
-      double v = lane < nwarp_rows ? cand_v[lane] : -2.0;
-      int p = lane < nwarp_rows ? cand_i[lane] : INT_MAX;
+    for (int j = 0; j < NB; ++j) {
+      const int par = j & 1;
+      __syncthreads();  // the only barrier of step j
+      if (j < 8) { DBG(10 + j) }
+      double v = lane < nwarp_rows ? cand_v[par][lane] : -2.0;
+      int p = lane < nwarp_rows ? cand_i[par][lane] : INT_MAX;
+      int ws = lane;
 #pragma unroll
       for (int o = 4; o; o >>= 1) {
         double v2 = __shfl_xor_sync(0xffffffffu, v, o);
         int i2 = __shfl_xor_sync(0xffffffffu, p, o);
-        argmax_merge(v, p, v2, i2);
+        int w2 = __shfl_xor_sync(0xffffffffu, ws, o);
+        if (v2 > v || (v2 == v && i2 < p)) {
+          v = v2;
+          p = i2;
+          ws = w2;
+        }
       }
-      p = __shfl_sync(0xffffffffu, p, 0);  // lanes 0..7 hold the reduction; broadcast
-      if (p == INT_MAX) p = j;              // empty / NaN column: keep row j
-      if (p != j && lane < NB) {
-        const double2 x = pn[lane * ldp + j];
-        pn[lane * ldp + j] = pn[lane * ldp + p];
-        pn[lane * ldp + p] = x;
-      }
-      __syncwarp();
-      if (lane == 0) {
+      p = __shfl_sync(0xffffffffu, p, 0);
+      ws = __shfl_sync(0xffffffffu, ws, 0);
+      if (j == 1) { DBG(20) }
+      int phj = -1;
+      const bool has = p != INT_MAX;
+      if (!has) p = j;  // no candidate (NaN column): keep logical row j in place
+      else phj = cand_ph[par][ws];
+      const double2 (&prow)[NB] = cand_row[par][has ? ws : 0];
+      if (tid == 0) {
         s_piv[j] = p;
         piv[k + j] = k + p;
-        const double2 pv = pn[j * ldp + j];  // pivot value, now in row j
-        if (k + j < n_true && hypot(pv.x, pv.y) <= tol) s_fail = min(s_fail, k + j);
-        s_inv = crcp(pv);
       }
+      // logical interchange j <-> p
+      int nl = mylog;
+      if (mylog == j) nl = p;
+      if (t == phj) nl = j;
+      if (phj < 0 && mylog == j) nl = j;
+      mylog = nl;
+      const double2 inv = has ? crcp_fast(prow[j]) : make_double2(0.0, 0.0);
+      if (j == 1) { DBG(22) }
+      const bool upd = own && mylog > j && has;
+      double bv = -1.0;
+#define GJR_CHUNK(C0)                                                          \
+  {                                                                            \
+    double2 aj = a[C0];                                                        \
+    _Pragma("unroll") for (int c = (C0) + 1; c < (C0) + 8 && c < NB; ++c)     \
+      if (c == j) aj = a[c];                                                   \
+    const double2 l = cmul(aj, inv);                                           \
+    const double2 lz = upd ? l : make_double2(0.0, 0.0);                       \
+    _Pragma("unroll") for (int c = (C0); c < NB; ++c) {                        \
+      const double2 lc = (c > j) ? lz : make_double2(0.0, 0.0);               \
+      const double2 pc = prow[c];                                              \
+      double2 x = a[c];                                                        \
+      x.x = fma(-lc.x, pc.x, fma(lc.y, pc.y, x.x));                            \
+      x.y = fma(-lc.x, pc.y, fma(-lc.y, pc.x, x.y));                           \
+      if (c == j + 1) bv = cabs1(x);                                           \
+      a[c] = (upd && c == j) ? l : x;                                          \
+    }                                                                          \
+  }
+      const int ch = j >> 3;
+      if (ch == 0) {
+        GJR_CHUNK(0)
+      } else if (ch == 1) {
+        GJR_CHUNK(8 < NB ? 8 : 0)
+      } else if (ch == 2) {
+        GJR_CHUNK(16 < NB ? 16 : 0)
+      } else {
+        GJR_CHUNK(24 < NB ? 24 : 0)
+      }
+#undef GJR_CHUNK
+      if (j == 1) { DBG(23) }
+      if (j + 1 < NB) publish_reg(par ^ 1, (own && mylog > j) ? bv : -1.0, (own && mylog > j) ? mylog : INT_MAX);
+      if (j == 1) { DBG(24) }
     }
-    __syncthreads();  // B2
-    const double2 inv = s_inv;
-    for (int r = j + 1 + tid; r < rows; r += PT) pn[j * ldp + r] = cmul(pn[j * ldp + r], inv);
-    __syncthreads();  // B3
+    __syncthreads();
+    int* fp = perm + (NB & 1) * rows;
+    if (own) {
+#pragma unroll
+      for (int c = 0; c < NB; ++c) pn[c * ldp + t] = a[c];
+      fp[mylog] = t;
+    }
+  } else {
+#pragma unroll 1
+  for (int j = 0; j < NB; ++j) {
+    const int par = j & 1;
+    __syncthreads();  // the only barrier of step j
+    if (j < 8) { DBG(10 + j) }
+    double v = lane < nwarp_rows ? cand_v[par][lane] : -2.0;
+    int p = lane < nwarp_rows ? cand_i[par][lane] : INT_MAX;
+#pragma unroll
+    for (int o = 4; o; o >>= 1) {
+      double v2 = __shfl_xor_sync(0xffffffffu, v, o);
+      int i2 = __shfl_xor_sync(0xffffffffu, p, o);
+      argmax_merge(v, p, v2, i2);
+    }
+    p = __shfl_sync(0xffffffffu, p, 0);
+    if (j == 1) { DBG(20) }
+    if (p == INT_MAX) p = j;  // empty / NaN column: keep row j
+    const int* pold = perm + par * rows;
+    int* pnew = perm + (par ^ 1) * rows;
+    const int phj = pold[p];  // physical row of the pivot = new logical row j
+    const int php = pold[j];  // physical row of old logical row j = new logical row p
+    for (int r = tid; r < rows; r += PT) pnew[r] = (r == j) ? phj : ((r == p) ? php : pold[r]);
+    if (tid == 0) {
+      s_piv[j] = p;
+      piv[k + j] = k + p;
+    }
+    if (j == 1) { DBG(21) }
+    const double2 inv = crcp_fast(pn[j * ldp + phj]);
+    if (j == 1) { DBG(22) }
     double bv = -1.0;
     int bi = INT_MAX;
-    for (int r = j + 1 + rt; r < rows; r += 256) {
-      const double2 l = pn[j * ldp + r];
-      for (int c = j + 1 + cg; c < NB; c += 4) {
-        const double2 u = pn[c * ldp + j];
-        double2 x = pn[c * ldp + r];
-        x.x = fma(-l.x, u.x, fma(l.y, u.y, x.x));
-        x.y = fma(-l.x, u.y, fma(-l.y, u.x, x.y));
-        pn[c * ldp + r] = x;
-        if (c == j + 1) {
-          const double a = cabs1(x);
+    // each logical row r > j is owned by exactly one thread: it scales its
+    // multiplier in place and updates its trailing columns in batches of 8
+    for (int r = j + 1 + tid; r < rows; r += PT) {
+      const int ph = (r == p) ? php : pold[r];
+      const double2 l = cmul(pn[j * ldp + ph], inv);
+      pn[j * ldp + ph] = l;
+#pragma unroll 1
+      for (int c0 = j + 1; c0 < NB; c0 += 8) {
+        double2 x[8], u[8];
+#pragma unroll
+        for (int i = 0; i < 8; ++i) {
+          const int c = c0 + i;
+          if (c < NB) {
+            u[i] = pn[c * ldp + phj];
+            x[i] = pn[c * ldp + ph];
+          }
+        }
+#pragma unroll
+        for (int i = 0; i < 8; ++i) {
+          const int c = c0 + i;
+          if (c < NB) {
+            x[i].x = fma(-l.x, u[i].x, fma(l.y, u[i].y, x[i].x));
+            x[i].y = fma(-l.x, u[i].y, fma(-l.y, u[i].x, x[i].y));
+            pn[c * ldp + ph] = x[i];
+          }
+        }
+        if (c0 == j + 1) {  // column j+1 candidates
+          const double a = cabs1(x[0]);
           if (a > bv) {
             bv = a;
             bi = r;
@@ -227,9 +378,19 @@ __global__ void __launch_bounds__(PT, 1)
         }
       }
     }
-    if (j + 1 < NB && warp < nwarp_rows) publish(bv, bi);
+    if (j == 1) { DBG(23) }
+    if (j + 1 < NB && warp < nwarp_rows) publish(par ^ 1, bv, bi);
+    if (j == 1) { DBG(24) }
   }
   __syncthreads();
+  }
+  const int* fperm = perm + (NB & 1) * rows;  // final logical -> physical rows
+  __syncthreads();
+  DBG(2)
+  if (tid < NB && k + tid < n_true) {  // negligible-pivot test on the U diagonal
+    const double2 d = pn[tid * ldp + fperm[tid]];
+    if (hypot(d.x, d.y) <= tol) atomicMin(&s_fail, k + tid);
+  }
 
   // ---- row map of the interchanges (new row r holds old row src(r))
   for (int r = tid; r < n; r += PT) {
@@ -248,32 +409,35 @@ __global__ void __launch_bounds__(PT, 1)
     if (r >= k && r < k + NB) s_src[r - k] = src;
   }
 
-  // ---- Pinv = U^{-1} L^{-1} of the pivot block (panel rows 0..NB-1): one warp per column
-  if (warp < NB) {
+  // ---- Pinv = U^{-1} L^{-1} of the pivot block (logical rows 0..NB-1): warp per column
+  {
     double2* __restrict__ pinv = S.pinv + (long long)b * NB * NB;
     const bool act = lane < NB;
     const int row = act ? lane : 0;
-    const int c = warp;
-    double2 t = make_double2(lane == c ? 1.0 : 0.0, 0.0);
+    const int prow_ph = fperm[row];
+    const double2 dinv = crcp_fast(pn[row * ldp + prow_ph]);
+#pragma unroll 1
+    for (int c = warp; c < NB; c += PT / 32) {
+      double2 t = make_double2(lane == c ? 1.0 : 0.0, 0.0);
 #pragma unroll
-    for (int q = 0; q < NB; ++q) {  // forward: unit lower L
-      const double2 lq = pn[q * ldp + row];
-      double2 tq;
-      tq.x = __shfl_sync(0xffffffffu, t.x, q);
-      tq.y = __shfl_sync(0xffffffffu, t.y, q);
-      if (act && lane > q) t = csub(t, cmul(lq, tq));
-    }
-    const double2 dinv = crcp(pn[row * ldp + row]);
+      for (int q = 0; q < NB; ++q) {  // forward: unit lower L
+        const double2 lq = pn[q * ldp + prow_ph];
+        double2 tq;
+        tq.x = __shfl_sync(0xffffffffu, t.x, q);
+        tq.y = __shfl_sync(0xffffffffu, t.y, q);
+        if (act && lane > q) t = csub(t, cmul(lq, tq));
+      }
 #pragma unroll
-    for (int q = NB - 1; q >= 0; --q) {  // backward: upper U
-      const double2 uq = pn[q * ldp + row];
-      if (lane == q) t = cmul(t, dinv);
-      double2 xq;
-      xq.x = __shfl_sync(0xffffffffu, t.x, q);
-      xq.y = __shfl_sync(0xffffffffu, t.y, q);
-      if (lane < q) t = csub(t, cmul(uq, xq));
+      for (int q = NB - 1; q >= 0; --q) {  // backward: upper U
+        const double2 uq = pn[q * ldp + prow_ph];
+        if (lane == q) t = cmul(t, dinv);
+        double2 xq;
+        xq.x = __shfl_sync(0xffffffffu, t.x, q);
+        xq.y = __shfl_sync(0xffffffffu, t.y, q);
+        if (lane < q) t = csub(t, cmul(uq, xq));
+      }
+      if (act) pinv[c * NB + lane] = t;
     }
-    if (act) pinv[c * NB + lane] = t;
   }
   __syncthreads();
 
@@ -318,6 +482,7 @@ __global__ void __launch_bounds__(PT, 1)
     }
   }
   __syncthreads();
+  DBG(4)
   if (tid == 0 && s_fail != INT_MAX && status[b] < 0) status[b] = s_fail;
 }
 
@@ -349,6 +514,8 @@ __global__ void build_colmap_kernel(const int* __restrict__ piv0, int* __restric
 
 }  // namespace
 
+extern "C" int bbsi_debug_zinv(long long* out) { return (int)cudaMemcpyFromSymbol(out, g_zinv_dbg, sizeof(long long) * 64); }
+
 size_t zinv_scratch_bytes(int n, int batch) {
   GjScratch s;
   return carve(s, nullptr, n, pick_nb(n), batch) + 256;
@@ -361,7 +528,7 @@ cudaError_t zinv_batched(double2* M, long long ld, long long bstride, int n, int
   const int nb = pick_nb(n);
   GjScratch S;
   carve(S, scratch, n, nb, batch);
-  const size_t smem = size_t(nb) * (n + 1) * sizeof(double2);
+  const size_t smem = size_t(nb) * (n + 1) * sizeof(double2) + 2 * size_t(n) * sizeof(int);
   static size_t attr16 = 0, attr32 = 0;
   cudaError_t e;
   if (nb == 32 && smem > attr32) {
