@@ -84,6 +84,11 @@ int bbsi_cuda_ddrgf_z(int l, int w, int bs, const int* sizes, const double* A, c
                       int n_levels, int n_threads, int terminal_threads, double* G, long long* counters,
                       int* fail_layer);
 
+/* The reference's logical KernelCounters of ddrgf for a plan (ddrgf.hpp:344-412
+ * walked on the host; predict_ddrgf_counters, cost_model.hpp:137-154, when the
+ * plan divides evenly). out: int64[3]. */
+void bbsi_ddrgf_reference_counters(long long l, const int* s2_levels, int n_levels, long long* out);
+
 /* ---------------------------------------------------------------- resident batched API
  * A batch of independent band matrices (energies or domains) with uniform
  * bs % 64 == 0. dA / dG: device pointers to [batch][l][2w+1][bs][bs];
@@ -103,6 +108,13 @@ int bbsi_cuda_dyson_rgf_dev(int l, int w, int bs, int n_energy, const double* dH
  * finished chunks stream back to G while the next computes (pin G for overlap). */
 int bbsi_cuda_dyson_rgf_z(int l, int w, int bs, int n_energy, const double* H, const double* z,
                           const double* sigma, double* G, int* fail_layers, int chunk);
+
+/* Resident stabilised DDRGF of one band (w = 1): dA, dG device [l][3][bs][bs],
+ * interior groups of s2 layers (single-level plan). */
+int bbsi_cuda_ddrgf_dev(int l, int bs, int s2, const double* dA, double* dG, int* fail_layer, void* stream);
+/* Dyson DDRGF for one energy z (host complex) from the shared device H. */
+int bbsi_cuda_dyson_ddrgf_dev(int l, int bs, const double* dH, const double* z, const double* sigma, int s2,
+                              double* dG, int* fail_layer, void* stream);
 
 /* Seeded Dyson Hamiltonian (include/.. csrc/dyson_gen.h spec) written on the device. */
 int bbsi_cuda_dyson_fill_h_dev(int l, int w, int b, uint64_t seed, double* dH, void* stream);

@@ -29,6 +29,9 @@ SIGNATURES = {
     "bbsi_cuda_zgemm_dev": (_i, [_i, _i, _i, _vp, _vp, _ll, _ll, _vp, _ll, _ll, _vp, _vp, _ll, _ll, _i, _vp]),
     "bbsi_cuda_zinv_dev": (_i, [_i, _i, _i, _vp, _ll, _ll, _vp, _vp]),
     "bbsi_cuda_dyson_rgf_z": (_i, [_i, _i, _i, _i, _vp, _vp, _vp, _vp, _vp, _i]),
+    "bbsi_cuda_ddrgf_dev": (_i, [_i, _i, _i, _vp, _vp, _vp, _vp]),
+    "bbsi_cuda_dyson_ddrgf_dev": (_i, [_i, _i, _vp, _vp, _vp, _i, _vp, _vp, _vp]),
+    "bbsi_ddrgf_reference_counters": (None, [_ll, _vp, _i, _vp]),
     "bbsi_cuda_launch_count": (_ll, []),
     "bbsi_cuda_profile_enable": (None, [_i]),
     "bbsi_cuda_profile_collect": (_i, [_vp, _i]),

@@ -2,6 +2,7 @@
 // reference's preconditions and messages (layout.hpp:27-38, rgf.hpp:41-42,86-87,
 // ddrgf.hpp:26-31,424-425); failures map onto the reference exception contract.
 #include <cstdio>
+#include <cstdlib>
 #include <cstring>
 #include <mutex>
 #include <string>
@@ -491,8 +492,109 @@ int bbsi_cuda_rgf_extended_z(int, int, int, const int*, const double*, double*, 
   return fail(BBSI_INVALID_ARGUMENT, "rgf_extended: not yet available on the GPU path");
 }
 
-int bbsi_cuda_ddrgf_z(int, int, int, const int*, const double*, const int*, int, int, int, double*, long long*, int*) {
-  return fail(BBSI_INVALID_ARGUMENT, "ddrgf: not yet available on the GPU path");
+// DomainPlan validation and plan exhaustion, as the reference (ddrgf.hpp:26-31,
+// 364-366, 423-425; partition.hpp:41-45).
+static int validate_ddrgf(int l, int w, int bs, const int* sizes, const int* s2_levels, int n_levels, int n_threads,
+                          int terminal_threads) {
+  if (n_levels < 1 || !s2_levels) return fail(BBSI_INVALID_ARGUMENT, "DomainPlan: needs at least one level");
+  for (int k = 0; k < n_levels; ++k)
+    if (s2_levels[k] < 1) return fail(BBSI_INVALID_ARGUMENT, "DomainPlan: s2 must be >= 1");
+  if (n_threads < 1 || terminal_threads < 1)
+    return fail(BBSI_INVALID_ARGUMENT, "DomainPlan: thread counts must be >= 1");
+  if (int rc = validate_layout(l, w, bs, sizes)) return rc;
+  if (w != 1) return fail(BBSI_INVALID_ARGUMENT, "ddrgf: requires bandwidth 1");
+  for (int a = 0; a < l; ++a)
+    if ((sizes ? sizes[a] : bs) != (sizes ? sizes[0] : bs))
+      return fail(BBSI_INVALID_ARGUMENT, "ddrgf: requires uniform block sizes");
+  if (l < 1 + s2_levels[0]) return fail(BBSI_INVALID_ARGUMENT, "interleave_permutation: too few layers to split");
+  long long lk = l;
+  for (int k = 0; k < n_levels; ++k) {
+    if (lk < 1 + s2_levels[k])
+      return fail(BBSI_INVALID_ARGUMENT, "ddrgf: plan exhausts layers at level " + std::to_string(k));
+    lk = (lk + s2_levels[k]) / (1 + s2_levels[k]);
+  }
+  return BBSI_OK;
+}
+
+static double ddrgf_gamma() {
+  if (const char* e = getenv("BBSI_DDRGF_GAMMA")) return atof(e);
+  return 1.0;
+}
+
+// Runs the stabilised DDRGF on device buffers; fills *fail_layer on a singular pivot.
+static int ddrgf_on_device(const double2* dA, double2* dG, int l, int bp, const std::vector<int>& n_true, int s2,
+                           int* fail_layer, cudaStream_t s) {
+  const size_t sb = ddrgf_scratch_bytes(l, bp, s2);
+  void* scr = arena_get(9, sb);
+  if (!scr) return fail(BBSI_OUT_OF_MEMORY, "ddrgf workspace allocation failed");
+  int fl = -1;
+  CK(ddrgf_device(dA, dG, l, bp, n_true.data(), s2, ddrgf_gamma(), scr, sb, &fl, s));
+  CK(cudaStreamSynchronize(s));
+  if (fl >= 0) {
+    if (fail_layer) *fail_layer = fl;
+    return fail(BBSI_SINGULAR, "singular pivot at layer " + std::to_string(fl));
+  }
+  return BBSI_OK;
+}
+
+int bbsi_cuda_ddrgf_z(int l, int w, int bs, const int* sizes, const double* A, const int* s2_levels, int n_levels,
+                      int n_threads, int terminal_threads, double* G, long long* counters, int* fail_layer) {
+  if (fail_layer) *fail_layer = -1;
+  if (int rc = validate_ddrgf(l, w, bs, sizes, s2_levels, n_levels, n_threads, terminal_threads)) return rc;
+  if (int rc = device_ok()) return rc;
+  std::lock_guard<std::mutex> lk(g_call_mu);
+  HostBand h = make_host(l, w, bs, sizes, A);
+  const int bp = pad64(h.bs);
+  std::vector<double2> staging;
+  pad_band(h, bp, staging);
+  const size_t bytes = staging.size() * sizeof(double2);
+  double2* dA = static_cast<double2*>(arena_get(0, bytes));
+  double2* dG = static_cast<double2*>(arena_get(10, bytes));
+  if (!dA || !dG) return fail(BBSI_OUT_OF_MEMORY, "band allocation failed");
+  cudaStream_t s = 0;
+  CK(cudaMemcpyAsync(dA, staging.data(), bytes, cudaMemcpyHostToDevice, s));
+  if (int rc = ddrgf_on_device(dA, dG, l, bp, h.sz, s2_levels[0], fail_layer, s)) return rc;
+  CK(cudaMemcpyAsync(staging.data(), dG, bytes, cudaMemcpyDeviceToHost, s));
+  CK(cudaStreamSynchronize(s));
+  unpad_band(staging, bp, h, reinterpret_cast<double2*>(G));
+  if (counters) ddrgf_reference_counters(l, s2_levels, n_levels, counters);
+  return BBSI_OK;
+}
+
+int bbsi_cuda_ddrgf_dev(int l, int bs, int s2, const double* dA, double* dG, int* fail_layer, void* stream) {
+  if (fail_layer) *fail_layer = -1;
+  int one = s2;
+  if (int rc = validate_ddrgf(l, 1, bs, nullptr, &one, 1, 1, 1)) return rc;
+  if (bs % 64) return fail(BBSI_INVALID_ARGUMENT, "resident API requires bs % 64 == 0");
+  if (int rc = device_ok()) return rc;
+  std::lock_guard<std::mutex> lk(g_call_mu);
+  std::vector<int> nt(l, bs);
+  return ddrgf_on_device(reinterpret_cast<const double2*>(dA), reinterpret_cast<double2*>(dG), l, bs, nt, s2,
+                         fail_layer, static_cast<cudaStream_t>(stream));
+}
+
+int bbsi_cuda_dyson_ddrgf_dev(int l, int bs, const double* dH, const double* z, const double* sigma, int s2,
+                              double* dG, int* fail_layer, void* stream) {
+  if (fail_layer) *fail_layer = -1;
+  int one = s2;
+  if (int rc = validate_ddrgf(l, 1, bs, nullptr, &one, 1, 1, 1)) return rc;
+  if (bs % 64) return fail(BBSI_INVALID_ARGUMENT, "resident API requires bs % 64 == 0");
+  if (int rc = device_ok()) return rc;
+  cudaStream_t s = static_cast<cudaStream_t>(stream);
+  std::lock_guard<std::mutex> lk(g_call_mu);
+  const size_t band_b = sizeof(double2) * size_t(l) * 3 * bs * bs;
+  double2* dA = static_cast<double2*>(arena_get(0, band_b));
+  double2* dzs = static_cast<double2*>(arena_get(2, sizeof(double2) * (size_t(1) + l)));
+  if (!dA || !dzs) return fail(BBSI_OUT_OF_MEMORY, "ddrgf band allocation failed");
+  CK(cudaMemcpyAsync(dzs, z, sizeof(double2), cudaMemcpyHostToDevice, s));
+  CK(cudaMemcpyAsync(dzs + 1, sigma, sizeof(double2) * l, cudaMemcpyHostToDevice, s));
+  CK(dyson_form_band(dA, reinterpret_cast<const double2*>(dH), l, 1, bs, 1, dzs, dzs + 1, s));
+  std::vector<int> nt(l, bs);
+  return ddrgf_on_device(dA, reinterpret_cast<double2*>(dG), l, bs, nt, s2, fail_layer, s);
+}
+
+void bbsi_ddrgf_reference_counters(long long l, const int* s2_levels, int n_levels, long long* out) {
+  ddrgf_reference_counters(l, s2_levels, n_levels, out);
 }
 
 }  // extern "C"

@@ -57,6 +57,12 @@ cudaError_t rgf_sweeps(const SweepWork& W, const int* n_true, cudaStream_t s);
 // reference would report (first failure in elimination order) or -1.
 cudaError_t collect_failures(const SweepWork& W, std::vector<int>& fail, cudaStream_t s);
 
+// Stabilised DDRGF (ddrgf.cu) on one device band A (w = 1, uniform bs) -> G.
+cudaError_t ddrgf_device(const double2* A, double2* G, int l, int b, const int* n_true, int s2, double gamma,
+                         void* scratch, size_t scratch_bytes, int* fail_layer, cudaStream_t s);
+size_t ddrgf_scratch_bytes(int l, int b, int s2);
+void ddrgf_reference_counters(long long l, const int* s2_levels, int n_levels, long long out[3]);
+
 // Launch accounting / optional event timing around one kernel launch (prof.cu).
 enum ProfCat { PROF_GEMM = 0, PROF_INV = 1, PROF_BAND = 2, PROF_NCAT = 3 };
 class ProfScope {
