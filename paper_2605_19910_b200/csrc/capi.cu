@@ -487,9 +487,116 @@ int bbsi_cuda_dyson_rgf_z(int l, int w, int bs, int n_energy, const double* H, c
   return bad ? fail(BBSI_SINGULAR, "singular Schur pivot in at least one energy") : BBSI_OK;
 }
 
-int bbsi_cuda_rgf_extended_z(int, int, int, const int*, const double*, double*, double*, double*, double*, double*,
-                             long long*, int*) {
-  return fail(BBSI_INVALID_ARGUMENT, "rgf_extended: not yet available on the GPU path");
+// rgf_extended (rgf.hpp:209-270): the tridiagonal core plus the full first/last
+// block rows and columns of the inverse. The reference carries whole columns and
+// rows through the downward sweep ((l-1)(l-2) extra GEMMs); here they come from
+// O(l) chains over the stored multipliers after the sweep:
+//   first row  G[0,a]   = -G[0,a-1] um_a            (left to right)
+//   first col  G[a,0]   = -lm_a G[a-1,0]
+//   last col   G[a,l-1] = G[a,a] Q_a,  Q_a = -um_{a+1} Q_{a+1},  Q_{l-1} = I
+//   last row   G[l-1,a] = R_a G[a,a],  R_a = -R_{a+1} lm_{a+1},  R_{l-1} = I
+// with the entries that lie in the band copied from the core, as the reference does.
+int bbsi_cuda_rgf_extended_z(int l, int w, int bs, const int* sizes, const double* A, double* G, double* first_row,
+                             double* last_row, double* first_col, double* last_col, long long* counters,
+                             int* fail_layer) {
+  if (fail_layer) *fail_layer = -1;
+  if (int rc = validate_layout(l, w, bs, sizes)) return rc;
+  if (w != 1 && l != 1) return fail(BBSI_INVALID_ARGUMENT, "rgf_extended: requires bandwidth 1");
+  if (int rc = device_ok()) return rc;
+  std::lock_guard<std::mutex> lk(g_call_mu);
+  HostBand h = make_host(l, w, bs, sizes, A);
+  const int bp = pad64(h.bs);
+  const long long bb = (long long)bp * bp;
+  std::vector<double2> staging;
+  pad_band(h, bp, staging);
+  const size_t bytes = staging.size() * sizeof(double2);
+  double2* dG = static_cast<double2*>(arena_get(0, bytes));
+  double2* halo = static_cast<double2*>(arena_get(11, sizeof(double2) * size_t(4 * l + 4) * bb));
+  if (!dG || !halo) return fail(BBSI_OUT_OF_MEMORY, "rgf_extended allocation failed");
+  cudaStream_t s = 0;
+  CK(cudaMemcpyAsync(dG, staging.data(), bytes, cudaMemcpyHostToDevice, s));
+  SweepWork W;
+  W.l = l;
+  W.w = w;
+  W.bs = bp;
+  W.batch = 1;
+  W.G = dG;
+  W.g_bstride = (long long)l * (2 * w + 1) * bb;
+  std::vector<int> fails;
+  if (int rc = run_sweeps(W, h.sz, fails, s)) return rc;
+  if (fails[0] >= 0) {
+    if (fail_layer) *fail_layer = fails[0];
+    return fail(BBSI_SINGULAR, "singular Schur pivot at layer " + std::to_string(fails[0]));
+  }
+  const int ns = 2 * w + 1;
+  auto gs = [&](int a, int off) { return dG + ((long long)a * ns + off + w) * bb; };
+  double2* FR = halo;                 // [l]
+  double2* LR = halo + (long long)l * bb;
+  double2* FC = halo + 2LL * l * bb;
+  double2* LC = halo + 3LL * l * bb;
+  double2* Q = halo + 4LL * l * bb;   // [4] accumulators (P, S ping-pong)
+  const double2 m1 = make_double2(-1.0, 0.0), p1 = make_double2(1.0, 0.0);
+  auto cp = [&](double2* d, const double2* x) {
+    return cudaMemcpyAsync(d, x, bb * sizeof(double2), cudaMemcpyDeviceToDevice, s);
+  };
+  auto um = [&](int a) { return W.UM + (long long)a * bb; };
+  auto lm = [&](int a) { return W.LM + (long long)a * bb; };
+  CK(cp(FR, gs(0, 0)));
+  CK(cp(FC, gs(0, 0)));
+  CK(cp(LC + (l - 1) * bb, gs(l - 1, 0)));
+  CK(cp(LR + (l - 1) * bb, gs(l - 1, 0)));
+  if (l >= 2) {
+    CK(cp(FR + bb, gs(0, 1)));
+    CK(cp(FC + bb, gs(1, -1)));
+    CK(cp(LC + (l - 2) * bb, gs(l - 2, 1)));
+    CK(cp(LR + (l - 2) * bb, gs(l - 1, -1)));
+  }
+  for (int a = 2; a < l; ++a) {
+    CK(zmm(bp, 1, m1, zblk(FR + (a - 1) * bb, bp), zblk(um(a), bp), 0.0, zblk(FR + a * bb, bp), s));
+    CK(zmm(bp, 1, m1, zblk(lm(a), bp), zblk(FC + (a - 1) * bb, bp), 0.0, zblk(FC + a * bb, bp), s));
+  }
+  if (l >= 3) {
+    // P_a = um_{a+1} ... um_{l-1},  S_a = lm_{l-1} ... lm_{a+1};  sign (-1)^(l-1-a) applied at the end
+    double2* Pp[2] = {Q, Q + bb};
+    double2* Sp[2] = {Q + 2 * bb, Q + 3 * bb};
+    CK(cp(Pp[0], um(l - 1)));
+    CK(cp(Sp[0], lm(l - 1)));
+    int cur = 0;
+    for (int a = l - 3; a >= 0; --a) {
+      CK(zmm(bp, 1, p1, zblk(um(a + 1), bp), zblk(Pp[cur], bp), 0.0, zblk(Pp[cur ^ 1], bp), s));
+      CK(zmm(bp, 1, p1, zblk(Sp[cur], bp), zblk(lm(a + 1), bp), 0.0, zblk(Sp[cur ^ 1], bp), s));
+      cur ^= 1;
+      const double2 sg = ((l - 1 - a) % 2) ? m1 : p1;
+      CK(zmm(bp, 1, sg, zblk(gs(a, 0), bp), zblk(Pp[cur], bp), 0.0, zblk(LC + a * bb, bp), s));
+      CK(zmm(bp, 1, sg, zblk(Sp[cur], bp), zblk(gs(a, 0), bp), 0.0, zblk(LR + a * bb, bp), s));
+    }
+  }
+  std::vector<double2> hh(size_t(4) * l * bb);
+  CK(cudaMemcpyAsync(staging.data(), dG, bytes, cudaMemcpyDeviceToHost, s));
+  CK(cudaMemcpyAsync(hh.data(), halo, hh.size() * sizeof(double2), cudaMemcpyDeviceToHost, s));
+  CK(cudaStreamSynchronize(s));
+  unpad_band(staging, bp, h, reinterpret_cast<double2*>(G));
+  // halo blocks: first_row[b]: rows(0) x cols(b); last_row[b]: rows(l-1) x cols(b);
+  //              first_col[a]: rows(a) x cols(0); last_col[a]: rows(a) x cols(l-1)
+  auto put = [&](double* dst, int which, int rows_of, int cols_of) {
+    if (!dst) return;
+    double2* d = reinterpret_cast<double2*>(dst);
+    std::memset(d, 0, sizeof(double2) * size_t(l) * h.bs * h.bs);
+    for (int k = 0; k < l; ++k) {
+      const int r = rows_of >= 0 ? h.sz[rows_of] : h.sz[k];
+      const int c = cols_of >= 0 ? h.sz[cols_of] : h.sz[k];
+      const double2* src = hh.data() + ((size_t)which * l + k) * bb;
+      for (int j = 0; j < c; ++j)
+        std::memcpy(d + (size_t)k * h.bs * h.bs + (size_t)j * h.bs, src + (size_t)j * bp, sizeof(double2) * r);
+    }
+  };
+  put(first_row, 0, 0, -1);
+  put(last_row, 1, l - 1, -1);
+  put(first_col, 2, -1, 0);
+  put(last_col, 3, -1, l - 1);
+  long long L = l;
+  put_counters(counters, 4 * (L - 1) + (L <= 2 ? 0 : (L - 1) * (L - 2)), L, 3 * L - 2);
+  return BBSI_OK;
 }
 
 // DomainPlan validation and plan exhaustion, as the reference (ddrgf.hpp:26-31,

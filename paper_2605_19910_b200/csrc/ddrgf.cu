@@ -134,6 +134,26 @@ Part partition(int l, int s2) {
 
 }  // namespace
 
+ZOp zblk(const double2* p, int b, long long bstride) { return blk(p, b, bstride); }
+
+cudaError_t zmm(int b, int batch, double2 alpha, ZOp A, ZOp B, double beta, ZOp C, cudaStream_t s) {
+  ZGemmGroup g{};
+  g.batch = batch;
+  g.bs = 64;
+  g.nprob = 1;
+  ZGemmProblem& p = g.prob[0];
+  p.M = b;
+  p.N = b;
+  p.K = b;
+  p.alpha = alpha;
+  p.beta = make_double2(beta, 0.0);
+  p.A = A;
+  p.B = B;
+  p.C = C;
+  p.D = C;
+  return zgemm_grouped(g, s);
+}
+
 cudaError_t ddrgf_device(const double2* A, double2* G, int l, int b, const int* n_true, int s2, double gamma,
                          void* scratch, size_t scratch_bytes, int* fail_layer, cudaStream_t s) {
   *fail_layer = -1;

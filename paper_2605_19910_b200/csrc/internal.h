@@ -57,6 +57,11 @@ cudaError_t rgf_sweeps(const SweepWork& W, const int* n_true, cudaStream_t s);
 // reference would report (first failure in elimination order) or -1.
 cudaError_t collect_failures(const SweepWork& W, std::vector<int>& fail, cudaStream_t s);
 
+// Small b x b helpers (ddrgf.cu): plain block operand (ld = b) and
+// D = alpha*A*B + beta*C over `batch` products (C may alias D).
+ZOp zblk(const double2* p, int b, long long bstride = 0);
+cudaError_t zmm(int b, int batch, double2 alpha, ZOp A, ZOp B, double beta, ZOp C, cudaStream_t s);
+
 // Stabilised DDRGF (ddrgf.cu) on one device band A (w = 1, uniform bs) -> G.
 cudaError_t ddrgf_device(const double2* A, double2* G, int l, int b, const int* n_true, int s2, double gamma,
                          void* scratch, size_t scratch_bytes, int* fail_layer, cudaStream_t s);

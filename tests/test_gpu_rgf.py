@@ -139,3 +139,49 @@ def test_padded_and_native_block_sizes(gpu, l, b, w):
     m = O.random_spd_like(O.make_layout(l, b, w), 1000 + l + b + w, 2.0)
     g, _ = P.rgf_ndiag(to_product(m))
     assert max_err(g, O.rgf_ndiag(m)[0]) <= 1e-12
+
+
+@pytest.mark.parametrize("l", [1, 2, 3, 5, 6])
+def test_extended_halos_equal_dense_inverse(gpu, l):
+    """test_rgf.cpp:97-123"""
+    m = O.random_spd_like(O.make_layout(l, 3, 0 if l == 1 else 1), 200 + l, 2.0)
+    ext, c = P.rgf_extended(to_product(m))
+    assert c.as_tuple() == O.predict_extended_counters(l).as_tuple()
+    dense = np.linalg.inv(O.to_dense(m))
+
+    def slab(a, b):
+        return dense[3 * a:3 * a + 3, 3 * b:3 * b + 3]
+
+    for b in range(l):
+        assert O.rel_frobenius_error(ext.first_row[b], slab(0, b)) <= 1e-10
+        assert O.rel_frobenius_error(ext.last_row[b], slab(l - 1, b)) <= 1e-10
+        assert O.rel_frobenius_error(ext.first_col[b], slab(b, 0)) <= 1e-10
+        assert O.rel_frobenius_error(ext.last_col[b], slab(b, l - 1)) <= 1e-10
+    g, _ = P.rgf_tridiag(to_product(m))
+    assert np.array_equal(ext.core.data, g.data)
+
+
+def test_extended_overlaps_are_exact_copies(gpu):
+    """test_rgf.cpp:125-135"""
+    m = O.random_spd_like(O.make_layout(6, 2, 1), 201, 2.0)
+    ext, _ = P.rgf_extended(to_product(m))
+    core = ext.core
+    assert np.array_equal(ext.first_row[0], core.block(0, 0))
+    assert np.array_equal(ext.first_row[1], core.block(0, 1))
+    assert np.array_equal(ext.last_row[5], core.block(5, 0))
+    assert np.array_equal(ext.last_row[4], core.block(5, -1))
+    assert np.array_equal(ext.first_col[1], core.block(1, -1))
+    assert np.array_equal(ext.last_col[4], core.block(4, 1))
+
+
+def test_extended_vs_reference_on_dyson_blocks(gpu):
+    """Halos at b = 64 on a Dyson matrix against the reference rgf_extended (numpy restatement)."""
+    from oracle import dyson_oracle as DO
+
+    a = DO.dyson_matrix(DO.hamiltonian(9, 1, 64, 5), complex(0.2, 1e-3), 1)
+    ext, _ = P.rgf_extended(to_product(a))
+    ref, _ = O.rgf_extended(a)
+    for k in range(9):
+        for got, exp in ((ext.first_row[k], ref.first_row[k]), (ext.last_row[k], ref.last_row[k]),
+                         (ext.first_col[k], ref.first_col[k]), (ext.last_col[k], ref.last_col[k])):
+            assert O.rel_frobenius_error(got, exp) <= 1e-10
