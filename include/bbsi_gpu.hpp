@@ -70,6 +70,7 @@ inline BlockBandedMatrix<cd> from_slots(const BlockLayout& lay, Slots& s) {
   return g;
 }
 
+// (evaluate the C call before reading fail_layer: argument order is unspecified)
 inline void check(int rc, int fail_layer) {
   if (rc == BBSI_OK) return;
   const std::string msg = bbsi_cuda_last_error();
@@ -105,9 +106,9 @@ inline std::pair<BlockBandedMatrix<cd>, KernelCounters> rgf_tridiag(const BlockB
   std::vector<cd> g(s.data.size());
   long long c[3];
   int fl = -1;
-  detail::check(bbsi_cuda_rgf_tridiag_z(s.l, s.w, s.bs, s.sizes.data(), reinterpret_cast<const double*>(s.data.data()),
-                                        reinterpret_cast<double*>(g.data()), c, &fl),
-                fl);
+  const int rc = bbsi_cuda_rgf_tridiag_z(s.l, s.w, s.bs, s.sizes.data(), reinterpret_cast<const double*>(s.data.data()),
+                                        reinterpret_cast<double*>(g.data()), c, &fl);
+  detail::check(rc, fl);
   if (trace) trace->max_update_offset = 0;
   s.data.swap(g);
   return {detail::from_slots(m.layout(), s), detail::counters(c)};
@@ -119,9 +120,9 @@ inline std::pair<BlockBandedMatrix<cd>, KernelCounters> rgf_ndiag(const BlockBan
   std::vector<cd> g(s.data.size());
   long long c[3];
   int fl = -1, mo = trace ? trace->max_update_offset : 0;
-  detail::check(bbsi_cuda_rgf_ndiag_z(s.l, s.w, s.bs, s.sizes.data(), reinterpret_cast<const double*>(s.data.data()),
-                                      reinterpret_cast<double*>(g.data()), c, &mo, &fl),
-                fl);
+  const int rc = bbsi_cuda_rgf_ndiag_z(s.l, s.w, s.bs, s.sizes.data(), reinterpret_cast<const double*>(s.data.data()),
+                                      reinterpret_cast<double*>(g.data()), c, &mo, &fl);
+  detail::check(rc, fl);
   if (trace) trace->max_update_offset = mo;
   s.data.swap(g);
   return {detail::from_slots(m.layout(), s), detail::counters(c)};
@@ -132,9 +133,9 @@ inline std::pair<BlockBandedMatrix<cd>, KernelCounters> rgf_fused(const BlockBan
   std::vector<cd> g(s.data.size());
   long long c[3];
   int fl = -1;
-  detail::check(bbsi_cuda_rgf_fused_z(s.l, s.w, s.bs, s.sizes.data(), reinterpret_cast<const double*>(s.data.data()),
-                                      reinterpret_cast<double*>(g.data()), c, &fl),
-                fl);
+  const int rc = bbsi_cuda_rgf_fused_z(s.l, s.w, s.bs, s.sizes.data(), reinterpret_cast<const double*>(s.data.data()),
+                                      reinterpret_cast<double*>(g.data()), c, &fl);
+  detail::check(rc, fl);
   s.data.swap(g);
   return {detail::from_slots(m.layout(), s), detail::counters(c)};
 }
@@ -146,12 +147,11 @@ inline std::pair<ExtendedInverse<cd>, KernelCounters> rgf_extended(const BlockBa
   std::vector<cd> fr(hn), lr(hn), fc(hn), lc(hn);
   long long c[3];
   int fl = -1;
-  detail::check(
-      bbsi_cuda_rgf_extended_z(s.l, s.w, s.bs, s.sizes.data(), reinterpret_cast<const double*>(s.data.data()),
+  const int rc = bbsi_cuda_rgf_extended_z(s.l, s.w, s.bs, s.sizes.data(), reinterpret_cast<const double*>(s.data.data()),
                                reinterpret_cast<double*>(g.data()), reinterpret_cast<double*>(fr.data()),
                                reinterpret_cast<double*>(lr.data()), reinterpret_cast<double*>(fc.data()),
-                               reinterpret_cast<double*>(lc.data()), c, &fl),
-      fl);
+                               reinterpret_cast<double*>(lc.data()), c, &fl);
+  detail::check(rc, fl);
   s.data.swap(g);
   ExtendedInverse<cd> ext;
   ext.core = detail::from_slots(m.layout(), s);
@@ -169,10 +169,10 @@ inline std::pair<BlockBandedMatrix<cd>, KernelCounters> ddrgf(const BlockBandedM
   std::vector<cd> g(s.data.size());
   long long c[3];
   int fl = -1;
-  detail::check(bbsi_cuda_ddrgf_z(s.l, s.w, s.bs, s.sizes.data(), reinterpret_cast<const double*>(s.data.data()),
+  const int rc = bbsi_cuda_ddrgf_z(s.l, s.w, s.bs, s.sizes.data(), reinterpret_cast<const double*>(s.data.data()),
                                   plan.s2_levels.data(), plan.n_levels(), plan.n_threads, plan.terminal_threads,
-                                  reinterpret_cast<double*>(g.data()), c, &fl),
-                fl);
+                                  reinterpret_cast<double*>(g.data()), c, &fl);
+  detail::check(rc, fl);
   s.data.swap(g);
   return {detail::from_slots(m.layout(), s), detail::counters(c)};
 }
