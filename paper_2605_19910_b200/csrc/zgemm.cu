@@ -166,15 +166,24 @@ __global__ void __launch_bounds__(128, 2) zgemm_grouped_kernel(const __grid_cons
         br[ni] = v.x;
         bi[ni] = v.y;
       }
+      // 4 passes over the 16 sub-tiles: consecutive DMMAs never share an
+      // accumulator, so the pipe never waits on its own result
 #pragma unroll
       for (int mi = 0; mi < 4; ++mi)
 #pragma unroll
-        for (int ni = 0; ni < 4; ++ni) {
-          dmma884(cr[mi][ni], ar[mi], br[ni]);
-          dmma884(ci[mi][ni], ar[mi], bi[ni]);
-          dmma884(cr[mi][ni], an[mi], bi[ni]);
-          dmma884(ci[mi][ni], ai[mi], br[ni]);
-        }
+        for (int ni = 0; ni < 4; ++ni) dmma884(cr[mi][ni], ar[mi], br[ni]);
+#pragma unroll
+      for (int mi = 0; mi < 4; ++mi)
+#pragma unroll
+        for (int ni = 0; ni < 4; ++ni) dmma884(ci[mi][ni], ar[mi], bi[ni]);
+#pragma unroll
+      for (int mi = 0; mi < 4; ++mi)
+#pragma unroll
+        for (int ni = 0; ni < 4; ++ni) dmma884(cr[mi][ni], an[mi], bi[ni]);
+#pragma unroll
+      for (int mi = 0; mi < 4; ++mi)
+#pragma unroll
+        for (int ni = 0; ni < 4; ++ni) dmma884(ci[mi][ni], ai[mi], br[ni]);
     }
     __syncthreads();
   }
