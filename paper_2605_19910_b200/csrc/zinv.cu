@@ -25,6 +25,7 @@
 // threshold (kernels.hpp:149-158); status[] gets the first failing column or -1.
 #include <cfloat>
 #include <climits>
+#include <cstdlib>
 
 #include "internal.h"
 
@@ -48,7 +49,19 @@ struct GjScratch {
   double2* s1;    // [batch][n*n]
 };
 
-int pick_nb(int n) { return (size_t(n) * 32 * sizeof(double2) <= 200 * 1024) ? 32 : 16; }
+// Panel width. 16 is the default: blocked Gauss-Jordan loses accuracy with the
+// pivot-block width (numpy emulation on config 3, E = 0.145: RGF vs reference
+// 2.2e-10 at nb = 32, 1.4e-10 at nb = 16, 1.3e-10 unblocked; the reference's own
+// 1/2-ulp input-noise floor there is 1.1-1.4e-10). BBSI_GJ_NB=32 trades accuracy
+// for fewer, wider panels.
+int pick_nb(int n) {
+  static int forced = [] {
+    const char* e = getenv("BBSI_GJ_NB");
+    return e ? atoi(e) : 0;
+  }();
+  if (forced == 32 && size_t(n) * 32 * sizeof(double2) <= 200 * 1024) return 32;
+  return 16;
+}
 
 size_t align256(size_t x) { return (x + 255) & ~size_t(255); }
 
