@@ -112,6 +112,22 @@ int bbsi_cuda_dyson_rgf_z(int l, int w, int bs, int n_energy, const double* H, c
 /* Resident stabilised DDRGF of one band (w = 1): dA, dG device [l][3][bs][bs],
  * interior groups of s2 layers (single-level plan). */
 int bbsi_cuda_ddrgf_dev(int l, int bs, int s2, const double* dA, double* dG, int* fail_layer, void* stream);
+/* Domain-sharded DDRGF (one process per GPU). Tasks = interleave_permutation(l,1,s2)
+ * groups (partition.hpp:39-75), T = bbsi_cuda_ddrgf_num_tasks(l, s2). A rank owning
+ * tasks [t0,t1) holds the band rows of layers [first(t0), sep(t1-1)] (dA/dG local,
+ * [rows][3][bs][bs], slot order). Protocol: phase1 -> all-gather of the packets
+ * (packet_bytes(t1-t0) per rank, T packets in task order) -> phase2 (identical on
+ * every rank) -> phase3. Only the packets (9 bs x bs blocks per task) are exchanged. */
+int bbsi_cuda_ddrgf_num_tasks(int l, int s2);
+long long bbsi_cuda_ddrgf_packet_bytes(int ntask, int bs);
+long long bbsi_cuda_ddrgf_phase2_bytes(int ntask, int bs);
+int bbsi_cuda_ddrgf_phase1_dev(int l, int bs, int s2, int t0, int t1, const double* dA, double* dG, double* dPacket,
+                               int* fail_layer, void* stream);
+int bbsi_cuda_ddrgf_phase2_dev(int l, int bs, int s2, const double* dPackets, double* dOut, int* fail_layer,
+                               void* stream);
+int bbsi_cuda_ddrgf_phase3_dev(int l, int bs, int s2, int t0, int t1, const double* dA, double* dG, const double* dOut,
+                               int* fail_layer, void* stream);
+
 /* Dyson DDRGF for one energy z (host complex) from the shared device H. */
 int bbsi_cuda_dyson_ddrgf_dev(int l, int bs, const double* dH, const double* z, const double* sigma, int s2,
                               double* dG, int* fail_layer, void* stream);

@@ -32,6 +32,12 @@ SIGNATURES = {
     "bbsi_cuda_ddrgf_dev": (_i, [_i, _i, _i, _vp, _vp, _vp, _vp]),
     "bbsi_cuda_dyson_ddrgf_dev": (_i, [_i, _i, _vp, _vp, _vp, _i, _vp, _vp, _vp]),
     "bbsi_ddrgf_reference_counters": (None, [_ll, _vp, _i, _vp]),
+    "bbsi_cuda_ddrgf_num_tasks": (_i, [_i, _i]),
+    "bbsi_cuda_ddrgf_packet_bytes": (_ll, [_i, _i]),
+    "bbsi_cuda_ddrgf_phase2_bytes": (_ll, [_i, _i]),
+    "bbsi_cuda_ddrgf_phase1_dev": (_i, [_i, _i, _i, _i, _i, _vp, _vp, _vp, _vp, _vp]),
+    "bbsi_cuda_ddrgf_phase2_dev": (_i, [_i, _i, _i, _vp, _vp, _vp, _vp]),
+    "bbsi_cuda_ddrgf_phase3_dev": (_i, [_i, _i, _i, _i, _i, _vp, _vp, _vp, _vp, _vp]),
     "bbsi_cuda_launch_count": (_ll, []),
     "bbsi_cuda_profile_enable": (None, [_i]),
     "bbsi_cuda_profile_collect": (_i, [_vp, _i]),

@@ -700,6 +700,67 @@ int bbsi_cuda_dyson_ddrgf_dev(int l, int bs, const double* dH, const double* z, 
   return ddrgf_on_device(dA, reinterpret_cast<double2*>(dG), l, bs, nt, s2, fail_layer, s);
 }
 
+int bbsi_cuda_ddrgf_num_tasks(int l, int s2) { return (l >= 1 + s2 && s2 >= 1) ? ddrgf_num_tasks(l, s2) : -1; }
+
+long long bbsi_cuda_ddrgf_packet_bytes(int ntask, int bs) { return (long long)ddrgf_packet_bytes(ntask, bs); }
+long long bbsi_cuda_ddrgf_phase2_bytes(int ntask, int bs) { return (long long)ddrgf_phase2_out_bytes(ntask, bs); }
+
+static int phase_rc(cudaError_t e, int fl, int* fail_layer, const char* what) {
+  if (e != cudaSuccess) return cuda_fail(e, what);
+  if (fl >= 0) {
+    if (fail_layer) *fail_layer = fl;
+    return fail(BBSI_SINGULAR, std::string(what) + ": singular pivot at layer " + std::to_string(fl));
+  }
+  return BBSI_OK;
+}
+
+int bbsi_cuda_ddrgf_phase1_dev(int l, int bs, int s2, int t0, int t1, const double* dA, double* dG, double* dPacket,
+                               int* fail_layer, void* stream) {
+  if (fail_layer) *fail_layer = -1;
+  int one = s2;
+  if (int rc = validate_ddrgf(l, 1, bs, nullptr, &one, 1, 1, 1)) return rc;
+  if (bs % 64) return fail(BBSI_INVALID_ARGUMENT, "resident API requires bs % 64 == 0");
+  if (t0 < 0 || t1 > ddrgf_num_tasks(l, s2) || t0 >= t1) return fail(BBSI_INVALID_ARGUMENT, "bad task range");
+  if (int rc = device_ok()) return rc;
+  std::lock_guard<std::mutex> lk(g_call_mu);
+  int fl = -1;
+  cudaError_t e = ddrgf_phase1(reinterpret_cast<const double2*>(dA), reinterpret_cast<double2*>(dG), l, bs, nullptr,
+                               s2, ddrgf_gamma(), t0, t1, reinterpret_cast<double2*>(dPacket), &fl,
+                               static_cast<cudaStream_t>(stream));
+  if (e == cudaSuccess) e = cudaStreamSynchronize(static_cast<cudaStream_t>(stream));
+  return phase_rc(e, fl, fail_layer, "ddrgf phase 1");
+}
+
+int bbsi_cuda_ddrgf_phase2_dev(int l, int bs, int s2, const double* dPackets, double* dOut, int* fail_layer,
+                               void* stream) {
+  if (fail_layer) *fail_layer = -1;
+  int one = s2;
+  if (int rc = validate_ddrgf(l, 1, bs, nullptr, &one, 1, 1, 1)) return rc;
+  if (bs % 64) return fail(BBSI_INVALID_ARGUMENT, "resident API requires bs % 64 == 0");
+  if (int rc = device_ok()) return rc;
+  std::lock_guard<std::mutex> lk(g_call_mu);
+  int fl = -1;
+  cudaError_t e = ddrgf_phase2(reinterpret_cast<const double2*>(dPackets), l, bs, nullptr, s2, ddrgf_gamma(),
+                               reinterpret_cast<double2*>(dOut), &fl, static_cast<cudaStream_t>(stream));
+  return phase_rc(e, fl, fail_layer, "ddrgf phase 2");
+}
+
+int bbsi_cuda_ddrgf_phase3_dev(int l, int bs, int s2, int t0, int t1, const double* dA, double* dG, const double* dOut,
+                               int* fail_layer, void* stream) {
+  if (fail_layer) *fail_layer = -1;
+  int one = s2;
+  if (int rc = validate_ddrgf(l, 1, bs, nullptr, &one, 1, 1, 1)) return rc;
+  if (bs % 64) return fail(BBSI_INVALID_ARGUMENT, "resident API requires bs % 64 == 0");
+  if (t0 < 0 || t1 > ddrgf_num_tasks(l, s2) || t0 >= t1) return fail(BBSI_INVALID_ARGUMENT, "bad task range");
+  if (int rc = device_ok()) return rc;
+  std::lock_guard<std::mutex> lk(g_call_mu);
+  int fl = -1;
+  cudaError_t e = ddrgf_phase3(reinterpret_cast<const double2*>(dA), reinterpret_cast<double2*>(dG), l, bs, nullptr, s2,
+                               t0, t1, reinterpret_cast<const double2*>(dOut), &fl, static_cast<cudaStream_t>(stream));
+  if (e == cudaSuccess) e = cudaStreamSynchronize(static_cast<cudaStream_t>(stream));
+  return phase_rc(e, fl, fail_layer, "ddrgf phase 3");
+}
+
 void bbsi_ddrgf_reference_counters(long long l, const int* s2_levels, int n_levels, long long* out) {
   ddrgf_reference_counters(l, s2_levels, n_levels, out);
 }

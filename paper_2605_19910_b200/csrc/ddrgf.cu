@@ -154,94 +154,127 @@ cudaError_t zmm(int b, int batch, double2 alpha, ZOp A, ZOp B, double beta, ZOp 
   return zgemm_grouped(g, s);
 }
 
-cudaError_t ddrgf_device(const double2* A, double2* G, int l, int b, const int* n_true, int s2, double gamma,
-                         void* scratch, size_t scratch_bytes, int* fail_layer, cudaStream_t s) {
-  *fail_layer = -1;
-  const long long bb = (long long)b * b;
-  const long long slot3 = 3 * bb;
-  auto aslot = [&](int a, int off) { return A + ((long long)a * 3 + off + 1) * bb; };
-  auto gslot = [&](int a, int off) { return G + ((long long)a * 3 + off + 1) * bb; };
-  const Part P = partition(l, s2);
-  const int T = P.T;
-  // full-length domains are tasks 0..nfull-1 (all but possibly the trailing one)
-  int nfull = T;
-  if (P.count[T - 1] != s2) nfull = T - 1;
-  const int tc = P.count[T - 1];  // trailing interior count (== s2 when nfull == T)
-  cudaError_t e;
+// ---------------------------------------------------------------------------------
+// The three phases operate on a rank-local slice of the band (whole chains
+// [domain t, separator t] for tasks t0..t1-1, layers [first(t0), sep(t1-1)]) plus a
+// per-task interface packet of PK b x b blocks; only packets cross ranks.
+//   packet[t] = { a, b, c, e (fake-lead corners), A[s,s], A[s,l], A[l,s], A[s,s+1], A[x0,x0-1] }
+//   phase-2 output[t] = { Sigma^L on the chain's first block, Sigma^R on its separator,
+//                         Y_t (right-connected G at x0: couplings), G[s,s] }
+enum { PA, PB, PC, PE, PASS, PASL, PALS, PASN, PAX0, PK };
+enum { OSL, OSR, OY, OGSS, NOUT };
 
-  // ---- device scratch carve: per-task b x b matrices
-  enum { KA, KB, KC, KE, GL, GR, GLD, GRD, NMAT };
-  const size_t per = size_t(NMAT) * T * bb * sizeof(double2);
-  const size_t tmp_n = 8;  // temporaries for phase 2
-  const size_t need = per + tmp_n * bb * sizeof(double2) + 2 * size_t(T) * bb * sizeof(double2);
-  if (scratch_bytes < need) return cudaErrorMemoryAllocation;
-  double2* mats = static_cast<double2*>(scratch);
-  auto M_ = [&](int kind, int t) { return mats + ((size_t)kind * T + t) * bb; };
-  double2* tmp = mats + (size_t)NMAT * T * bb;
-  auto Tm = [&](int i) { return tmp + (size_t)i * bb; };
-  double2* rc = tmp + tmp_n * bb;  // [2][T] ping-pong for the first row / column chains (R, C)
+namespace {
 
-  // ================= phase 1: corners with fake absorbing leads
-  if ((e = cudaMemcpyAsync(G, A, sizeof(double2) * size_t(l) * slot3, cudaMemcpyDeviceToDevice, s))) return e;
-  const double2 ig = make_double2(0.0, gamma);  // -Sigma0 = +i*gamma
-  // fake leads on the first and last block of every nonempty domain
-  for (int t = 0; t < T; ++t) {
-    if (P.count[t] == 0) continue;
-    if ((e = diag_add(gslot(P.first[t], 0), 0, b, 1, ig, s))) return e;
-    if ((e = diag_add(gslot(P.first[t] + P.count[t] - 1, 0), 0, b, 1, ig, s))) return e;
+struct Local {
+  const double2* A;  // local band, layer 0 = global layer L0
+  double2* G;
+  int L0;
+  long long bb;
+  const double2* aslot(int a, int off) const { return A + ((long long)(a - L0) * 3 + off + 1) * bb; }
+  double2* gslot(int a, int off) const { return G + ((long long)(a - L0) * 3 + off + 1) * bb; }
+};
+
+// RGF sweeps over the chains of tasks [t, t+nt) (same length len), in place in G.
+cudaError_t chain_sweeps(const Local& X, const Part& P, int s2, int t, int nt, int len, int b, const int* n_true,
+                         SweepWork& W, int* fail_layer, cudaStream_t s) {
+  W = SweepWork{};
+  W.l = len;
+  W.w = 1;
+  W.bs = b;
+  W.batch = nt;
+  W.G = X.gslot(P.first[t], -1);
+  W.g_bstride = (long long)(s2 + 1) * 3 * X.bb;
+  W.groups = default_groups(nt, b);
+  void* sc = arena_get(6, sweep_scratch_bytes(len, 1, b, nt, W.groups));
+  if (!sc) return cudaErrorMemoryAllocation;
+  sweep_carve(W, sc);
+  std::vector<int> ntr(len, b);
+  for (int j = 0; j < len; ++j) ntr[j] = n_true ? n_true[P.first[t] + j] : b;
+  cudaError_t e = rgf_sweeps(W, ntr.data(), s);
+  if (e) return e;
+  std::vector<int> fails;
+  if ((e = collect_failures(W, fails, s))) return e;
+  for (int q = 0; q < nt; ++q)
+    if (fails[q] >= 0) {
+      *fail_layer = P.first[t + q] + fails[q];
+      break;
+    }
+  return cudaSuccess;
+}
+
+// groups of equal-length consecutive tasks inside [t0, t1): only the global trailing
+// task can be shorter than s2
+template <class F>
+cudaError_t for_task_runs(const Part& P, int s2, int t0, int t1, F&& f) {
+  int t = t0;
+  while (t < t1) {
+    int u = t;
+    while (u < t1 && P.count[u] == P.count[t]) ++u;
+    cudaError_t e = f(t, u - t, P.count[t]);
+    if (e) return e;
+    t = u;
   }
-  auto sweep = [&](int first_task, int ntask, int len, SweepWork& W, std::vector<int>& fails) -> cudaError_t {
-    W = SweepWork{};
-    W.l = len;
-    W.w = 1;
-    W.bs = b;
-    W.batch = ntask;
-    W.G = gslot(P.first[first_task], -1);
-    W.g_bstride = (long long)(s2 + 1) * slot3;
-    W.groups = default_groups(ntask, b);
-    void* sc = arena_get(6, sweep_scratch_bytes(len, 1, b, ntask, W.groups));
-    if (!sc) return cudaErrorMemoryAllocation;
-    sweep_carve(W, sc);
-    std::vector<int> nt(len, b);
-    for (int j = 0; j < len; ++j) nt[j] = n_true ? n_true[P.first[first_task] + j] : b;
-    cudaError_t e2 = rgf_sweeps(W, nt.data(), s);
-    if (e2) return e2;
-    return collect_failures(W, fails, s);
-  };
-  auto first_fail = [&](const std::vector<int>& fails, int first_task) {
-    for (size_t q = 0; q < fails.size(); ++q)
-      if (fails[q] >= 0) return P.first[first_task + q] + fails[q];
-    return -1;
-  };
-  // corners of a batch of domains (tasks t0..t0+nt-1, all of length len) from a finished sweep
-  auto corners = [&](int t0, int nt, int len, const SweepWork& W) -> cudaError_t {
-    cudaError_t e2;
+  return cudaSuccess;
+}
+
+}  // namespace
+
+size_t ddrgf_packet_bytes(int ntask, int b) { return size_t(ntask) * PK * b * b * sizeof(double2); }
+size_t ddrgf_phase2_out_bytes(int ntask, int b) { return size_t(ntask) * NOUT * b * b * sizeof(double2); }
+
+// Phase 1: fake-lead corners of the local domains + interface A blocks -> packet.
+cudaError_t ddrgf_phase1(const double2* A, double2* G, int l, int b, const int* n_true, int s2, double gamma, int t0,
+                         int t1, double2* packet, int* fail_layer, cudaStream_t s) {
+  *fail_layer = -1;
+  const Part P = partition(l, s2);
+  if (t0 < 0 || t1 > P.T || t0 >= t1) return cudaErrorInvalidValue;
+  const long long bb = (long long)b * b;
+  Local X{A, G, P.first[t0], bb};
+  const int L1 = P.sep[t1 - 1] + 1;
+  const size_t band_b = sizeof(double2) * size_t(L1 - X.L0) * 3 * bb;
+  cudaError_t e;
+  if ((e = cudaMemcpyAsync(G, A, band_b, cudaMemcpyDeviceToDevice, s))) return e;
+  const double2 ig = make_double2(0.0, gamma);  // -Sigma0 = +i*gamma
+  for (int t = t0; t < t1; ++t) {
+    if (P.count[t] == 0) continue;
+    if ((e = diag_add(X.gslot(P.first[t], 0), 0, b, 1, ig, s))) return e;
+    if ((e = diag_add(X.gslot(P.first[t] + P.count[t] - 1, 0), 0, b, 1, ig, s))) return e;
+  }
+  auto pk = [&](int t, int k) { return packet + ((size_t)(t - t0) * PK + k) * bb; };
+  double2* rc = static_cast<double2*>(arena_get(12, 2 * size_t(t1 - t0) * bb * sizeof(double2)));
+  if (!rc) return cudaErrorMemoryAllocation;
+  e = for_task_runs(P, s2, t0, t1, [&](int t, int nt, int len) -> cudaError_t {
+    if (len == 0) return cudaSuccess;
+    SweepWork W;
+    cudaError_t e2 = chain_sweeps(X, P, s2, t, nt, len, b, n_true, W, fail_layer, s);
+    if (e2 || *fail_layer >= 0) return e2;
+    // a = G[f,f], e = G[l,l]; b = G[f,l], c = G[l,f] by the first row / column chains
     const long long gs = W.g_bstride;
-    // a = G[0,0], e = G[len-1,0]
-    if ((e2 = cudaMemcpy2DAsync(M_(KA, t0), bb * sizeof(double2), gslot(P.first[t0], 0), gs * sizeof(double2),
+    const size_t pkstride = PK * bb * sizeof(double2);
+    if ((e2 = cudaMemcpy2DAsync(pk(t, PA), pkstride, X.gslot(P.first[t], 0), gs * sizeof(double2),
                                 bb * sizeof(double2), nt, cudaMemcpyDeviceToDevice, s)))
       return e2;
-    if ((e2 = cudaMemcpy2DAsync(M_(KE, t0), bb * sizeof(double2), gslot(P.first[t0] + len - 1, 0),
-                                gs * sizeof(double2), bb * sizeof(double2), nt, cudaMemcpyDeviceToDevice, s)))
+    if ((e2 = cudaMemcpy2DAsync(pk(t, PE), pkstride, X.gslot(P.first[t] + len - 1, 0), gs * sizeof(double2),
+                                bb * sizeof(double2), nt, cudaMemcpyDeviceToDevice, s)))
       return e2;
-    // first row R_j = G[0,j] = -R_{j-1} um_j ; first column C_j = G[j,0] = -lm_j C_{j-1}
-    // ping-pong between the b / c output slots and scratch (nt matrices each)
-    double2* pr = rc;             // R ping  [nt]
-    double2* pc = rc + nt * bb;   // C ping  [nt]  (rc has 2*T matrices)
     if (len == 1) {
-      if ((e2 = cudaMemcpyAsync(M_(KB, t0), M_(KA, t0), nt * bb * sizeof(double2), cudaMemcpyDeviceToDevice, s)))
+      if ((e2 = cudaMemcpy2DAsync(pk(t, PB), pkstride, pk(t, PA), pkstride, bb * sizeof(double2), nt,
+                                  cudaMemcpyDeviceToDevice, s)))
         return e2;
-      return cudaMemcpyAsync(M_(KC, t0), M_(KA, t0), nt * bb * sizeof(double2), cudaMemcpyDeviceToDevice, s);
+      return cudaMemcpy2DAsync(pk(t, PC), pkstride, pk(t, PA), pkstride, bb * sizeof(double2), nt,
+                               cudaMemcpyDeviceToDevice, s);
     }
-    // R_0 = C_0 = a; chains alternate between (pr/pc) and the output slots (KB/KC)
-    double2* r_cur = M_(KA, t0);
-    double2* c_cur = M_(KA, t0);
+    double2* pr = rc;
+    double2* pc = rc + (size_t)nt * bb;
+    const double2* r_cur = pk(t, PA);
+    const double2* c_cur = pk(t, PA);
+    long long rstride = PK * bb, cstride = PK * bb;
     for (int j = 1; j < len; ++j) {
-      const bool to_out = ((len - 1 - j) % 2) == 0;  // the last step lands in KB / KC
-      double2* r_nxt = to_out ? M_(KB, t0) : pr;
-      double2* c_nxt = to_out ? M_(KC, t0) : pc;
-      const double2* um = W.UM + (long long)j * bb;  // um[j] (w = 1), batch stride l*bb
-      const double2* lm = W.LM + (long long)j * bb;
+      const bool to_out = ((len - 1 - j) % 2) == 0;  // the last step lands in the packet
+      double2* r_nxt = to_out ? pk(t, PB) : pr;
+      double2* c_nxt = to_out ? pk(t, PC) : pc;
+      const long long nstride = to_out ? PK * bb : bb;
       ZGemmGroup g{};
       g.batch = nt;
       g.bs = 64;
@@ -250,44 +283,71 @@ cudaError_t ddrgf_device(const double2* A, double2* G, int l, int b, const int* 
       p0.M = p0.N = p0.K = b;
       p0.alpha = make_double2(-1.0, 0.0);
       p0.beta = make_double2(0.0, 0.0);
-      p0.A = blk(r_cur, b, bb);
-      p0.B = blk(um, b, (long long)W.l * bb);
-      p0.C = p0.D = blk(r_nxt, b, bb);
+      p0.A = blk(r_cur, b, rstride);
+      p0.B = blk(W.UM + (long long)j * bb, b, (long long)W.l * bb);
+      p0.C = p0.D = blk(r_nxt, b, nstride);
       ZGemmProblem& p1 = g.prob[1];
       p1 = p0;
-      p1.A = blk(lm, b, (long long)W.l * bb);
-      p1.B = blk(c_cur, b, bb);
-      p1.C = p1.D = blk(c_nxt, b, bb);
+      p1.A = blk(W.LM + (long long)j * bb, b, (long long)W.l * bb);
+      p1.B = blk(c_cur, b, cstride);
+      p1.C = p1.D = blk(c_nxt, b, nstride);
       if ((e2 = zgemm_grouped(g, s))) return e2;
       r_cur = r_nxt;
       c_cur = c_nxt;
+      rstride = cstride = nstride;
     }
     return cudaSuccess;
+  });
+  if (e || *fail_layer >= 0) return e;
+  // interface A blocks (out-of-band slots are zero in the band)
+  auto cp = [&](double2* d, const double2* x) {
+    return cudaMemcpyAsync(d, x, bb * sizeof(double2), cudaMemcpyDeviceToDevice, s);
   };
-  {
-    SweepWork W;
-    std::vector<int> fails;
-    if (nfull > 0) {
-      if ((e = sweep(0, nfull, s2, W, fails))) return e;
-      if ((*fail_layer = first_fail(fails, 0)) >= 0) return cudaSuccess;
-      if ((e = corners(0, nfull, s2, W))) return e;
+  for (int t = t0; t < t1; ++t) {
+    const int sp = P.sep[t], cnt = P.count[t];
+    const int x0 = cnt > 0 ? P.first[t] : sp;
+    if ((e = cp(pk(t, PASS), X.aslot(sp, 0)))) return e;
+    if ((e = cp(pk(t, PASL), X.aslot(sp, -1)))) return e;
+    if (cnt > 0) {
+      if ((e = cp(pk(t, PALS), X.aslot(sp - 1, 1)))) return e;
+    } else if ((e = cudaMemsetAsync(pk(t, PALS), 0, bb * sizeof(double2), s))) {
+      return e;
     }
-    if (nfull < T && tc > 0) {
-      if ((e = sweep(T - 1, 1, tc, W, fails))) return e;
-      if ((*fail_layer = first_fail(fails, T - 1)) >= 0) return cudaSuccess;
-      if ((e = corners(T - 1, 1, tc, W))) return e;
+    if ((e = cp(pk(t, PASN), X.aslot(sp, 1)))) return e;
+    if ((e = cp(pk(t, PAX0), X.aslot(x0, -1)))) return e;
+    if (cnt == 0) {  // no corners: keep them zero
+      for (int k = PA; k <= PE; ++k)
+        if ((e = cudaMemsetAsync(pk(t, k), 0, bb * sizeof(double2), s))) return e;
     }
   }
+  return cudaSuccess;
+}
 
-  // ================= phase 3 input: fresh copy of A (phase 2 adds the self-energies)
-  if ((e = cudaMemcpyAsync(G, A, sizeof(double2) * size_t(l) * slot3, cudaMemcpyDeviceToDevice, s))) return e;
-
-  // ================= phase 2: left / right sweeps over the separators (b x b work)
-  const int max_inv = 6 * T + 2;
+// Phase 2 (redundant on every rank): left-/right-connected sweeps over all T
+// separators from the gathered packets.
+cudaError_t ddrgf_phase2(const double2* packets, int l, int b, const int* n_true, int s2, double gamma, double2* out,
+                         int* fail_layer, cudaStream_t s) {
+  *fail_layer = -1;
+  const Part P = partition(l, s2);
+  const int T = P.T;
+  const long long bb = (long long)b * b;
+  auto pk = [&](int t, int k) { return packets + ((size_t)t * PK + k) * bb; };
+  auto o = [&](int t, int k) { return out + ((size_t)t * NOUT + k) * bb; };
+  const double2 ig = make_double2(0.0, gamma);
+  const double2 m1 = make_double2(-1.0, 0.0);
+  cudaError_t e;
+  // scratch: gL, gLdom, SigmaLsep per task, gR (current), 8 temporaries
+  double2* scr = static_cast<double2*>(arena_get(13, (size_t(3) * T + 10) * bb * sizeof(double2)));
+  const int max_inv = 8 * T + 4;
   void* inv_scr = arena_get(7, zinv_scratch_bytes(b, 1) + 256);
   int* st = static_cast<int*>(arena_get(8, sizeof(int) * size_t(max_inv)));
-  if (!inv_scr || !st) return cudaErrorMemoryAllocation;
-  std::vector<int> st_layer;  // layer to blame per inversion (failure attribution)
+  if (!scr || !inv_scr || !st) return cudaErrorMemoryAllocation;
+  auto gL = [&](int t) { return scr + (size_t)t * bb; };
+  auto gLD = [&](int t) { return scr + ((size_t)T + t) * bb; };
+  auto SLs = [&](int t) { return scr + ((size_t)2 * T + t) * bb; };
+  double2* gR = scr + (size_t)3 * T * bb;
+  auto Tm = [&](int i) { return scr + ((size_t)3 * T + 1 + i) * bb; };
+  std::vector<int> st_layer;
   auto inv = [&](double2* m, int layer) -> cudaError_t {
     if (int(st_layer.size()) >= max_inv) return cudaErrorInvalidValue;
     int* slot = st + st_layer.size();
@@ -301,126 +361,155 @@ cudaError_t ddrgf_device(const double2* A, double2* G, int l, int b, const int* 
   auto copy = [&](double2* d, const double2* x) {
     return cudaMemcpyAsync(d, x, bb * sizeof(double2), cudaMemcpyDeviceToDevice, s);
   };
-  // out = x + i*gamma * x (I - i*gamma x)^{-1} x   (removes the fake lead -i*gamma at the block of x)
-  auto remove_fake = [&](double2* out, double2* x, int layer) -> cudaError_t {
+  auto mm3 = [&](double2* d, double alpha, const double2* x, const double2* y, const double2* z) -> cudaError_t {
+    // d = alpha * x * y * z  (via Tm(7))
+    cudaError_t e2 = mm(b, 1, 1.0, blk(x, b), blk(y, b), 0.0, blk(Tm(7), b), s);
+    return e2 ? e2 : mm(b, 1, alpha, blk(Tm(7), b), blk(z, b), 0.0, blk(d, b), s);
+  };
+  // out = x + i*gamma x (I - i*gamma x)^{-1} x   (removes the fake lead at the block of x)
+  auto remove_fake = [&](double2* o_, const double2* x, int layer) -> cudaError_t {
     cudaError_t e2;
     if ((e2 = ident(Tm(2)))) return e2;
     if ((e2 = axpy(Tm(2), x, bb, make_double2(0.0, -gamma), s))) return e2;
     if ((e2 = inv(Tm(2), layer))) return e2;
     if ((e2 = mm(b, 1, 1.0, blk(Tm(2), b), blk(x, b), 0.0, blk(Tm(3), b), s))) return e2;
-    if ((e2 = copy(out, x))) return e2;
-    return mmz(b, make_double2(0.0, gamma), blk(x, b), blk(Tm(3), b), 1.0, blk(out, b), s);
+    if ((e2 = copy(o_, x))) return e2;
+    return mmz(b, make_double2(0.0, gamma), blk(x, b), blk(Tm(3), b), 1.0, blk(o_, b), s);
   };
-  // left sweep
+  // ---- left sweep
   for (int t = 0; t < T; ++t) {
     const int f = P.first[t], cnt = P.count[t], sp = P.sep[t];
-    double2* gl = M_(GL, t);
     if (cnt > 0) {
+      // Sigma^L on the first block (from separator t-1); Df = Sigma^L - Sigma0
       double2* Df = Tm(1);
-      if (t > 0) {  // Sigma^L = A[f,-1] gL_{t-1} A[f-1,+1], also subtracted from phase 3's first block
-        if ((e = mm(b, 1, 1.0, blk(aslot(f, -1), b), blk(M_(GL, t - 1), b), 0.0, blk(Tm(0), b), s))) return e;
-        if ((e = mm(b, 1, 1.0, blk(Tm(0), b), blk(aslot(f - 1, 1), b), 0.0, blk(Df, b), s))) return e;
-        if ((e = axpy(gslot(f, 0), Df, bb, make_double2(-1.0, 0.0), s))) return e;
-      } else {
-        if ((e = cudaMemsetAsync(Df, 0, bb * sizeof(double2), s))) return e;
+      if (t > 0) {
+        if ((e = mm3(o(t, OSL), 1.0, pk(t, PAX0), gL(t - 1), pk(t - 1, PASN)))) return e;
+      } else if ((e = cudaMemsetAsync(o(t, OSL), 0, bb * sizeof(double2), s))) {
+        return e;
       }
-      // step A (true lead at f): Df = Sigma^L - Sigma0 ; P = I - Df a ; e' = e + c P^{-1} Df b
+      if ((e = copy(Df, o(t, OSL)))) return e;
       if ((e = diag_add(Df, 0, b, 1, ig, s))) return e;
+      // e' = e + c (I - Df a)^{-1} Df b
       if ((e = ident(Tm(2)))) return e;
-      if ((e = mm(b, 1, -1.0, blk(Df, b), blk(M_(KA, t), b), 1.0, blk(Tm(2), b), s))) return e;
+      if ((e = mm(b, 1, -1.0, blk(Df, b), blk(pk(t, PA), b), 1.0, blk(Tm(2), b), s))) return e;
       if ((e = inv(Tm(2), f))) return e;
       if ((e = mm(b, 1, 1.0, blk(Tm(2), b), blk(Df, b), 0.0, blk(Tm(3), b), s))) return e;
-      if ((e = mm(b, 1, 1.0, blk(Tm(3), b), blk(M_(KB, t), b), 0.0, blk(Tm(4), b), s))) return e;
-      if ((e = copy(Tm(5), M_(KE, t)))) return e;
-      if ((e = mm(b, 1, 1.0, blk(M_(KC, t), b), blk(Tm(4), b), 1.0, blk(Tm(5), b), s))) return e;
-      // step B (drop the fake lead at l): gLdom
-      if ((e = remove_fake(M_(GLD, t), Tm(5), f + cnt - 1))) return e;
-      if ((e = mm(b, 1, 1.0, blk(aslot(sp, -1), b), blk(M_(GLD, t), b), 0.0, blk(Tm(0), b), s))) return e;
+      if ((e = mm(b, 1, 1.0, blk(Tm(3), b), blk(pk(t, PB), b), 0.0, blk(Tm(4), b), s))) return e;
+      if ((e = copy(Tm(5), pk(t, PE)))) return e;
+      if ((e = mm(b, 1, 1.0, blk(pk(t, PC), b), blk(Tm(4), b), 1.0, blk(Tm(5), b), s))) return e;
+      if ((e = remove_fake(gLD(t), Tm(5), f + cnt - 1))) return e;
+      if ((e = mm3(SLs(t), 1.0, pk(t, PASL), gLD(t), pk(t, PALS)))) return e;
     } else {
       if (t == 0) return cudaErrorInvalidValue;  // task 0 always has interior layers
-      if ((e = mm(b, 1, 1.0, blk(aslot(sp, -1), b), blk(M_(GL, t - 1), b), 0.0, blk(Tm(0), b), s))) return e;
+      if ((e = mm3(SLs(t), 1.0, pk(t, PASL), gL(t - 1), pk(t - 1, PASN)))) return e;
+      if ((e = copy(o(t, OSL), SLs(t)))) return e;  // the chain's only block is the separator
     }
-    // gL_t = (A[s,0] - Tm0 A[s-1,+1])^{-1}; an empty trailing domain also puts Sigma^L on G[s,0]
-    if ((e = copy(gl, aslot(sp, 0)))) return e;
-    if ((e = mm(b, 1, 1.0, blk(Tm(0), b), blk(aslot(sp - 1, 1), b), 0.0, blk(Tm(1), b), s))) return e;
-    if ((e = axpy(gl, Tm(1), bb, make_double2(-1.0, 0.0), s))) return e;
-    if (cnt == 0 && (e = axpy(gslot(sp, 0), Tm(1), bb, make_double2(-1.0, 0.0), s))) return e;
-    if ((e = inv(gl, sp))) return e;
+    if ((e = copy(gL(t), pk(t, PASS)))) return e;
+    if ((e = axpy(gL(t), SLs(t), bb, m1, s))) return e;
+    if ((e = inv(gL(t), sp))) return e;
   }
-  // right sweep
+  // ---- right sweep
   for (int t = T - 1; t >= 0; --t) {
-    const int sp = P.sep[t];
-    double2* gr = M_(GR, t);
-    if ((e = copy(gr, aslot(sp, 0)))) return e;
-    if (t < T - 1) {  // Sigma^R of separator t = A[s,+1] Y A[s+1,-1], also subtracted from phase 3's G[s,0]
-      const double2* Y = P.count[t + 1] > 0 ? M_(GRD, t + 1) : M_(GR, t + 1);
-      if ((e = mm(b, 1, 1.0, blk(aslot(sp, 1), b), blk(Y, b), 0.0, blk(Tm(0), b), s))) return e;
-      if ((e = mm(b, 1, 1.0, blk(Tm(0), b), blk(aslot(sp + 1, -1), b), 0.0, blk(Tm(1), b), s))) return e;
-      if ((e = axpy(gr, Tm(1), bb, make_double2(-1.0, 0.0), s))) return e;
-      if ((e = axpy(gslot(sp, 0), Tm(1), bb, make_double2(-1.0, 0.0), s))) return e;
+    const int sp = P.sep[t], cnt = P.count[t];
+    if (t < T - 1) {
+      if ((e = mm3(o(t, OSR), 1.0, pk(t, PASN), o(t + 1, OY), pk(t + 1, PAX0)))) return e;
+    } else if ((e = cudaMemsetAsync(o(t, OSR), 0, bb * sizeof(double2), s))) {
+      return e;
     }
-    if ((e = inv(gr, sp))) return e;
-    const int cnt = P.count[t];
+    // pre = A[s,s] - Sigma^R ; G[s,s] = (pre - Sigma^L_sep)^{-1} ; gR = pre^{-1}
+    if ((e = copy(gR, pk(t, PASS)))) return e;
+    if ((e = axpy(gR, o(t, OSR), bb, m1, s))) return e;
+    if ((e = copy(o(t, OGSS), gR))) return e;
+    if ((e = axpy(o(t, OGSS), SLs(t), bb, m1, s))) return e;
+    if ((e = inv(o(t, OGSS), sp))) return e;
+    if ((e = inv(gR, sp))) return e;
     if (cnt > 0) {
       const int last = P.first[t] + cnt - 1;
-      // step A (true lead at l): Dl = A[l,+1] gR_t A[s,-1] - Sigma0 ; P = I - Dl e ; a' = a + b P^{-1} Dl c
       double2* Dl = Tm(1);
-      if ((e = mm(b, 1, 1.0, blk(aslot(last, 1), b), blk(gr, b), 0.0, blk(Tm(0), b), s))) return e;
-      if ((e = mm(b, 1, 1.0, blk(Tm(0), b), blk(aslot(sp, -1), b), 0.0, blk(Dl, b), s))) return e;
+      if ((e = mm3(Dl, 1.0, pk(t, PALS), gR, pk(t, PASL)))) return e;
       if ((e = diag_add(Dl, 0, b, 1, ig, s))) return e;
       if ((e = ident(Tm(2)))) return e;
-      if ((e = mm(b, 1, -1.0, blk(Dl, b), blk(M_(KE, t), b), 1.0, blk(Tm(2), b), s))) return e;
+      if ((e = mm(b, 1, -1.0, blk(Dl, b), blk(pk(t, PE), b), 1.0, blk(Tm(2), b), s))) return e;
       if ((e = inv(Tm(2), last))) return e;
       if ((e = mm(b, 1, 1.0, blk(Tm(2), b), blk(Dl, b), 0.0, blk(Tm(3), b), s))) return e;
-      if ((e = mm(b, 1, 1.0, blk(Tm(3), b), blk(M_(KC, t), b), 0.0, blk(Tm(4), b), s))) return e;
-      if ((e = copy(Tm(5), M_(KA, t)))) return e;
-      if ((e = mm(b, 1, 1.0, blk(M_(KB, t), b), blk(Tm(4), b), 1.0, blk(Tm(5), b), s))) return e;
-      // step B (drop the fake lead at f): gRdom
-      if ((e = remove_fake(M_(GRD, t), Tm(5), P.first[t]))) return e;
+      if ((e = mm(b, 1, 1.0, blk(Tm(3), b), blk(pk(t, PC), b), 0.0, blk(Tm(4), b), s))) return e;
+      if ((e = copy(Tm(5), pk(t, PA)))) return e;
+      if ((e = mm(b, 1, 1.0, blk(pk(t, PB), b), blk(Tm(4), b), 1.0, blk(Tm(5), b), s))) return e;
+      if ((e = remove_fake(o(t, OY), Tm(5), P.first[t]))) return e;
+    } else if ((e = copy(o(t, OY), gR))) {
+      return e;
     }
   }
-  {  // phase 2 failures, first in issue order
-    std::vector<int> sh(st_layer.size());
-    if ((e = cudaMemcpyAsync(sh.data(), st, sh.size() * sizeof(int), cudaMemcpyDeviceToHost, s))) return e;
-    if ((e = cudaStreamSynchronize(s))) return e;
-    for (size_t q = 0; q < sh.size(); ++q)
-      if (sh[q] >= 0) {
-        *fail_layer = st_layer[q];
-        return cudaSuccess;
-      }
-  }
+  std::vector<int> sh(st_layer.size());
+  if ((e = cudaMemcpyAsync(sh.data(), st, sh.size() * sizeof(int), cudaMemcpyDeviceToHost, s))) return e;
+  if ((e = cudaStreamSynchronize(s))) return e;
+  for (size_t q = 0; q < sh.size(); ++q)
+    if (sh[q] >= 0) {
+      *fail_layer = st_layer[q];
+      break;
+    }
+  return cudaSuccess;
+}
 
-  // ================= phase 3: re-solve [domain t, separator t] chains in place
-  {
-    SweepWork W;
-    std::vector<int> fails;
-    if (nfull > 0) {
-      if ((e = sweep(0, nfull, s2 + 1, W, fails))) return e;
-      if ((*fail_layer = first_fail(fails, 0)) >= 0) return cudaSuccess;
-    }
-    if (nfull < T) {
-      if ((e = sweep(T - 1, 1, tc + 1, W, fails))) return e;
-      if ((*fail_layer = first_fail(fails, T - 1)) >= 0) return cudaSuccess;
-    }
-  }
-  // couplings between separator t-1 and the first layer x0 of chain t
-  for (int t = 1; t < T; ++t) {
+// Phase 3: re-solve the local chains with the exact boundary self-energies; couplings.
+cudaError_t ddrgf_phase3(const double2* A, double2* G, int l, int b, const int* n_true, int s2, int t0, int t1,
+                         const double2* out, int* fail_layer, cudaStream_t s) {
+  *fail_layer = -1;
+  const Part P = partition(l, s2);
+  const int T = P.T;
+  const long long bb = (long long)b * b;
+  Local X{A, G, P.first[t0], bb};
+  const int L1 = P.sep[t1 - 1] + 1;
+  auto o = [&](int t, int k) { return out + ((size_t)t * NOUT + k) * bb; };
+  const double2 m1 = make_double2(-1.0, 0.0);
+  cudaError_t e;
+  if ((e = cudaMemcpyAsync(G, A, sizeof(double2) * size_t(L1 - X.L0) * 3 * bb, cudaMemcpyDeviceToDevice, s))) return e;
+  for (int t = t0; t < t1; ++t) {
     const int x0 = P.count[t] > 0 ? P.first[t] : P.sep[t];
-    const int sp = P.sep[t - 1];
-    const double2* Y = P.count[t] > 0 ? M_(GRD, t) : M_(GR, t);
-    // G[x0,-1] = -Y A[x0,-1] G[s,0] ;  G[s,+1] = -G[s,0] A[s,+1] Y
-    if ((e = mm(b, 1, 1.0, blk(Y, b), blk(aslot(x0, -1), b), 0.0, blk(Tm(0), b), s))) return e;
-    if ((e = mm(b, 1, -1.0, blk(Tm(0), b), blk(gslot(sp, 0), b), 0.0, blk(gslot(x0, -1), b), s))) return e;
-    if ((e = mm(b, 1, 1.0, blk(gslot(sp, 0), b), blk(aslot(sp, 1), b), 0.0, blk(Tm(1), b), s))) return e;
-    if ((e = mm(b, 1, -1.0, blk(Tm(1), b), blk(Y, b), 0.0, blk(gslot(sp, 1), b), s))) return e;
+    if (t > 0 && (e = axpy(X.gslot(x0, 0), o(t, OSL), bb, m1, s))) return e;
+    if (t < T - 1 && (e = axpy(X.gslot(P.sep[t], 0), o(t, OSR), bb, m1, s))) return e;
+  }
+  e = for_task_runs(P, s2, t0, t1, [&](int t, int nt, int len) -> cudaError_t {
+    SweepWork W;
+    return chain_sweeps(X, P, s2, t, nt, len + 1, b, n_true, W, fail_layer, s);
+  });
+  if (e || *fail_layer >= 0) return e;
+  // couplings: G[x0_t, x0_t - 1] = -Y_t A[x0,-1] G_ss(t-1);  G[s_t, s_t + 1] = -G_ss(t) A[s,+1] Y_{t+1}
+  double2* tmp = static_cast<double2*>(arena_get(14, bb * sizeof(double2)));
+  if (!tmp) return cudaErrorMemoryAllocation;
+  for (int t = t0; t < t1; ++t) {
+    const int x0 = P.count[t] > 0 ? P.first[t] : P.sep[t];
+    if (t > 0) {
+      if ((e = mm(b, 1, 1.0, blk(o(t, OY), b), blk(X.aslot(x0, -1), b), 0.0, blk(tmp, b), s))) return e;
+      if ((e = mm(b, 1, -1.0, blk(tmp, b), blk(o(t - 1, OGSS), b), 0.0, blk(X.gslot(x0, -1), b), s))) return e;
+    }
+    if (t < T - 1) {
+      const int sp = P.sep[t];
+      if ((e = mm(b, 1, 1.0, blk(o(t, OGSS), b), blk(X.aslot(sp, 1), b), 0.0, blk(tmp, b), s))) return e;
+      if ((e = mm(b, 1, -1.0, blk(tmp, b), blk(o(t + 1, OY), b), 0.0, blk(X.gslot(sp, 1), b), s))) return e;
+    }
   }
   return cudaSuccess;
 }
 
-size_t ddrgf_scratch_bytes(int l, int b, int s2) {
+cudaError_t ddrgf_device(const double2* A, double2* G, int l, int b, const int* n_true, int s2, double gamma,
+                         void* scratch, size_t scratch_bytes, int* fail_layer, cudaStream_t s) {
   const Part P = partition(l, s2);
-  const long long bb = (long long)b * b;
-  return (size_t(8) * P.T + 8 + 2 * size_t(P.T)) * bb * sizeof(double2) + 4096;
+  const int T = P.T;
+  if (scratch_bytes < ddrgf_packet_bytes(T, b) + ddrgf_phase2_out_bytes(T, b)) return cudaErrorMemoryAllocation;
+  double2* packet = static_cast<double2*>(scratch);
+  double2* out = packet + (size_t)T * PK * b * b;
+  cudaError_t e;
+  if ((e = ddrgf_phase1(A, G, l, b, n_true, s2, gamma, 0, T, packet, fail_layer, s)) || *fail_layer >= 0) return e;
+  if ((e = ddrgf_phase2(packet, l, b, n_true, s2, gamma, out, fail_layer, s)) || *fail_layer >= 0) return e;
+  return ddrgf_phase3(A, G, l, b, n_true, s2, 0, T, out, fail_layer, s);
+}
+
+int ddrgf_num_tasks(int l, int s2) { return partition(l, s2).T; }
+
+size_t ddrgf_scratch_bytes(int l, int b, int s2) {
+  const int T = partition(l, s2).T;
+  return ddrgf_packet_bytes(T, b) + ddrgf_phase2_out_bytes(T, b) + 4096;
 }
 
 // Logical kernel counts of the reference ddrgf for this plan (walks the same

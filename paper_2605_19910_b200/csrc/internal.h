@@ -66,6 +66,17 @@ cudaError_t zmm(int b, int batch, double2 alpha, ZOp A, ZOp B, double beta, ZOp 
 cudaError_t ddrgf_device(const double2* A, double2* G, int l, int b, const int* n_true, int s2, double gamma,
                          void* scratch, size_t scratch_bytes, int* fail_layer, cudaStream_t s);
 size_t ddrgf_scratch_bytes(int l, int b, int s2);
+// Phases of the same algorithm on a rank-local slice (tasks [t0, t1)); only the
+// per-task interface packets cross ranks (csrc/ddrgf.cu).
+int ddrgf_num_tasks(int l, int s2);
+size_t ddrgf_packet_bytes(int ntask, int b);
+size_t ddrgf_phase2_out_bytes(int ntask, int b);
+cudaError_t ddrgf_phase1(const double2* A, double2* G, int l, int b, const int* n_true, int s2, double gamma, int t0,
+                         int t1, double2* packet, int* fail_layer, cudaStream_t s);
+cudaError_t ddrgf_phase2(const double2* packets, int l, int b, const int* n_true, int s2, double gamma, double2* out,
+                         int* fail_layer, cudaStream_t s);
+cudaError_t ddrgf_phase3(const double2* A, double2* G, int l, int b, const int* n_true, int s2, int t0, int t1,
+                         const double2* out, int* fail_layer, cudaStream_t s);
 void ddrgf_reference_counters(long long l, const int* s2_levels, int n_levels, long long out[3]);
 
 // Launch accounting / optional event timing around one kernel launch (prof.cu).

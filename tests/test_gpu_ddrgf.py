@@ -105,3 +105,31 @@ def test_dyson_matrices_within_bar(gpu, l, b, s2, eta, E):
     ref, _ = O.rgf_tridiag(a)
     g, _ = P.ddrgf(to_product(a), _plan([s2]))
     assert max_err(g, ref) <= 1e-10
+
+
+@pytest.mark.parametrize("l,b,s2,world", [(63, 64, 7, 2), (70, 64, 8, 3), (45, 128, 10, 4)])
+def test_sharded_phases_emulated_ranks(gpu, l, b, s2, world):
+    """The domain-sharded protocol with the CUDA phases, ranks emulated one after the
+    other on one device (packets concatenated instead of all-gathered)."""
+    import torch
+
+    from paper_2605_19910_b200 import distributed as Dd
+
+    a = DO.dyson_matrix(DO.hamiltonian(l, 1, b, 4), complex(-0.2, 1e-4), 1)
+    ref, _ = O.rgf_tridiag(a)
+    full = torch.from_numpy(np.ascontiguousarray(a.data.transpose(0, 1, 3, 2))).cuda()
+    tasks = Dd.partition(l, s2)
+    ranges = Dd.task_ranges(len(tasks), world)
+    eng = Dd.CudaPhases(l, b, s2)
+    packets, locs = [], []
+    for t0, t1 in ranges:
+        L0, L1 = Dd.layer_range(tasks, t0, t1)
+        A_loc = full[L0:L1].clone()
+        packets.append(eng.phase1(A_loc, t0, t1))
+        locs.append((L0, L1, A_loc, t0, t1))
+    out = eng.phase2(torch.cat(packets))
+    G = torch.zeros_like(full)
+    for L0, L1, A_loc, t0, t1 in locs:
+        G[L0:L1] = eng.phase3(A_loc, out, t0, t1)
+    got = O.Band(a.layout, np.ascontiguousarray(G.cpu().numpy().transpose(0, 1, 3, 2)))
+    assert O.max_block_error(got, ref) <= 1e-10
