@@ -212,7 +212,10 @@ def run_ours(args, rank, world, local_rank):
     H = torch.empty((l, 2 * w + 1, b, b), dtype=torch.complex128, device=dev)
     D.fill_h_device(cfg, H)
     G = torch.empty((n_loc, l, 2 * w + 1, b, b), dtype=torch.complex128, device=dev)
-    stream = torch.cuda.current_stream()
+    # a dedicated (non-default) stream: the library captures the static per-step
+    # launch sequence into a CUDA graph after the first call (legacy stream 0 cannot be captured)
+    stream = torch.cuda.Stream(device=dev)
+    torch.cuda.set_stream(stream)
 
     def step():
         D.solve_device(cfg, H, G, z=zs, stream=stream)

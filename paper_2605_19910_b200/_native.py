@@ -6,9 +6,10 @@ module raises at import / first use.
 from __future__ import annotations
 
 import ctypes as C
+import os
 from pathlib import Path
 
-LIB_PATH = Path(__file__).resolve().parent / "_lib" / "libbbsi_cuda.so"
+LIB_PATH = Path(os.environ.get("BBSI_LIB") or Path(__file__).resolve().parent / "_lib" / "libbbsi_cuda.so")
 
 # Every symbol include/bbsi_cuda.h declares, with its ctypes signature.
 _vp, _ip, _i, _ll, _d = C.c_void_p, C.POINTER(C.c_int), C.c_int, C.c_longlong, C.c_double

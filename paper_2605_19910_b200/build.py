@@ -25,25 +25,31 @@ def _stale() -> bool:
     return any(p.exists() and p.stat().st_mtime > t for p in deps)
 
 
-def build(force: bool = False, verbose: bool = False) -> Path:
+def build(force: bool = False, verbose: bool = False, extra: tuple = (), out: Path | None = None) -> Path:
+    """extra/out: instrumented variants (e.g. -DBBSI_ZINV_DEBUG into _lib/libbbsi_cuda_dbg.so,
+    loaded with BBSI_LIB=...); the default call builds the product library."""
     srcs = [s for s in SOURCES if (CSRC / s).exists()]
-    if not force and not _stale():
+    lib = Path(out) if out else LIB
+    if out is None and not force and not _stale():
         return LIB
     LIB_DIR.mkdir(exist_ok=True)
     objs = []
     for s in srcs:
-        obj = LIB_DIR / (Path(s).stem + ".o")
-        cmd = [NVCC, *FLAGS, "-dc" if False else "-c", str(CSRC / s), "-o", str(obj)]
+        obj = LIB_DIR / (Path(s).stem + lib.stem + ".o")
+        cmd = [NVCC, *FLAGS, *extra, "-c", str(CSRC / s), "-o", str(obj)]
         if verbose:
             print(" ".join(cmd), file=sys.stderr)
         subprocess.run(cmd, check=True, cwd=CSRC)
         objs.append(str(obj))
-    cmd = [NVCC, "-shared", "-gencode", "arch=compute_100a,code=sm_100a", *objs, "-o", str(LIB), "-cudart", "static"]
+    cmd = [NVCC, "-shared", "-gencode", "arch=compute_100a,code=sm_100a", *objs, "-o", str(lib), "-cudart", "static"]
     subprocess.run(cmd, check=True, cwd=CSRC)
     for o in objs:
         Path(o).unlink(missing_ok=True)
-    return LIB
+    return lib
 
 
 if __name__ == "__main__":
-    print(build(force="--force" in sys.argv, verbose=True))
+    if "--debug-zinv" in sys.argv:
+        print(build(verbose=True, extra=("-DBBSI_ZINV_DEBUG",), out=LIB_DIR / "libbbsi_cuda_dbg.so"))
+    else:
+        print(build(force="--force" in sys.argv, verbose=True))

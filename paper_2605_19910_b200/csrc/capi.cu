@@ -2,6 +2,7 @@
 // reference's preconditions and messages (layout.hpp:27-38, rgf.hpp:41-42,86-87,
 // ddrgf.hpp:26-31,424-425); failures map onto the reference exception contract.
 #include <cstdio>
+#include <map>
 #include <cstdlib>
 #include <cstring>
 #include <mutex>
@@ -105,6 +106,68 @@ void unpad_band(const std::vector<double2>& in, int bp, const HostBand& h, doubl
       const int r = h.sz[a], c = h.sz[a + off];
       for (int j = 0; j < c; ++j) std::memcpy(d + (long long)j * h.bs, s + (long long)j * bp, sizeof(double2) * r);
     }
+}
+
+// ---- CUDA-graph replay of a static launch sequence (a sweep is ~10^4 small
+// launches per step). Keyed by shapes and every device pointer the sequence
+// touches; the first call runs eagerly, the second captures, later calls replay.
+struct GraphEntry {
+  cudaGraphExec_t exec = nullptr;
+  long long launches = 0;
+};
+std::mutex g_graph_mu;
+std::map<std::string, GraphEntry> g_graphs;
+
+bool graphs_enabled() {
+  const char* e = getenv("BBSI_GRAPHS");
+  return !(e && e[0] == '0');
+}
+
+template <class F>
+cudaError_t run_graphed(const std::string& key, cudaStream_t s, F&& enqueue) {
+  if (!graphs_enabled() || prof_enabled() || s == nullptr) return enqueue(s);
+  std::lock_guard<std::mutex> lk(g_graph_mu);
+  auto it = g_graphs.find(key);
+  if (it == g_graphs.end()) {
+    g_graphs.emplace(key, GraphEntry{});
+    return enqueue(s);
+  }
+  if (!it->second.exec) {
+    const long long c0 = launch_count();
+    cudaError_t e = cudaStreamBeginCapture(s, cudaStreamCaptureModeThreadLocal);
+    if (e) return e;
+    cudaError_t e2 = enqueue(s);
+    cudaGraph_t g = nullptr;
+    e = cudaStreamEndCapture(s, &g);
+    if (e2 || e) {
+      if (g) cudaGraphDestroy(g);
+      cudaGetLastError();
+      g_graphs.erase(it);  // fall back to eager launches for this key
+      return enqueue(s);
+    }
+    cudaGraphExec_t x = nullptr;
+    e = cudaGraphInstantiate(&x, g, 0);
+    cudaGraphDestroy(g);
+    if (e) {
+      cudaGetLastError();
+      g_graphs.erase(it);
+      return enqueue(s);
+    }
+    it->second.exec = x;
+    it->second.launches = launch_count() - c0;
+    return cudaGraphLaunch(x, s);
+  }
+  launch_count_add(it->second.launches);
+  return cudaGraphLaunch(it->second.exec, s);
+}
+
+std::string graph_key(const char* tag, std::initializer_list<long long> v) {
+  std::string k(tag);
+  int dev = 0;
+  cudaGetDevice(&dev);
+  k += ":" + std::to_string(dev);
+  for (long long x : v) k += ":" + std::to_string(x);
+  return k;
 }
 
 // Runs the batched sweeps on a device band (already holding A) with the arena scratch.
@@ -296,8 +359,6 @@ int bbsi_cuda_dyson_rgf_dev(int l, int w, int bs, int n_energy, const double* dH
   if (!dzs) return fail(BBSI_OUT_OF_MEMORY, "parameter upload allocation failed");
   CK(cudaMemcpyAsync(dzs, z, sizeof(double2) * n_energy, cudaMemcpyHostToDevice, s));
   CK(cudaMemcpyAsync(dzs + n_energy, sigma, sizeof(double2) * l, cudaMemcpyHostToDevice, s));
-  CK(dyson_form_band(reinterpret_cast<double2*>(dG), reinterpret_cast<const double2*>(dH), l, w, bs, n_energy, dzs,
-                     dzs + n_energy, s));
   SweepWork W;
   W.l = l;
   W.w = w;
@@ -305,8 +366,19 @@ int bbsi_cuda_dyson_rgf_dev(int l, int w, int bs, int n_energy, const double* dH
   W.batch = n_energy;
   W.G = reinterpret_cast<double2*>(dG);
   W.g_bstride = (long long)l * (2 * w + 1) * bs * bs;
+  W.groups = default_groups(W.batch, W.bs);
+  void* scratch = arena_get(1, sweep_scratch_bytes(W.l, W.w, W.bs, W.batch, W.groups));
+  if (!scratch) return fail(BBSI_OUT_OF_MEMORY, "sweep workspace allocation failed");
+  sweep_carve(W, scratch);
   std::vector<int> nt(l, bs), fails;
-  if (int rc = run_sweeps(W, nt, fails, s)) return rc;
+  const std::string key = graph_key("dyson", {l, w, bs, n_energy, (long long)dH, (long long)dG, (long long)dzs,
+                                              (long long)scratch, W.groups});
+  CK(run_graphed(key, s, [&](cudaStream_t st) -> cudaError_t {
+    cudaError_t e = dyson_form_band(reinterpret_cast<double2*>(dG), reinterpret_cast<const double2*>(dH), l, w, bs,
+                                    n_energy, dzs, dzs + n_energy, st);
+    return e ? e : rgf_sweeps(W, nt.data(), st);
+  }));
+  CK(collect_failures(W, fails, s));
   bool bad = false;
   for (int b = 0; b < n_energy; ++b) {
     if (fail_layers) fail_layers[b] = fails[b];

@@ -94,6 +94,8 @@ class ProfScope {
   double flops_ = 0, bytes_ = 0;
 };
 long long launch_count();
+void launch_count_add(long long n);
+bool prof_enabled();
 void prof_enable(bool on);
 int prof_collect(double* out, int ncat);
 double fp64_dmma_peak(double duration_ms, int reps);

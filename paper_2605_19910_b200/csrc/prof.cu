@@ -53,6 +53,11 @@ ProfScope::~ProfScope() {
 }
 
 long long launch_count() { return g_launches.load(); }
+void launch_count_add(long long n) { g_launches.fetch_add(n, std::memory_order_relaxed); }
+bool prof_enabled() {
+  std::lock_guard<std::mutex> lk(g_mu);
+  return g_on;
+}
 
 void prof_enable(bool on) {
   std::lock_guard<std::mutex> lk(g_mu);

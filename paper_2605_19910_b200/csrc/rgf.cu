@@ -32,8 +32,9 @@ int default_groups(int batch, int bs) {
     if (g >= 1) return g < batch ? g : batch;
   }
   (void)bs;
-  int g = 1;  // measured: 2 side-stream groups were slower on B200 at batch 64 (990 vs 860 ms)
-  return g;
+  // Two side-stream groups: one group's latency-bound panels overlap the other's
+  // GEMMs (B200, config 2, 64 energies: 739 ms vs 771 ms with one group).
+  return batch >= 8 ? 2 : 1;
 }
 
 size_t sweep_scratch_bytes(int l, int w, int bs, int batch, int groups) {

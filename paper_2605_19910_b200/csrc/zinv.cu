@@ -8,16 +8,15 @@
 // become plain GEMMs with the explicit inverse.
 //
 // Block sweep on the panel K = [k, k+nb) with pivot rows P (after interchanges):
-//   M[P,K] <- Pinv = (L_P U)^{-1},  M[P,C] <- Pinv M[P,C],
+//   M[P,K] <- Pinv = (L_P U)^{-1},  M[P,C] <- Pinv M[P,C]  (both = V below),
 //   M[R,K] <- -M[R,K] Pinv,         M[R,C] <- M[R,C] - M[R,K] Pinv M[P,C].
 // Per panel:
 //   gj_panel (1 CTA / matrix): tall-panel LU with partial pivoting of rows k..n-1
 //     (|re|+|im| pivot choice, first index on ties, as izamax in zgetrf); the
-//     row interchanges become a row map; Pinv by warp-parallel triangular solves;
-//     Wz = M[:,K] in post-interchange row order with -I on the pivot rows;
-//     Vs = M[P,:] with the identity in the K columns.
-//   GEMM 1: V = Pinv Vs                                  (nb x n)
-//   GEMM 2: Next = Cur[rowmap] (0 on rows P / cols K) - Wz V  (n x n, all SMs)
+//     row interchanges become a row map; Wz = M[:,K] in post-interchange row
+//     order with -I on the pivot rows; V = U^{-1} L^{-1} M[P,:] (identity in the
+//     K columns, so V[:,K] = Pinv) by triangular solves, one column per thread.
+//   GEMM:  Next = Cur[rowmap] (0 on rows P / cols K) - Wz V  (n x n, all SMs)
 // Cur/Next ping-pong between the input block and two scratch matrices; the last
 // panel's GEMM writes into the input block with the column map that undoes the
 // interchanges (X = Y P), so no separate un-pivoting pass exists.
@@ -61,6 +60,16 @@ int pick_nb(int n) {
   }();
   if (forced == 32 && size_t(n) * 32 * sizeof(double2) <= 200 * 1024) return 32;
   return 16;
+}
+
+int panel_priority() {
+  static int p = [] {
+    int lo = 0, hi = 0;
+    if (cudaDeviceGetStreamPriorityRange(&lo, &hi) != cudaSuccess) return 0;
+    const char* e = getenv("BBSI_PANEL_PRIORITY");
+    return (e && atoi(e) == 0) ? lo : hi;  // hi = greatest priority (numerically lowest)
+  }();
+  return p;
 }
 
 size_t align256(size_t x) { return (x + 255) & ~size_t(255); }
@@ -422,36 +431,9 @@ __global__ void __launch_bounds__(PT, 1)
     if (r >= k && r < k + NB) s_src[r - k] = src;
   }
 
-  // ---- Pinv = U^{-1} L^{-1} of the pivot block (logical rows 0..NB-1): warp per column
-  {
-    double2* __restrict__ pinv = S.pinv + (long long)b * NB * NB;
-    const bool act = lane < NB;
-    const int row = act ? lane : 0;
-    const int prow_ph = fperm[row];
-    const double2 dinv = crcp_fast(pn[row * ldp + prow_ph]);
-#pragma unroll 1
-    for (int c = warp; c < NB; c += PT / 32) {
-      double2 t = make_double2(lane == c ? 1.0 : 0.0, 0.0);
-#pragma unroll
-      for (int q = 0; q < NB; ++q) {  // forward: unit lower L
-        const double2 lq = pn[q * ldp + prow_ph];
-        double2 tq;
-        tq.x = __shfl_sync(0xffffffffu, t.x, q);
-        tq.y = __shfl_sync(0xffffffffu, t.y, q);
-        if (act && lane > q) t = csub(t, cmul(lq, tq));
-      }
-#pragma unroll
-      for (int q = NB - 1; q >= 0; --q) {  // backward: upper U
-        const double2 uq = pn[q * ldp + prow_ph];
-        if (lane == q) t = cmul(t, dinv);
-        double2 xq;
-        xq.x = __shfl_sync(0xffffffffu, t.x, q);
-        xq.y = __shfl_sync(0xffffffffu, t.y, q);
-        if (lane < q) t = csub(t, cmul(uq, xq));
-      }
-      if (act) pinv[c * NB + lane] = t;
-    }
-  }
+  // 1 / U[j][j] of the pivot block (logical rows 0..NB-1, physical fperm[j])
+  __shared__ double2 s_uinv[NB];
+  if (tid < NB) s_uinv[tid] = crcp_fast(pn[tid * ldp + fperm[tid]]);
   __syncthreads();
 
   // ---- Wz (n x NB, ld n): current M[:,K] in post-interchange order, -I on pivot rows
@@ -474,24 +456,33 @@ __global__ void __launch_bounds__(PT, 1)
       }
     }
   }
-  // ---- Vs (NB x n, ld NB): pivot rows of M after interchanges, identity in columns K
+  // ---- V (NB x n, ld NB) = U^{-1} L^{-1} Vs, Vs = pivot rows of M after the
+  //      interchanges with the identity in columns K (so V[:,K] = (L U)^{-1}).
+  //      Triangular solves, one column per thread: backward stable, no explicit
+  //      inverse of the pivot block.
   {
-    double2* __restrict__ vs = S.vs + (long long)b * NB * n;
-    for (int base = tid; base < n * NB; base += 4 * PT) {
-      double2 v[4];
+    double2* __restrict__ vb = S.vbuf + (long long)b * NB * n;
+    for (int col = tid; col < n; col += PT) {
+      const bool kc = col >= k && col < k + NB;
+      double2 x[NB];
 #pragma unroll
-      for (int u = 0; u < 4; ++u) {
-        const int idx = base + u * PT;
-        const int j = idx % NB, col = idx / NB;
-        if (idx < n * NB)
-          v[u] = (col >= k && col < k + NB) ? make_double2(col - k == j ? 1.0 : 0.0, 0.0)
-                                            : cur[(long long)col * ld + s_src[j]];
+      for (int j = 0; j < NB; ++j)
+        x[j] = kc ? make_double2(col - k == j ? 1.0 : 0.0, 0.0) : cur[(long long)col * ld + s_src[j]];
+#pragma unroll
+      for (int j = 1; j < NB; ++j) {  // L (unit lower): x_j -= sum_{q<j} L[j][q] x_q
+        const int pj = fperm[j];
+#pragma unroll
+        for (int q = 0; q < j; ++q) x[j] = csub(x[j], cmul(pn[q * ldp + pj], x[q]));
       }
 #pragma unroll
-      for (int u = 0; u < 4; ++u) {
-        const int idx = base + u * PT;
-        if (idx < n * NB) vs[idx] = v[u];
+      for (int j = NB - 1; j >= 0; --j) {  // U: x_j = (x_j - sum_{q>j} U[j][q] x_q) / U[j][j]
+        const int pj = fperm[j];
+#pragma unroll
+        for (int q = j + 1; q < NB; ++q) x[j] = csub(x[j], cmul(pn[q * ldp + pj], x[q]));
+        x[j] = cmul(x[j], s_uinv[j]);
       }
+#pragma unroll
+      for (int j = 0; j < NB; ++j) vb[(long long)col * NB + j] = x[j];
     }
   }
   __syncthreads();
@@ -565,32 +556,33 @@ cudaError_t zinv_batched(double2* M, long long ld, long long bstride, int n, int
     const long long nld = last ? ld : n, nbs = last ? bstride : nn;
     {
       ProfScope prof(stream, PROF_INV, 8.0 * double(n) * nb * nb * batch, 16.0 * (3.0 * n * nb) * batch);
+      // The panel is latency-bound and on the critical path of the sweep: launched at
+      // the greatest priority so its CTAs take SMs ahead of queued GEMM tiles of
+      // other streams (side-stream groups).
+      cudaLaunchConfig_t cfg{};
+      cfg.gridDim = dim3(batch);
+      cfg.blockDim = dim3(PT);
+      cfg.dynamicSmemBytes = smem;
+      cfg.stream = stream;
+      cudaLaunchAttribute attr[1];
+      attr[0].id = cudaLaunchAttributePriority;
+      attr[0].val.priority = panel_priority();
+      cfg.attrs = attr;
+      cfg.numAttrs = 1;
       if (nb == 32)
-        gj_panel_kernel<32><<<batch, PT, smem, stream>>>(cur, cld, cbs, n, n_true, k, S, status);
+        e = cudaLaunchKernelEx(&cfg, gj_panel_kernel<32>, (const double2*)cur, cld, cbs, n, n_true, k, S, status);
       else
-        gj_panel_kernel<16><<<batch, PT, smem, stream>>>(cur, cld, cbs, n, n_true, k, S, status);
-      if ((e = cudaGetLastError())) return e;
+        e = cudaLaunchKernelEx(&cfg, gj_panel_kernel<16>, (const double2*)cur, cld, cbs, n, n_true, k, S, status);
+      if (e) return e;
       if (last) {
         build_colmap_kernel<<<batch, 256, 2 * n * sizeof(int), stream>>>(S.piv, S.colmap, n);
         if ((e = cudaGetLastError())) return e;
       }
     }
-    // GEMM 1: V = Pinv * Vs
     ZGemmGroup g{};
     g.batch = batch;
     g.bs = 64;
     g.nprob = 1;
-    ZGemmProblem& p1 = g.prob[0];
-    p1.M = nb;
-    p1.N = n;
-    p1.K = nb;
-    p1.alpha = make_double2(1.0, 0.0);
-    p1.beta = make_double2(0.0, 0.0);
-    p1.A = ZOp{S.pinv, nb, 64, 64LL * nb, (long long)nb * nb};
-    p1.B = ZOp{S.vs, nb, 64, 64LL * nb, (long long)nb * n};
-    p1.D = ZOp{S.vbuf, nb, 64, 64LL * nb, (long long)nb * n};
-    p1.C = p1.D;
-    if ((e = zgemm_grouped(g, stream))) return e;
     // GEMM 2: Next = Cur[rowmap] (zero on rows P, cols K) - Wz * V
     ZGemmProblem& p2 = g.prob[0];
     p2 = ZGemmProblem{};
