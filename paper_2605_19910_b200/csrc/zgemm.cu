@@ -9,6 +9,8 @@
 // Complex product with 4 real DMMAs per 8x8x4 step (no 3M trick: same rounding
 // class as zgemm). CTA tile 64x64 complex, 4 warps of 32x32, K staged 16 at a
 // time through a 2-stage cp.async pipeline into padded, bank-conflict-free smem.
+#include <cstdlib>
+
 #include "internal.h"
 
 namespace bbsi_gpu {
@@ -56,8 +58,10 @@ __device__ __forceinline__ void load_tile(const ZGemmProblem& P, int bs, int bat
   }
 }
 
-template <bool PLAIN>
-__global__ void __launch_bounds__(128, 2) zgemm_grouped_kernel(const __grid_constant__ ZGemmGroup g) {
+// MINB = resident CTAs per SM the register budget is sized for (2: 243 regs, no
+// spills; 3: 168 regs, 12 warps per SM, a few epilogue spills).
+template <bool PLAIN, int MINB>
+__global__ void __launch_bounds__(128, MINB) zgemm_grouped_kernel(const __grid_constant__ ZGemmGroup g) {
   extern __shared__ __align__(16) double2 smem[];
   double2* As = smem;
   double2* Bs = smem + STAGES * A_STAGE;
@@ -259,16 +263,28 @@ __global__ void __launch_bounds__(128, 2) zgemm_grouped_kernel(const __grid_cons
 
 }  // namespace
 
-cudaError_t zgemm_grouped(ZGemmGroup& g, cudaStream_t stream) {
-  static bool attr_set = false;
-  if (!attr_set) {
-    cudaError_t e = cudaFuncSetAttribute(zgemm_grouped_kernel<false>, cudaFuncAttributeMaxDynamicSharedMemorySize,
+int gemm_minb() {
+  static int m = [] {
+    const char* e = getenv("BBSI_GEMM_MINB");
+    return (e && atoi(e) == 2) ? 2 : 3;
+  }();
+  return m;
+}
+
+template <bool PLAIN, int MINB>
+cudaError_t gemm_attrs() {
+  static cudaError_t e = [] {
+    cudaError_t r = cudaFuncSetAttribute(zgemm_grouped_kernel<PLAIN, MINB>, cudaFuncAttributeMaxDynamicSharedMemorySize,
                                          SMEM_BYTES);
-    if (e == cudaSuccess)
-      e = cudaFuncSetAttribute(zgemm_grouped_kernel<true>, cudaFuncAttributeMaxDynamicSharedMemorySize, SMEM_BYTES);
-    if (e != cudaSuccess) return e;
-    attr_set = true;
-  }
+    if (r == cudaSuccess)
+      r = cudaFuncSetAttribute(zgemm_grouped_kernel<PLAIN, MINB>, cudaFuncAttributePreferredSharedMemoryCarveout,
+                               cudaSharedmemCarveoutMaxShared);
+    return r;
+  }();
+  return e;
+}
+
+cudaError_t zgemm_grouped(ZGemmGroup& g, cudaStream_t stream) {
   int total = 0;
   bool plain = true;
   auto is_plain = [&](const ZOp& o) { return o.rs == g.bs && o.cs == (long long)g.bs * o.ld; };
@@ -291,10 +307,21 @@ cudaError_t zgemm_grouped(ZGemmGroup& g, cudaStream_t stream) {
     by += 16.0 * g.batch * (double(P.M) * P.K + double(P.K) * P.N + double(P.M) * P.N * (rc ? 2 : 1));
   }
   ProfScope prof(stream, PROF_GEMM, fl, by);
-  if (plain)
-    zgemm_grouped_kernel<true><<<total, 128, SMEM_BYTES, stream>>>(g);
-  else
-    zgemm_grouped_kernel<false><<<total, 128, SMEM_BYTES, stream>>>(g);
+  cudaError_t e;
+  const bool three = gemm_minb() == 3;
+  if (plain && three) {
+    if ((e = gemm_attrs<true, 3>())) return e;
+    zgemm_grouped_kernel<true, 3><<<total, 128, SMEM_BYTES, stream>>>(g);
+  } else if (plain) {
+    if ((e = gemm_attrs<true, 2>())) return e;
+    zgemm_grouped_kernel<true, 2><<<total, 128, SMEM_BYTES, stream>>>(g);
+  } else if (three) {
+    if ((e = gemm_attrs<false, 3>())) return e;
+    zgemm_grouped_kernel<false, 3><<<total, 128, SMEM_BYTES, stream>>>(g);
+  } else {
+    if ((e = gemm_attrs<false, 2>())) return e;
+    zgemm_grouped_kernel<false, 2><<<total, 128, SMEM_BYTES, stream>>>(g);
+  }
   return cudaGetLastError();
 }
 

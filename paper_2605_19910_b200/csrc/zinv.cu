@@ -62,6 +62,15 @@ int pick_nb(int n) {
   return 16;
 }
 
+// BBSI_PANEL_ROWS=0 selects the shared-memory panel kernel everywhere (A/B checks).
+bool use_rows_kernel() {
+  static bool on = [] {
+    const char* e = getenv("BBSI_PANEL_ROWS");
+    return !(e && atoi(e) == 0);
+  }();
+  return on;
+}
+
 int panel_priority() {
   static int p = [] {
     int lo = 0, hi = 0;
@@ -102,6 +111,105 @@ __device__ __forceinline__ void argmax_merge(double& v, int& i, double v2, int i
   }
 }
 
+// Everything after the pivot search, shared by both panel kernels.
+//   lu[j][c]  pivot row j (logical): L multipliers for c < j, U for c >= j
+//   lmap[r]   panel-local logical row r -> physical (= original) row
+//   lpiv[j]   LAPACK-style interchange partner of step j (panel-local)
+// Writes rowmap / piv, Wz and V, and the first negligible U-diagonal column.
+template <int NB>
+__device__ __forceinline__ void panel_tail(const double2* __restrict__ cur, long long ld, int n, int n_true, int k, int b,
+                                           const GjScratch& S, int* __restrict__ status, const double2 (*lu)[NB + 1],
+                                           const int* lmap, const int* lpiv, double tol, int* s_fail) {
+  __shared__ double2 s_uinv[NB];
+  __shared__ int s_src[NB];
+  const int tid = threadIdx.x;
+  int* __restrict__ rowmap = S.rowmap + (long long)b * n;
+  if (tid < NB) {
+    const double2 d = lu[tid][tid];
+    if (k + tid < n_true && hypot(d.x, d.y) <= tol) atomicMin(s_fail, k + tid);  // kernels.hpp:149-158
+    s_uinv[tid] = crcp_fast(d);
+    S.piv[(long long)b * n + k + tid] = k + lpiv[tid];
+  }
+  // row map of the interchanges: new row r holds old row rowmap[r]
+  for (int r = tid; r < n; r += PT) {
+    const int src = r < k ? r : k + lmap[r - k];
+    rowmap[r] = src;
+    if (r >= k && r < k + NB) s_src[r - k] = src;
+  }
+  __syncthreads();
+  // Wz (n x NB, ld n): current M[:,K] in post-interchange order, -I on the pivot rows
+  {
+    double2* __restrict__ wz = S.wz + (long long)b * n * NB;
+#pragma unroll 1
+    for (int c = 0; c < NB; c += 4) {
+      for (int r = tid; r < n; r += PT) {
+        const bool pr = r >= k && r < k + NB;
+        const int src = r < k ? r : k + lmap[r - k];
+        double2 v[4];
+#pragma unroll
+        for (int u = 0; u < 4; ++u)
+          v[u] = pr ? make_double2(r - k == c + u ? -1.0 : 0.0, 0.0) : cur[(long long)(k + c + u) * ld + src];
+#pragma unroll
+        for (int u = 0; u < 4; ++u) wz[(long long)(c + u) * n + r] = v[u];
+      }
+    }
+  }
+  // V (NB x n, ld NB) = U^{-1} L^{-1} Vs, Vs = pivot rows of M after the interchanges
+  // with the identity in columns K (so V[:,K] = (L U)^{-1}); triangular solves, one
+  // column per thread (backward stable, no explicit inverse of the pivot block).
+  {
+    double2* __restrict__ vb = S.vbuf + (long long)b * NB * n;
+    for (int col = tid; col < n; col += PT) {
+      const bool kc = col >= k && col < k + NB;
+      double2 x[NB];
+#pragma unroll
+      for (int j = 0; j < NB; ++j)
+        x[j] = kc ? make_double2(col - k == j ? 1.0 : 0.0, 0.0) : cur[(long long)col * ld + s_src[j]];
+#pragma unroll
+      for (int j = 1; j < NB; ++j) {  // unit lower L
+#pragma unroll
+        for (int q = 0; q < j; ++q) x[j] = csub(x[j], cmul(lu[j][q], x[q]));
+      }
+#pragma unroll
+      for (int j = NB - 1; j >= 0; --j) {  // upper U
+#pragma unroll
+        for (int q = j + 1; q < NB; ++q) x[j] = csub(x[j], cmul(lu[j][q], x[q]));
+        x[j] = cmul(x[j], s_uinv[j]);
+      }
+#pragma unroll
+      for (int j = 0; j < NB; ++j) vb[(long long)col * NB + j] = x[j];
+    }
+  }
+  __syncthreads();
+  if (tid == 0 && *s_fail != INT_MAX && status[b] < 0) status[b] = *s_fail;
+}
+
+// max |a_ij| (hypot) over the true n_true x n_true block -> eps * n_true * max (kernels.hpp:149-158)
+__device__ __forceinline__ double panel_threshold(const double2* __restrict__ cur, long long ld, int n_true,
+                                                  double* red) {
+  const int tid = threadIdx.x, lane = tid & 31, warp = tid >> 5;
+  double mx = 0.0;
+  for (int r = tid; r < n_true; r += PT) {
+#pragma unroll 1
+    for (int c0 = 0; c0 < n_true; c0 += 16) {
+      double2 v[16];
+#pragma unroll
+      for (int u = 0; u < 16; ++u)
+        v[u] = (c0 + u < n_true) ? cur[(long long)(c0 + u) * ld + r] : make_double2(0.0, 0.0);
+#pragma unroll
+      for (int u = 0; u < 16; ++u) mx = fmax(mx, hypot(v[u].x, v[u].y));
+    }
+  }
+#pragma unroll
+  for (int o = 16; o; o >>= 1) mx = fmax(mx, __shfl_xor_sync(0xffffffffu, mx, o));
+  if (lane == 0) red[warp] = mx;
+  __syncthreads();
+  double m = 0.0;
+#pragma unroll
+  for (int q = 0; q < PT / 32; ++q) m = fmax(m, red[q]);
+  return DBL_EPSILON * double(n_true) * m;
+}
+
 template <int NB>
 __global__ void __launch_bounds__(PT, 1)
     gj_panel_kernel(const double2* __restrict__ cur0, long long ld, long long bstride, int n, int n_true, int k,
@@ -110,7 +218,6 @@ __global__ void __launch_bounds__(PT, 1)
   __shared__ double cand_v[2][PT / 32];
   __shared__ int cand_i[2][PT / 32];
   __shared__ int s_piv[NB];   // pivot row (panel-local) chosen at step j
-  __shared__ int s_src[NB];   // source row (global index) of pivot row k+j after interchanges
   __shared__ int s_fail;
   __shared__ double s_tol;
 
@@ -119,7 +226,6 @@ __global__ void __launch_bounds__(PT, 1)
   const double2* __restrict__ cur = cur0 + (long long)b * bstride;
   const int rows = n - k;
   const int ldp = rows + 1;
-  int* __restrict__ rowmap = S.rowmap + (long long)b * n;
   int* __restrict__ piv = S.piv + (long long)b * n;
 
 #ifdef BBSI_ZINV_DEBUG
@@ -129,32 +235,12 @@ __global__ void __launch_bounds__(PT, 1)
 #endif
   DBG(0)
   if (tid == 0) s_fail = INT_MAX;
-  if (k == 0) {  // threshold eps * n * max|A| over the true block (kernels.hpp:149-158)
-    double mx = 0.0;
-    for (int r = tid; r < n_true; r += PT) {
-#pragma unroll 1
-      for (int c0 = 0; c0 < n_true; c0 += 8) {
-        double2 v[8];
-#pragma unroll
-        for (int u = 0; u < 8; ++u)
-          v[u] = (c0 + u < n_true) ? cur[(long long)(c0 + u) * ld + r] : make_double2(0.0, 0.0);
-#pragma unroll
-        for (int u = 0; u < 8; ++u) mx = fmax(mx, hypot(v[u].x, v[u].y));
-      }
-    }
-#pragma unroll
-    for (int o = 16; o; o >>= 1) mx = fmax(mx, __shfl_xor_sync(0xffffffffu, mx, o));
-    if (lane == 0) cand_v[1][warp] = mx;
-    __syncthreads();
-    if (warp == 0) {
-      double m = cand_v[1][lane];
-#pragma unroll
-      for (int o = 16; o; o >>= 1) m = fmax(m, __shfl_xor_sync(0xffffffffu, m, o));
-      if (lane == 0) {
-        s_tol = DBL_EPSILON * double(n_true) * m;
-        S.tol[b] = s_tol;
-        status[b] = -1;
-      }
+  if (k == 0) {
+    const double t = panel_threshold(cur, ld, n_true, cand_v[1]);
+    if (tid == 0) {
+      s_tol = t;
+      S.tol[b] = t;
+      status[b] = -1;
     }
   } else if (tid == 0) {
     s_tol = S.tol[b];
@@ -212,129 +298,7 @@ __global__ void __launch_bounds__(PT, 1)
   }
 
   const int nwarp_rows = (rows + 31) / 32 < PT / 32 ? (rows + 31) / 32 : PT / 32;
-  // The register-resident variant measured slower than the shared-memory one on
-  // B200 (4.6k vs 3.9k cycles per column at n = 256); kept for experiments.
-  constexpr bool kRegPath = false;
-  const bool reg = kRegPath && rows <= PT;
-  if (reg) {
-    // ---- register path: physical row t is owned by thread t and kept in
-    // registers; interchanges only relabel logical indices. Per column: one
-    // barrier; each warp's best candidate lane publishes its whole row, every
-    // warp resolves the pivot redundantly and reads the winning row.
-    __shared__ double2 cand_row[2][PT / 32][NB];
-    __shared__ int cand_ph[2][PT / 32];
-    const int t = tid;
-    const bool own = t < rows;
-    double2 a[NB];
-#pragma unroll
-    for (int c = 0; c < NB; ++c) a[c] = own ? pn[c * ldp + t] : make_double2(0.0, 0.0);
-    int mylog = t;
-    auto publish_reg = [&](int par, double bv, int blog) {
-      int bph = t;
-#pragma unroll
-      for (int o = 16; o; o >>= 1) {
-        double v2 = __shfl_xor_sync(0xffffffffu, bv, o);
-        int i2 = __shfl_xor_sync(0xffffffffu, blog, o);
-        int p2 = __shfl_xor_sync(0xffffffffu, bph, o);
-        if (v2 > bv || (v2 == bv && i2 < blog)) {
-          bv = v2;
-          blog = i2;
-          bph = p2;
-        }
-      }
-      if (bph == t && blog != INT_MAX) {
-#pragma unroll
-        for (int c = 0; c < NB; ++c) cand_row[par][warp][c] = a[c];
-      }
-      if (lane == 0) {
-        cand_v[par][warp] = bv;
-        cand_i[par][warp] = blog;
-        cand_ph[par][warp] = bph;
-      }
-    };
-    __syncthreads();  // everyone has consumed the smem-path candidates of column 0
-    publish_reg(0, own ? cabs1(a[0]) : -1.0, own ? t : INT_MAX);
-#pragma unroll 1
-    for (int j = 0; j < NB; ++j) {
-      const int par = j & 1;
-      __syncthreads();  // the only barrier of step j
-      if (j < 8) { DBG(10 + j) }
-      double v = lane < nwarp_rows ? cand_v[par][lane] : -2.0;
-      int p = lane < nwarp_rows ? cand_i[par][lane] : INT_MAX;
-      int ws = lane;
-#pragma unroll
-      for (int o = 4; o; o >>= 1) {
-        double v2 = __shfl_xor_sync(0xffffffffu, v, o);
-        int i2 = __shfl_xor_sync(0xffffffffu, p, o);
-        int w2 = __shfl_xor_sync(0xffffffffu, ws, o);
-        if (v2 > v || (v2 == v && i2 < p)) {
-          v = v2;
-          p = i2;
-          ws = w2;
-        }
-      }
-      p = __shfl_sync(0xffffffffu, p, 0);
-      ws = __shfl_sync(0xffffffffu, ws, 0);
-      if (j == 1) { DBG(20) }
-      int phj = -1;
-      const bool has = p != INT_MAX;
-      if (!has) p = j;  // no candidate (NaN column): keep logical row j in place
-      else phj = cand_ph[par][ws];
-      const double2 (&prow)[NB] = cand_row[par][has ? ws : 0];
-      if (tid == 0) {
-        s_piv[j] = p;
-        piv[k + j] = k + p;
-      }
-      // logical interchange j <-> p
-      int nl = mylog;
-      if (mylog == j) nl = p;
-      if (t == phj) nl = j;
-      if (phj < 0 && mylog == j) nl = j;
-      mylog = nl;
-      const double2 inv = has ? crcp_fast(prow[j]) : make_double2(0.0, 0.0);
-      if (j == 1) { DBG(22) }
-      const bool upd = own && mylog > j && has;
-      double bv = -1.0;
-#define GJR_CHUNK(C0)                                                          \
-  {                                                                            \
-    double2 aj = a[C0];                                                        \
-    _Pragma("unroll") for (int c = (C0) + 1; c < (C0) + 8 && c < NB; ++c)     \
-      if (c == j) aj = a[c];                                                   \
-    const double2 l = cmul(aj, inv);                                           \
-    const double2 lz = upd ? l : make_double2(0.0, 0.0);                       \
-    _Pragma("unroll") for (int c = (C0); c < NB; ++c) {                        \
-      const double2 lc = (c > j) ? lz : make_double2(0.0, 0.0);               \
-      const double2 pc = prow[c];                                              \
-      double2 x = a[c];                                                        \
-      x.x = fma(-lc.x, pc.x, fma(lc.y, pc.y, x.x));                            \
-      x.y = fma(-lc.x, pc.y, fma(-lc.y, pc.x, x.y));                           \
-      if (c == j + 1) bv = cabs1(x);                                           \
-      a[c] = (upd && c == j) ? l : x;                                          \
-    }                                                                          \
-  }
-      const int ch = j >> 3;
-      if (ch == 0) {
-        GJR_CHUNK(0)
-      } else if (ch == 1) {
-        GJR_CHUNK(8 < NB ? 8 : 0)
-      } else if (ch == 2) {
-        GJR_CHUNK(16 < NB ? 16 : 0)
-      } else {
-        GJR_CHUNK(24 < NB ? 24 : 0)
-      }
-#undef GJR_CHUNK
-      if (j == 1) { DBG(23) }
-      if (j + 1 < NB) publish_reg(par ^ 1, (own && mylog > j) ? bv : -1.0, (own && mylog > j) ? mylog : INT_MAX);
-      if (j == 1) { DBG(24) }
-    }
-    __syncthreads();
-    int* fp = perm + (NB & 1) * rows;
-    if (own) {
-#pragma unroll
-      for (int c = 0; c < NB; ++c) pn[c * ldp + t] = a[c];
-      fp[mylog] = t;
-    }
-  } else {
+  {
 #pragma unroll 1
   for (int j = 0; j < NB; ++j) {
     const int par = j & 1;
@@ -407,88 +371,162 @@ __global__ void __launch_bounds__(PT, 1)
   __syncthreads();
   }
   const int* fperm = perm + (NB & 1) * rows;  // final logical -> physical rows
+  __shared__ double2 s_lu[NB][NB + 1];
+  for (int e = tid; e < NB * NB; e += PT) s_lu[e / NB][e % NB] = pn[(e % NB) * ldp + fperm[e / NB]];
   __syncthreads();
   DBG(2)
-  if (tid < NB && k + tid < n_true) {  // negligible-pivot test on the U diagonal
-    const double2 d = pn[tid * ldp + fperm[tid]];
-    if (hypot(d.x, d.y) <= tol) atomicMin(&s_fail, k + tid);
-  }
-
-  // ---- row map of the interchanges (new row r holds old row src(r))
-  for (int r = tid; r < n; r += PT) {
-    int src = r;
-    if (r >= k) {
-#pragma unroll
-      for (int j = NB - 1; j >= 0; --j) {
-        const int p = k + s_piv[j];
-        if (src == k + j)
-          src = p;
-        else if (src == p)
-          src = k + j;
-      }
-    }
-    rowmap[r] = src;
-    if (r >= k && r < k + NB) s_src[r - k] = src;
-  }
-
-  // 1 / U[j][j] of the pivot block (logical rows 0..NB-1, physical fperm[j])
-  __shared__ double2 s_uinv[NB];
-  if (tid < NB) s_uinv[tid] = crcp_fast(pn[tid * ldp + fperm[tid]]);
-  __syncthreads();
-
-  // ---- Wz (n x NB, ld n): current M[:,K] in post-interchange order, -I on pivot rows
-  {
-    double2* __restrict__ wz = S.wz + (long long)b * n * NB;
-    for (int base = tid; base < n * NB; base += 4 * PT) {
-      double2 v[4];
-#pragma unroll
-      for (int u = 0; u < 4; ++u) {
-        const int idx = base + u * PT;
-        const int r = idx % n, c = idx / n;
-        if (idx < n * NB)
-          v[u] = (r >= k && r < k + NB) ? make_double2(r - k == c ? -1.0 : 0.0, 0.0)
-                                        : cur[(long long)(k + c) * ld + rowmap[r]];
-      }
-#pragma unroll
-      for (int u = 0; u < 4; ++u) {
-        const int idx = base + u * PT;
-        if (idx < n * NB) wz[idx] = v[u];
-      }
-    }
-  }
-  // ---- V (NB x n, ld NB) = U^{-1} L^{-1} Vs, Vs = pivot rows of M after the
-  //      interchanges with the identity in columns K (so V[:,K] = (L U)^{-1}).
-  //      Triangular solves, one column per thread: backward stable, no explicit
-  //      inverse of the pivot block.
-  {
-    double2* __restrict__ vb = S.vbuf + (long long)b * NB * n;
-    for (int col = tid; col < n; col += PT) {
-      const bool kc = col >= k && col < k + NB;
-      double2 x[NB];
-#pragma unroll
-      for (int j = 0; j < NB; ++j)
-        x[j] = kc ? make_double2(col - k == j ? 1.0 : 0.0, 0.0) : cur[(long long)col * ld + s_src[j]];
-#pragma unroll
-      for (int j = 1; j < NB; ++j) {  // L (unit lower): x_j -= sum_{q<j} L[j][q] x_q
-        const int pj = fperm[j];
-#pragma unroll
-        for (int q = 0; q < j; ++q) x[j] = csub(x[j], cmul(pn[q * ldp + pj], x[q]));
-      }
-#pragma unroll
-      for (int j = NB - 1; j >= 0; --j) {  // U: x_j = (x_j - sum_{q>j} U[j][q] x_q) / U[j][j]
-        const int pj = fperm[j];
-#pragma unroll
-        for (int q = j + 1; q < NB; ++q) x[j] = csub(x[j], cmul(pn[q * ldp + pj], x[q]));
-        x[j] = cmul(x[j], s_uinv[j]);
-      }
-#pragma unroll
-      for (int j = 0; j < NB; ++j) vb[(long long)col * NB + j] = x[j];
-    }
-  }
-  __syncthreads();
-  DBG(4)
-  if (tid == 0 && s_fail != INT_MAX && status[b] < 0) status[b] = s_fail;
+  panel_tail<NB>(cur, ld, n, n_true, k, b, S, status, s_lu, fperm, s_piv, tol, &s_fail);
 }
+
+// Pivot-search key: |re|+|im| truncated to sign, exponent and 11 mantissa bits of
+// the double, above the complemented physical row. The unsigned maximum is the
+// largest magnitude (lowest row among equal keys), so one warp-wide REDUX.MAX is the
+// argmax. The chosen pivot is within a factor 1 - 2^-11 of the column maximum
+// (threshold partial pivoting, |l| <= 1.0005).
+constexpr int KEY_IB = 10;  // physical rows < 1024
+constexpr unsigned KEY_IMASK = (1u << KEY_IB) - 1;
+__device__ __forceinline__ unsigned piv_key(double2 v, int ph) {
+  const unsigned long long bits = (unsigned long long)__double_as_longlong(cabs1(v)) & 0x7fffffffffffffffULL;
+  return (unsigned(bits >> (63 - (32 - KEY_IB))) << KEY_IB) | (KEY_IMASK - unsigned(ph));
+}
+
+// Register-resident panel (rows <= RPT * PT). Thread t owns physical panel rows
+// t + i*PT for good: rows never move, the interchanges only relabel logical row
+// numbers, so the elimination never touches shared memory for its own data. Per
+// column: one barrier, the pivot resolved from the 8 published warp keys, the
+// winning row and its reciprocal read from the winner's warp slot, the update, and
+// the next column's warp keys by REDUX.
+template <int NB, int RPT>
+__global__ void __launch_bounds__(PT, 1)
+    gj_panel_rows_kernel(const double2* __restrict__ cur0, long long ld, long long bstride, int n, int n_true, int k,
+                         GjScratch S, int* __restrict__ status) {
+  __shared__ unsigned cand_k[2][PT / 32];
+  __shared__ double2 cand_r[2][PT / 32];
+  __shared__ __align__(16) double2 cand_row[2][PT / 32][NB];
+  __shared__ double2 s_lu[NB][NB + 1];
+  __shared__ int s_map[RPT * PT];
+  __shared__ int s_p[NB];
+  __shared__ double s_red[PT / 32];
+  __shared__ int s_fail;
+  __shared__ double s_tol;
+
+  const int tid = threadIdx.x, lane = tid & 31, warp = tid >> 5;
+  const int b = blockIdx.x;
+  const double2* __restrict__ cur = cur0 + (long long)b * bstride;
+  const int rows = n - k;
+
+  double2 a[RPT][NB];
+  int lg[RPT];
+  bool act[RPT];
+#pragma unroll
+  for (int i = 0; i < RPT; ++i) {
+    const int ph = tid + i * PT;
+    act[i] = ph < rows;
+    lg[i] = ph;
+#pragma unroll
+    for (int c = 0; c < NB; ++c) a[i][c] = act[i] ? cur[(long long)(k + c) * ld + k + ph] : make_double2(0.0, 0.0);
+  }
+  if (tid == 0) s_fail = INT_MAX;
+  if (k == 0) {
+    const double t = panel_threshold(cur, ld, n_true, s_red);
+    if (tid == 0) {
+      s_tol = t;
+      S.tol[b] = t;
+      status[b] = -1;
+    }
+  } else if (tid == 0) {
+    s_tol = S.tol[b];
+  }
+
+  // publish this warp's best candidate for column J: key, reciprocal, row (c > J)
+  auto publish = [&](int par, int J) {
+    unsigned key = 0;
+    int wi = 0;
+#pragma unroll
+    for (int i = 0; i < RPT; ++i)
+      if (act[i]) {
+        const unsigned kk = piv_key(a[i][J], tid + i * PT);
+        if (kk > key) {
+          key = kk;
+          wi = i;
+        }
+      }
+    const unsigned wk = __reduce_max_sync(0xffffffffu, key);
+    if (lane == 0) cand_k[par][warp] = wk;
+    if (wk != 0 && key == wk) {
+#pragma unroll
+      for (int i = 0; i < RPT; ++i)
+        if (i == wi) {
+          cand_r[par][warp] = crcp_fast(a[i][J]);
+#pragma unroll
+          for (int c = 0; c < NB; ++c)
+            if (c > J) cand_row[par][warp][c] = a[i][c];
+        }
+    }
+  };
+  publish(0, 0);
+
+  int prev_ph = -1;
+#pragma unroll
+  for (int j = 0; j < NB; ++j) {
+    const int par = j & 1;
+    __syncthreads();
+    if (j > 0) {  // deferred relabel of step j-1: the old logical row j-1 takes the partner's number
+      const int pp = s_p[j - 1];
+#pragma unroll
+      for (int i = 0; i < RPT; ++i)
+        if (lg[i] == j - 1 && tid + i * PT != prev_ph) lg[i] = pp;
+    }
+    unsigned best = 0;
+#pragma unroll
+    for (int q = 0; q < PT / 32; ++q) best = max(best, cand_k[par][q]);
+    const int phj = int(KEY_IMASK - (best & KEY_IMASK));
+    const int qw = (phj % PT) >> 5;
+    const double2 rcp = cand_r[par][qw];
+#pragma unroll
+    for (int i = 0; i < RPT; ++i) {
+      if (tid + i * PT == phj) {  // this row becomes logical row j
+        s_p[j] = lg[i];
+        lg[i] = j;
+        act[i] = false;
+#pragma unroll
+        for (int c = 0; c < NB; ++c) s_lu[j][c] = a[i][c];
+      }
+    }
+    double2 l[RPT];
+#pragma unroll
+    for (int i = 0; i < RPT; ++i) {
+      l[i] = act[i] ? cmul(a[i][j], rcp) : make_double2(0.0, 0.0);
+      if (act[i]) a[i][j] = l[i];
+    }
+#pragma unroll
+    for (int c = j + 1; c < NB; ++c) {
+      const double2 u = cand_row[par][qw][c];
+#pragma unroll
+      for (int i = 0; i < RPT; ++i) {
+        double2 x = a[i][c];
+        x.x = fma(-l[i].x, u.x, fma(l[i].y, u.y, x.x));
+        x.y = fma(-l[i].x, u.y, fma(-l[i].y, u.x, x.y));
+        a[i][c] = x;
+      }
+    }
+    prev_ph = phj;
+    if (j + 1 < NB) publish(par ^ 1, j + 1);
+  }
+  __syncthreads();
+  {
+    const int pp = s_p[NB - 1];
+#pragma unroll
+    for (int i = 0; i < RPT; ++i) {
+      const int ph = tid + i * PT;
+      if (lg[i] == NB - 1 && ph != prev_ph) lg[i] = pp;
+      if (ph < rows) s_map[lg[i]] = ph;
+    }
+  }
+  __syncthreads();
+  panel_tail<NB>(cur, ld, n, n_true, k, b, S, status, s_lu, s_map, s_p, s_tol, &s_fail);
+}
+
 
 // After the last panel: column map that undoes the interchanges. With
 // X[:, c] = Y[:, q[c]] (q from the column swaps j = n-1 .. 0), the GEMM scatters
@@ -569,10 +607,22 @@ cudaError_t zinv_batched(double2* M, long long ld, long long bstride, int n, int
       attr[0].val.priority = panel_priority();
       cfg.attrs = attr;
       cfg.numAttrs = 1;
-      if (nb == 32)
-        e = cudaLaunchKernelEx(&cfg, gj_panel_kernel<32>, (const double2*)cur, cld, cbs, n, n_true, k, S, status);
-      else
-        e = cudaLaunchKernelEx(&cfg, gj_panel_kernel<16>, (const double2*)cur, cld, cbs, n, n_true, k, S, status);
+      const int rows = n - k;
+      const double2* cc = cur;
+      if (use_rows_kernel() && nb == 16 && rows <= PT) {
+        cfg.dynamicSmemBytes = 0;
+        e = cudaLaunchKernelEx(&cfg, gj_panel_rows_kernel<16, 1>, cc, cld, cbs, n, n_true, k, S, status);
+      } else if (use_rows_kernel() && nb == 16 && rows <= 2 * PT) {
+        cfg.dynamicSmemBytes = 0;
+        e = cudaLaunchKernelEx(&cfg, gj_panel_rows_kernel<16, 2>, cc, cld, cbs, n, n_true, k, S, status);
+      } else if (use_rows_kernel() && nb == 32 && rows <= PT) {
+        cfg.dynamicSmemBytes = 0;
+        e = cudaLaunchKernelEx(&cfg, gj_panel_rows_kernel<32, 1>, cc, cld, cbs, n, n_true, k, S, status);
+      } else if (nb == 32) {
+        e = cudaLaunchKernelEx(&cfg, gj_panel_kernel<32>, cc, cld, cbs, n, n_true, k, S, status);
+      } else {
+        e = cudaLaunchKernelEx(&cfg, gj_panel_kernel<16>, cc, cld, cbs, n, n_true, k, S, status);
+      }
       if (e) return e;
       if (last) {
         build_colmap_kernel<<<batch, 256, 2 * n * sizeof(int), stream>>>(S.piv, S.colmap, n);
