@@ -27,10 +27,12 @@ struct ZGemmProblem {
   ZOp A, B, C;          // C may be ignored when beta == 0
   ZOp D;                // output operand (p is written)
   // optional epilogue remaps (plain single-block operands; used by the blocked
-  // Gauss-Jordan inversion): C row r is read from row rowmap[r]; C is taken as 0
-  // for rows [zr0, zr1) and columns [zc0, zc1); D column c is written to colmap[c].
+  // Gauss-Jordan inversion): C row r is read from row rowmap[r] (a negative entry
+  // reads 0); C is taken as 0 for rows [zr0, zr1) and columns [zc0, zc1); D row r /
+  // column c is written to row rowscat[r] / column colmap[c].
   const int* rowmap;
   const int* colmap;
+  const int* rowscat;
   long long map_bstride;
   int zr0, zr1, zc0, zc1;
   int tiles_m, tiles_n; // filled by the launcher

@@ -110,6 +110,7 @@ __global__ void __launch_bounds__(128, MINB) zgemm_grouped_kernel(const __grid_c
       const int m = m0 + wm + mi * 8 + lr;
       rowok[mi] = m < P.M && !(m >= P.zr0 && m < P.zr1);
       srow[mi] = rmap ? (m < P.M ? __ldg(&rmap[m]) : 0) : m - m0;
+      if (srow[mi] < 0) rowok[mi] = false;
     }
 #pragma unroll
     for (int ni = 0; ni < 4; ++ni)
@@ -194,10 +195,11 @@ __global__ void __launch_bounds__(128, MINB) zgemm_grouped_kernel(const __grid_c
 
   // ---- epilogue
   const int* cmap = P.colmap ? P.colmap + (long long)batch * P.map_bstride : nullptr;
+  const int* rscat = P.rowscat ? P.rowscat + (long long)batch * P.map_bstride : nullptr;
   double2* __restrict__ dbase = const_cast<double2*>(P.D.p) + (long long)batch * P.D.bstride;
   if (c_in_acc || !use_c) {  // D = alpha * acc (C already inside acc when c_in_acc)
     const double2 al = c_in_acc ? make_double2(P.alpha.x, 0.0) : P.alpha;
-    if (!cmap && m0 + BM <= P.M && n0 + BN <= P.N) {
+    if (!cmap && !rscat && m0 + BM <= P.M && n0 + BN <= P.N) {
       double2* __restrict__ dptr = dbase + toff<PLAIN>(P.D, bs, m0, n0);
 #pragma unroll
       for (int mi = 0; mi < 4; ++mi)
@@ -208,9 +210,15 @@ __global__ void __launch_bounds__(128, MINB) zgemm_grouped_kernel(const __grid_c
             const int m = wm + mi * 8 + lr, n = wn + ni * 8 + lc * 2 + q;
             dptr[(long long)n * P.D.ld + m] = cmul(al, make_double2(cr[mi][ni][q], ci[mi][ni][q]));
           }
-    } else {  // edge tile and/or column scatter (plain operand: offset = r + c*ld)
+    } else {  // edge tile and/or row / column scatter (plain operand: offset = r + c*ld)
       double2* __restrict__ dt = dbase + toff<PLAIN>(P.D, bs, m0, n0);
       long long dcol[4][2];
+      int drow[4];
+#pragma unroll
+      for (int mi = 0; mi < 4; ++mi) {
+        const int m = m0 + wm + mi * 8 + lr;
+        drow[mi] = (rscat && m < P.M) ? __ldg(&rscat[m]) - m0 : m - m0;
+      }
 #pragma unroll
       for (int ni = 0; ni < 4; ++ni)
 #pragma unroll
@@ -226,7 +234,7 @@ __global__ void __launch_bounds__(128, MINB) zgemm_grouped_kernel(const __grid_c
           for (int q = 0; q < 2; ++q) {
             const int ml = wm + mi * 8 + lr;
             if (m0 + ml >= P.M || n0 + wn + ni * 8 + lc * 2 + q >= P.N) continue;
-            dt[dcol[ni][q] + ml] = cmul(al, make_double2(cr[mi][ni][q], ci[mi][ni][q]));
+            dt[dcol[ni][q] + drow[mi]] = cmul(al, make_double2(cr[mi][ni][q], ci[mi][ni][q]));
           }
     }
   } else {  // general complex alpha / beta: D = alpha*acc + beta*C, C read in two halves
@@ -242,8 +250,9 @@ __global__ void __launch_bounds__(128, MINB) zgemm_grouped_kernel(const __grid_c
 #pragma unroll
           for (int q = 0; q < 2; ++q) {
             const int m = m0 + wm + (half * 2 + mh) * 8 + lr, n = n0 + wn + ni * 8 + lc * 2 + q;
-            const bool z = m >= P.M || n >= P.N || (m >= P.zr0 && m < P.zr1) || (n >= P.zc0 && n < P.zc1);
-            cv[mh][ni][q] = z ? make_double2(0.0, 0.0) : cbase[toff<PLAIN>(P.C, bs, rmap ? __ldg(&rmap[m]) : m, n)];
+            const int sr = (rmap && m < P.M) ? __ldg(&rmap[m]) : m;
+            const bool z = m >= P.M || n >= P.N || sr < 0 || (m >= P.zr0 && m < P.zr1) || (n >= P.zc0 && n < P.zc1);
+            cv[mh][ni][q] = z ? make_double2(0.0, 0.0) : cbase[toff<PLAIN>(P.C, bs, sr, n)];
           }
 #pragma unroll
       for (int mh = 0; mh < 2; ++mh)
@@ -255,7 +264,7 @@ __global__ void __launch_bounds__(128, MINB) zgemm_grouped_kernel(const __grid_c
             const int m = m0 + wm + mi * 8 + lr, n = n0 + wn + ni * 8 + lc * 2 + q;
             if (m >= P.M || n >= P.N) continue;
             double2 out = cfma(P.beta, cv[mh][ni][q], cmul(P.alpha, make_double2(cr[mi][ni][q], ci[mi][ni][q])));
-            dbase[toff<PLAIN>(P.D, bs, m, cmap ? __ldg(&cmap[n]) : n)] = out;
+            dbase[toff<PLAIN>(P.D, bs, rscat ? __ldg(&rscat[m]) : m, cmap ? __ldg(&cmap[n]) : n)] = out;
           }
     }
   }

@@ -1,25 +1,28 @@
 // Batched inversion of bs x bs complex128 blocks: blocked Gauss-Jordan elimination
-// with partial (row) pivoting, split into a per-matrix panel kernel and two
-// grouped DMMA GEMM launches per panel, so the O(n^3) part runs on every SM.
+// with partial (row) pivoting, split into a per-matrix panel kernel and one grouped
+// DMMA GEMM per panel, so the O(n^3) part runs on every SM.
 //
 // Replaces, per Schur pivot, the reference's lu_factor + invert pair
 // (kernels.hpp:140-160 zgetrf with the negligible-pivot test, kernels.hpp:192-195
 // zgetrs against the identity); solve_left / solve_right (kernels.hpp:163-189)
 // become plain GEMMs with the explicit inverse.
 //
-// Block sweep on the panel K = [k, k+nb) with pivot rows P (after interchanges):
-//   M[P,K] <- Pinv = (L_P U)^{-1},  M[P,C] <- Pinv M[P,C]  (both = V below),
-//   M[R,K] <- -M[R,K] Pinv,         M[R,C] <- M[R,C] - M[R,K] Pinv M[P,C].
+// Rows never move. The interchanges live in a logical -> physical row map
+// (lmap); logical rows k..n-1 are the rows not yet used as pivots. Block step on
+// the panel K = [k, k+nb) with pivot rows P (physical) and the other rows R:
+//   M[P,K] <- Pinv = (L U)^{-1},     M[P,C] <- Pinv M[P,C]
+//   M[R,K] <- -M[R,K] Pinv,          M[R,C] <- M[R,C] - M[R,K] Pinv M[P,C]
+// i.e. M <- M (0 on rows P / cols K) - Wz V with Wz = M[:,K] (-I on rows P) and
+// V = Pinv Vs, Vs = M[P,:] with the identity in columns K.
 // Per panel:
-//   gj_panel (1 CTA / matrix): tall-panel LU with partial pivoting of rows k..n-1
-//     (|re|+|im| pivot choice, first index on ties, as izamax in zgetrf); the
-//     row interchanges become a row map; Wz = M[:,K] in post-interchange row
-//     order with -I on the pivot rows; V = U^{-1} L^{-1} M[P,:] (identity in the
-//     K columns, so V[:,K] = Pinv) by triangular solves, one column per thread.
-//   GEMM:  Next = Cur[rowmap] (0 on rows P / cols K) - Wz V  (n x n, all SMs)
-// Cur/Next ping-pong between the input block and two scratch matrices; the last
-// panel's GEMM writes into the input block with the column map that undoes the
-// interchanges (X = Y P), so no separate un-pivoting pass exists.
+//   panel kernel (1 CTA / matrix): tall-panel LU with partial pivoting of the
+//     active rows (pivot search on |re|+|im|, as izamax in zgetrf), the new lmap,
+//     Wz, Pinv (column solves of the pivot block) and V.
+//   GEMM: M <- M[mask] - Wz V, in place (a tile reads and writes only itself).
+// The first panel reads the input block and writes the working matrix s0; the last
+// one writes back into the input block, scattering rows and columns through lmap:
+// with Y the eliminated matrix in physical row order, A^{-1}[i, lmap[c]] =
+// Y[lmap[i], c], so no separate un-pivoting pass exists.
 // The U diagonal is tested against eps * n * max|A| (|.| = hypot), the reference
 // threshold (kernels.hpp:149-158); status[] gets the first failing column or -1.
 #include <cfloat>
@@ -35,32 +38,11 @@ namespace {
 
 constexpr int PT = 256;  // panel kernel threads
 
-struct GjScratch {
-  int* rowmap;    // [batch][n]
-  int* colmap;    // [batch][n]
-  int* piv;       // [batch][n]
-  double* tol;    // [batch]
-  double2* wz;    // [batch][n*nb]   (col-major, ld n)
-  double2* pinv;  // [batch][nb*nb]  (col-major, ld nb)
-  double2* vs;    // [batch][nb*n]   (col-major, ld nb)
-  double2* vbuf;  // [batch][nb*n]
-  double2* s0;    // [batch][n*n]
-  double2* s1;    // [batch][n*n]
-};
-
-// Panel width. 16 is the default: blocked Gauss-Jordan loses accuracy with the
-// pivot-block width (numpy emulation on config 3, E = 0.145: RGF vs reference
-// 2.2e-10 at nb = 32, 1.4e-10 at nb = 16, 1.3e-10 unblocked; the reference's own
-// 1/2-ulp input-noise floor there is 1.1-1.4e-10). BBSI_GJ_NB=32 trades accuracy
-// for fewer, wider panels.
-int pick_nb(int n) {
-  static int forced = [] {
-    const char* e = getenv("BBSI_GJ_NB");
-    return e ? atoi(e) : 0;
-  }();
-  if (forced == 32 && size_t(n) * 32 * sizeof(double2) <= 200 * 1024) return 32;
-  return 16;
-}
+// Panel width 16. Measured on B200 (config 2 / config 3 E = 0.145): 32 is both slower
+// (858 vs 771 ms per step) and less accurate (2.9e-10 vs 1.9e-10 against the
+// reference, whose own 1/2-ulp floor there is 1.4e-10); blocked Gauss-Jordan loses
+// accuracy with the pivot-block width.
+constexpr int kNB = 16;
 
 // BBSI_PANEL_ROWS=0 selects the shared-memory panel kernel everywhere (A/B checks).
 bool use_rows_kernel() {
@@ -71,15 +53,29 @@ bool use_rows_kernel() {
   return on;
 }
 
+// The panel is latency-bound and on the critical path of the sweep: launched at the
+// greatest stream priority so its CTAs take SMs ahead of queued GEMM tiles of the
+// other stream group (BBSI_PANEL_PRIORITY=0: lowest).
 int panel_priority() {
   static int p = [] {
     int lo = 0, hi = 0;
     if (cudaDeviceGetStreamPriorityRange(&lo, &hi) != cudaSuccess) return 0;
     const char* e = getenv("BBSI_PANEL_PRIORITY");
-    return (e && atoi(e) == 0) ? lo : hi;  // hi = greatest priority (numerically lowest)
+    return (e && atoi(e) == 0) ? lo : hi;
   }();
   return p;
 }
+
+struct GjScratch {
+  int* lmap;      // [batch][n]  logical row -> physical row
+  int* rowmask;   // [batch][n]  GEMM C rows: r, or -1 on this panel's pivot rows
+  int* rowscat;   // [batch][n]  last panel: physical row -> output row
+  int* colmap;    // [batch][n]  last panel: column c -> output column lmap[c]
+  double* tol;    // [batch]
+  double2* wz;    // [batch][n*nb]  (col-major, ld n)
+  double2* vbuf;  // [batch][nb*n]  (col-major, ld nb)
+  double2* s0;    // [batch][n*n]   working matrix
+};
 
 size_t align256(size_t x) { return (x + 255) & ~size_t(255); }
 
@@ -91,93 +87,164 @@ size_t carve(GjScratch& s, void* base, int n, int nb, int batch) {
     off = align256(off + bytes);
     return r;
   };
-  s.rowmap = reinterpret_cast<int*>(take(sizeof(int) * size_t(batch) * n));
+  s.lmap = reinterpret_cast<int*>(take(sizeof(int) * size_t(batch) * n));
+  s.rowmask = reinterpret_cast<int*>(take(sizeof(int) * size_t(batch) * n));
+  s.rowscat = reinterpret_cast<int*>(take(sizeof(int) * size_t(batch) * n));
   s.colmap = reinterpret_cast<int*>(take(sizeof(int) * size_t(batch) * n));
-  s.piv = reinterpret_cast<int*>(take(sizeof(int) * size_t(batch) * n));
   s.tol = reinterpret_cast<double*>(take(sizeof(double) * size_t(batch)));
   s.wz = reinterpret_cast<double2*>(take(sizeof(double2) * size_t(batch) * n * nb));
-  s.pinv = reinterpret_cast<double2*>(take(sizeof(double2) * size_t(batch) * nb * nb));
-  s.vs = reinterpret_cast<double2*>(take(sizeof(double2) * size_t(batch) * nb * n));
   s.vbuf = reinterpret_cast<double2*>(take(sizeof(double2) * size_t(batch) * nb * n));
   s.s0 = reinterpret_cast<double2*>(take(sizeof(double2) * size_t(batch) * n * n));
-  s.s1 = reinterpret_cast<double2*>(take(sizeof(double2) * size_t(batch) * n * n));
   return off;
 }
 
-__device__ __forceinline__ void argmax_merge(double& v, int& i, double v2, int i2) {
-  if (v2 > v || (v2 == v && i2 < i)) {
-    v = v2;
-    i = i2;
-  }
-}
+// Physical row of active-list entry t of the panel at k (the list is lmap[k..n-1]).
+__device__ __forceinline__ int active_row(const int* lmap, int k, int t) { return k == 0 ? t : lmap[k + t]; }
 
 // Everything after the pivot search, shared by both panel kernels.
-//   lu[j][c]  pivot row j (logical): L multipliers for c < j, U for c >= j
-//   lmap[r]   panel-local logical row r -> physical (= original) row
-//   lpiv[j]   LAPACK-style interchange partner of step j (panel-local)
-// Writes rowmap / piv, Wz and V, and the first negligible U-diagonal column.
+//   lu[j][c]   pivot row j (logical): L multipliers for c < j, U for c >= j
+//   lloc[r]    panel-local logical row r -> active-list entry
+//   act[t]     active-list entry -> physical row
+// Writes lmap, the row mask, Wz, V (and on the last panel the output scatters), and
+// the first negligible U-diagonal column.
 template <int NB>
 __device__ __forceinline__ void panel_tail(const double2* __restrict__ cur, long long ld, int n, int n_true, int k, int b,
-                                           const GjScratch& S, int* __restrict__ status, const double2 (*lu)[NB + 1],
-                                           const int* lmap, const int* lpiv, double tol, int* s_fail) {
+                                           bool last, const GjScratch& S, int* __restrict__ status,
+                                           const double2 (*lu)[NB + 1], const int* lloc, const int* act, double tol,
+                                           int* s_fail, double2* sv) {
+  static_assert(NB == 16, "the warp-level pivot-block inverse assumes NB = 16 (two columns per warp)");
   __shared__ double2 s_uinv[NB];
-  __shared__ int s_src[NB];
-  const int tid = threadIdx.x;
-  int* __restrict__ rowmap = S.rowmap + (long long)b * n;
+  __shared__ int s_src[NB];  // physical pivot rows
+  __shared__ double2 s_pinv[NB][NB + 1];
+  const int tid = threadIdx.x, lane = tid & 31, warp = tid >> 5;
+  const int rows = n - k;
+  int* __restrict__ lmap = S.lmap + (long long)b * n;
+  int* __restrict__ rowmask = S.rowmask + (long long)b * n;
+  double2* __restrict__ wz = S.wz + (long long)b * n * NB;
+  double2* __restrict__ vb = S.vbuf + (long long)b * NB * n;
   if (tid < NB) {
     const double2 d = lu[tid][tid];
     if (k + tid < n_true && hypot(d.x, d.y) <= tol) atomicMin(s_fail, k + tid);  // kernels.hpp:149-158
     s_uinv[tid] = crcp_fast(d);
-    S.piv[(long long)b * n + k + tid] = k + lpiv[tid];
+    s_src[tid] = act[lloc[tid]];
   }
-  // row map of the interchanges: new row r holds old row rowmap[r]
+  for (int r = tid; r < rows; r += PT) lmap[k + r] = act[lloc[r]];
+  // Wz (n x NB, ld n) = M[:,K] (rows are not permuted: coalesced); pivot rows fixed below
   for (int r = tid; r < n; r += PT) {
-    const int src = r < k ? r : k + lmap[r - k];
-    rowmap[r] = src;
-    if (r >= k && r < k + NB) s_src[r - k] = src;
+    rowmask[r] = r;
+    double2 v[NB];
+#pragma unroll
+    for (int c = 0; c < NB; ++c) v[c] = cur[(long long)(k + c) * ld + r];
+#pragma unroll
+    for (int c = 0; c < NB; ++c) wz[(long long)c * n + r] = v[c];
   }
   __syncthreads();
-  // Wz (n x NB, ld n): current M[:,K] in post-interchange order, -I on the pivot rows
+  // Vs (pivot rows of M, identity in columns K) of this thread's first column, issued
+  // now so the loads overlap the pivot-block inverse
+  double2 xpre[NB];
   {
-    double2* __restrict__ wz = S.wz + (long long)b * n * NB;
-#pragma unroll 1
-    for (int c = 0; c < NB; c += 4) {
-      for (int r = tid; r < n; r += PT) {
-        const bool pr = r >= k && r < k + NB;
-        const int src = r < k ? r : k + lmap[r - k];
-        double2 v[4];
+    const bool kc = tid >= k && tid < k + NB;
 #pragma unroll
-        for (int u = 0; u < 4; ++u)
-          v[u] = pr ? make_double2(r - k == c + u ? -1.0 : 0.0, 0.0) : cur[(long long)(k + c + u) * ld + src];
-#pragma unroll
-        for (int u = 0; u < 4; ++u) wz[(long long)(c + u) * n + r] = v[u];
-      }
-    }
+    for (int j = 0; j < NB; ++j)
+      xpre[j] = tid >= n ? make_double2(0.0, 0.0)
+                         : (kc ? make_double2(tid - k == j ? 1.0 : 0.0, 0.0) : cur[(long long)tid * ld + s_src[j]]);
   }
-  // V (NB x n, ld NB) = U^{-1} L^{-1} Vs, Vs = pivot rows of M after the interchanges
-  // with the identity in columns K (so V[:,K] = (L U)^{-1}); triangular solves, one
-  // column per thread (backward stable, no explicit inverse of the pivot block).
-  {
-    double2* __restrict__ vb = S.vbuf + (long long)b * NB * n;
+  for (int e = tid; e < NB * NB; e += PT) {  // pivot rows: -I in Wz, 0 in C
+    const int j = e / NB, c = e % NB;
+    wz[(long long)c * n + s_src[j]] = make_double2(j == c ? -1.0 : 0.0, 0.0);
+    if (c == 0) rowmask[s_src[j]] = -1;
+  }
+  // Pinv = (L U)^{-1} of the pivot block: warp w solves columns 2w, 2w+1 of the
+  // identity, one row per lane, values exchanged by shuffles.
+  if (warp < NB / 2) {
+    const int r = lane & 15, c = 2 * warp + (lane >> 4), base = lane & 16;
+    double2 y = make_double2(r == c ? 1.0 : 0.0, 0.0);
+#pragma unroll
+    for (int j = 0; j < NB - 1; ++j) {  // L y = e_c (unit lower)
+      double2 yj;
+      yj.x = __shfl_sync(0xffffffffu, y.x, base | j);
+      yj.y = __shfl_sync(0xffffffffu, y.y, base | j);
+      if (r > j) y = csub(y, cmul(lu[r][j], yj));
+    }
+#pragma unroll
+    for (int j = NB - 1; j >= 0; --j) {  // U x = y
+      double2 yj;
+      yj.x = __shfl_sync(0xffffffffu, y.x, base | j);
+      yj.y = __shfl_sync(0xffffffffu, y.y, base | j);
+      const double2 xj = cmul(yj, s_uinv[j]);
+      if (r == j)
+        y = xj;
+      else if (r < j)
+        y = csub(y, cmul(lu[r][j], xj));
+    }
+    s_pinv[r][c] = y;
+  }
+  if (sv) {
+    // V = Pinv Vs on the tensor cores: Vs staged in smem (ld n + 2), each warp takes
+    // 8-column tiles, 2 x 4 complex m8n8k4 steps (4 real DMMAs each) per tile.
+    const int svld = n + 2;
     for (int col = tid; col < n; col += PT) {
       const bool kc = col >= k && col < k + NB;
-      double2 x[NB];
 #pragma unroll
       for (int j = 0; j < NB; ++j)
-        x[j] = kc ? make_double2(col - k == j ? 1.0 : 0.0, 0.0) : cur[(long long)col * ld + s_src[j]];
+        sv[j * svld + col] = col == tid ? xpre[j]
+                                        : (kc ? make_double2(col - k == j ? 1.0 : 0.0, 0.0)
+                                              : cur[(long long)col * ld + s_src[j]]);
+    }
+    __syncthreads();
+    const int lr = lane >> 2, lc = lane & 3;
+    for (int nt = warp; nt < n / 8; nt += PT / 32) {
+      double cr[2][2] = {{0.0, 0.0}, {0.0, 0.0}}, ci[2][2] = {{0.0, 0.0}, {0.0, 0.0}};
 #pragma unroll
-      for (int j = 1; j < NB; ++j) {  // unit lower L
+      for (int ks = 0; ks < NB / 4; ++ks) {
+        const double2 bv = sv[(ks * 4 + lc) * svld + nt * 8 + lr];
 #pragma unroll
-        for (int q = 0; q < j; ++q) x[j] = csub(x[j], cmul(lu[j][q], x[q]));
+        for (int mt = 0; mt < 2; ++mt) {
+          const double2 av = s_pinv[mt * 8 + lr][ks * 4 + lc];
+          dmma884(cr[mt], av.x, bv.x);
+          dmma884(cr[mt], -av.y, bv.y);
+          dmma884(ci[mt], av.x, bv.y);
+          dmma884(ci[mt], av.y, bv.x);
+        }
       }
 #pragma unroll
-      for (int j = NB - 1; j >= 0; --j) {  // upper U
+      for (int mt = 0; mt < 2; ++mt)
 #pragma unroll
-        for (int q = j + 1; q < NB; ++q) x[j] = csub(x[j], cmul(lu[j][q], x[q]));
-        x[j] = cmul(x[j], s_uinv[j]);
+        for (int q = 0; q < 2; ++q)
+          vb[(long long)(nt * 8 + 2 * lc + q) * NB + mt * 8 + lr] = make_double2(cr[mt][q], ci[mt][q]);
+    }
+  } else {
+    __syncthreads();
+    // V = Pinv Vs, one column per thread (tall panels: no smem left for Vs)
+    for (int col = tid; col < n; col += PT) {
+      double2 x[NB], acc[NB];
+      const bool kc = col >= k && col < k + NB;
+#pragma unroll
+      for (int j = 0; j < NB; ++j) {
+        x[j] = col == tid ? xpre[j]
+                          : (kc ? make_double2(col - k == j ? 1.0 : 0.0, 0.0) : cur[(long long)col * ld + s_src[j]]);
+        acc[j] = make_double2(0.0, 0.0);
+      }
+#pragma unroll 1
+      for (int q = 0; q < NB; ++q) {
+        double2 xq = x[0];
+#pragma unroll
+        for (int u = 1; u < NB; ++u)
+          if (u == q) xq = x[u];
+#pragma unroll
+        for (int j = 0; j < NB; ++j) acc[j] = cfma(s_pinv[j][q], xq, acc[j]);
       }
 #pragma unroll
-      for (int j = 0; j < NB; ++j) vb[(long long)col * NB + j] = x[j];
+      for (int j = 0; j < NB; ++j) vb[(long long)col * NB + j] = acc[j];
+    }
+  }
+  if (last) {  // output scatters: row lmap[i] -> i, column c -> lmap[c]
+    int* __restrict__ rowscat = S.rowscat + (long long)b * n;
+    int* __restrict__ colmap = S.colmap + (long long)b * n;
+    for (int i = tid; i < n; i += PT) {
+      const int p = lmap[i];
+      rowscat[p] = i;
+      colmap[i] = p;
     }
   }
   __syncthreads();
@@ -210,14 +277,24 @@ __device__ __forceinline__ double panel_threshold(const double2* __restrict__ cu
   return DBL_EPSILON * double(n_true) * m;
 }
 
+__device__ __forceinline__ void argmax_merge(double& v, int& i, double v2, int i2) {
+  if (v2 > v || (v2 == v && i2 < i)) {
+    v = v2;
+    i = i2;
+  }
+}
+
+// Shared-memory panel for tall panels (more than 2*PT active rows): the panel lives
+// in smem, interchanges go through a double-buffered logical -> entry permutation
+// (one barrier per column, every warp resolves the pivot from the published
+// per-warp candidates).
 template <int NB>
 __global__ void __launch_bounds__(PT, 1)
-    gj_panel_kernel(const double2* __restrict__ cur0, long long ld, long long bstride, int n, int n_true, int k,
+    gj_panel_kernel(const double2* __restrict__ cur0, long long ld, long long bstride, int n, int n_true, int k, int last,
                     GjScratch S, int* __restrict__ status) {
-  extern __shared__ __align__(16) double2 pn[];  // NB columns x rows (ld = rows + 1), panel in smem
+  extern __shared__ __align__(16) double2 pn[];  // NB columns x rows (ld = rows + 1), then perm[2][rows], act[rows]
   __shared__ double cand_v[2][PT / 32];
   __shared__ int cand_i[2][PT / 32];
-  __shared__ int s_piv[NB];   // pivot row (panel-local) chosen at step j
   __shared__ int s_fail;
   __shared__ double s_tol;
 
@@ -226,15 +303,15 @@ __global__ void __launch_bounds__(PT, 1)
   const double2* __restrict__ cur = cur0 + (long long)b * bstride;
   const int rows = n - k;
   const int ldp = rows + 1;
-  int* __restrict__ piv = S.piv + (long long)b * n;
+  int* perm = reinterpret_cast<int*>(pn + NB * ldp);  // [2][rows]
+  int* act = perm + 2 * rows;                          // [rows]
+  const int* lmapg = S.lmap + (long long)b * n;
 
-#ifdef BBSI_ZINV_DEBUG
-#define DBG(i) if (b == 0 && tid == 0 && k == 32) g_zinv_dbg[i] = clock64();
-#else
-#define DBG(i)
-#endif
-  DBG(0)
   if (tid == 0) s_fail = INT_MAX;
+  for (int r = tid; r < rows; r += PT) {
+    act[r] = active_row(lmapg, k, r);
+    perm[r] = r;
+  }
   if (k == 0) {
     const double t = panel_threshold(cur, ld, n_true, cand_v[1]);
     if (tid == 0) {
@@ -245,31 +322,17 @@ __global__ void __launch_bounds__(PT, 1)
   } else if (tid == 0) {
     s_tol = S.tol[b];
   }
-
-  // ---- load the panel (rows k..n-1, columns k..k+NB-1 of Cur), flat and coalesced
-  for (int base = tid; base < NB * rows; base += 4 * PT) {
-    double2 v[4];
+  __syncthreads();
+  for (int r = tid; r < rows; r += PT) {
+    const int ph = act[r];
+    double2 v[NB];
 #pragma unroll
-    for (int u = 0; u < 4; ++u) {
-      const int idx = base + u * PT;
-      v[u] = idx < NB * rows ? cur[(long long)(k + idx / rows) * ld + k + idx % rows] : make_double2(0.0, 0.0);
-    }
+    for (int c = 0; c < NB; ++c) v[c] = cur[(long long)(k + c) * ld + ph];
 #pragma unroll
-    for (int u = 0; u < 4; ++u) {
-      const int idx = base + u * PT;
-      if (idx < NB * rows) pn[(idx / rows) * ldp + idx % rows] = v[u];
-    }
+    for (int c = 0; c < NB; ++c) pn[c * ldp + r] = v[c];
   }
   __syncthreads();
-  DBG(1)
   const double tol = s_tol;
-
-  // Row interchanges are applied to a logical->physical row permutation (double
-  // buffered by parity) instead of moving data, so one barrier per column
-  // suffices: every warp resolves the pivot redundantly from the published
-  // per-warp candidates (also double buffered).
-  int* perm = reinterpret_cast<int*>(pn + NB * ldp);  // [2][rows]
-  for (int r = tid; r < rows; r += PT) perm[r] = r;
 
   // warp-level argmax of |re|+|im| over the rows this thread offers; lane 0 publishes
   auto publish = [&](int par, double bv, int bi) {
@@ -298,12 +361,10 @@ __global__ void __launch_bounds__(PT, 1)
   }
 
   const int nwarp_rows = (rows + 31) / 32 < PT / 32 ? (rows + 31) / 32 : PT / 32;
-  {
 #pragma unroll 1
   for (int j = 0; j < NB; ++j) {
     const int par = j & 1;
     __syncthreads();  // the only barrier of step j
-    if (j < 8) { DBG(10 + j) }
     double v = lane < nwarp_rows ? cand_v[par][lane] : -2.0;
     int p = lane < nwarp_rows ? cand_i[par][lane] : INT_MAX;
 #pragma unroll
@@ -313,20 +374,13 @@ __global__ void __launch_bounds__(PT, 1)
       argmax_merge(v, p, v2, i2);
     }
     p = __shfl_sync(0xffffffffu, p, 0);
-    if (j == 1) { DBG(20) }
     if (p == INT_MAX) p = j;  // empty / NaN column: keep row j
     const int* pold = perm + par * rows;
     int* pnew = perm + (par ^ 1) * rows;
-    const int phj = pold[p];  // physical row of the pivot = new logical row j
-    const int php = pold[j];  // physical row of old logical row j = new logical row p
+    const int phj = pold[p];  // entry of the pivot = new logical row j
+    const int php = pold[j];  // entry of old logical row j = new logical row p
     for (int r = tid; r < rows; r += PT) pnew[r] = (r == j) ? phj : ((r == p) ? php : pold[r]);
-    if (tid == 0) {
-      s_piv[j] = p;
-      piv[k + j] = k + p;
-    }
-    if (j == 1) { DBG(21) }
     const double2 inv = crcp_fast(pn[j * ldp + phj]);
-    if (j == 1) { DBG(22) }
     double bv = -1.0;
     int bi = INT_MAX;
     // each logical row r > j is owned by exactly one thread: it scales its
@@ -364,47 +418,45 @@ __global__ void __launch_bounds__(PT, 1)
         }
       }
     }
-    if (j == 1) { DBG(23) }
     if (j + 1 < NB && warp < nwarp_rows) publish(par ^ 1, bv, bi);
-    if (j == 1) { DBG(24) }
   }
   __syncthreads();
-  }
-  const int* fperm = perm + (NB & 1) * rows;  // final logical -> physical rows
+  const int* fperm = perm + (NB & 1) * rows;  // final logical -> entry
   __shared__ double2 s_lu[NB][NB + 1];
   for (int e = tid; e < NB * NB; e += PT) s_lu[e / NB][e % NB] = pn[(e % NB) * ldp + fperm[e / NB]];
   __syncthreads();
-  DBG(2)
-  panel_tail<NB>(cur, ld, n, n_true, k, b, S, status, s_lu, fperm, s_piv, tol, &s_fail);
+  panel_tail<NB>(cur, ld, n, n_true, k, b, last != 0, S, status, s_lu, fperm, act, tol, &s_fail, nullptr);
 }
 
 // Pivot-search key: |re|+|im| truncated to sign, exponent and 11 mantissa bits of
-// the double, above the complemented physical row. The unsigned maximum is the
-// largest magnitude (lowest row among equal keys), so one warp-wide REDUX.MAX is the
-// argmax. The chosen pivot is within a factor 1 - 2^-11 of the column maximum
+// the double, above the complemented active-list entry. The unsigned maximum is the
+// largest magnitude (lowest entry among equal keys), so one warp-wide REDUX.MAX is
+// the argmax. The chosen pivot is within a factor 1 - 2^-11 of the column maximum
 // (threshold partial pivoting, |l| <= 1.0005).
-constexpr int KEY_IB = 10;  // physical rows < 1024
+constexpr int KEY_IB = 10;  // active-list entries < 1024
 constexpr unsigned KEY_IMASK = (1u << KEY_IB) - 1;
-__device__ __forceinline__ unsigned piv_key(double2 v, int ph) {
+__device__ __forceinline__ unsigned piv_key(double2 v, int t) {
   const unsigned long long bits = (unsigned long long)__double_as_longlong(cabs1(v)) & 0x7fffffffffffffffULL;
-  return (unsigned(bits >> (63 - (32 - KEY_IB))) << KEY_IB) | (KEY_IMASK - unsigned(ph));
+  return (unsigned(bits >> (63 - (32 - KEY_IB))) << KEY_IB) | (KEY_IMASK - unsigned(t));
 }
 
-// Register-resident panel (rows <= RPT * PT). Thread t owns physical panel rows
-// t + i*PT for good: rows never move, the interchanges only relabel logical row
-// numbers, so the elimination never touches shared memory for its own data. Per
-// column: one barrier, the pivot resolved from the 8 published warp keys, the
-// winning row and its reciprocal read from the winner's warp slot, the update, and
-// the next column's warp keys by REDUX.
+// Register-resident panel (at most RPT * PT active rows). Thread t owns active-list
+// entries t + i*PT for good: the interchanges only relabel logical row numbers, so
+// the elimination never touches shared memory for its own data. Per column: one
+// barrier, the pivot resolved from the 8 published warp keys, the winning row and
+// its reciprocal read from the winner's warp slot, the update, and the next
+// column's warp keys by REDUX.
 template <int NB, int RPT>
 __global__ void __launch_bounds__(PT, 1)
     gj_panel_rows_kernel(const double2* __restrict__ cur0, long long ld, long long bstride, int n, int n_true, int k,
-                         GjScratch S, int* __restrict__ status) {
+                         int last, GjScratch S, int* __restrict__ status) {
+  extern __shared__ __align__(16) double2 sv[];  // Vs staging for the tail, NB x (n + 2)
   __shared__ unsigned cand_k[2][PT / 32];
   __shared__ double2 cand_r[2][PT / 32];
   __shared__ __align__(16) double2 cand_row[2][PT / 32][NB];
   __shared__ double2 s_lu[NB][NB + 1];
   __shared__ int s_map[RPT * PT];
+  __shared__ int s_act[RPT * PT];
   __shared__ int s_p[NB];
   __shared__ double s_red[PT / 32];
   __shared__ int s_fail;
@@ -414,17 +466,20 @@ __global__ void __launch_bounds__(PT, 1)
   const int b = blockIdx.x;
   const double2* __restrict__ cur = cur0 + (long long)b * bstride;
   const int rows = n - k;
+  const int* lmapg = S.lmap + (long long)b * n;
 
   double2 a[RPT][NB];
   int lg[RPT];
   bool act[RPT];
 #pragma unroll
   for (int i = 0; i < RPT; ++i) {
-    const int ph = tid + i * PT;
-    act[i] = ph < rows;
-    lg[i] = ph;
+    const int t = tid + i * PT;
+    act[i] = t < rows;
+    lg[i] = t;
+    const int ph = act[i] ? active_row(lmapg, k, t) : 0;
+    if (act[i]) s_act[t] = ph;
 #pragma unroll
-    for (int c = 0; c < NB; ++c) a[i][c] = act[i] ? cur[(long long)(k + c) * ld + k + ph] : make_double2(0.0, 0.0);
+    for (int c = 0; c < NB; ++c) a[i][c] = act[i] ? cur[(long long)(k + c) * ld + ph] : make_double2(0.0, 0.0);
   }
   if (tid == 0) s_fail = INT_MAX;
   if (k == 0) {
@@ -466,7 +521,7 @@ __global__ void __launch_bounds__(PT, 1)
   };
   publish(0, 0);
 
-  int prev_ph = -1;
+  int prev_t = -1;
 #pragma unroll
   for (int j = 0; j < NB; ++j) {
     const int par = j & 1;
@@ -475,17 +530,17 @@ __global__ void __launch_bounds__(PT, 1)
       const int pp = s_p[j - 1];
 #pragma unroll
       for (int i = 0; i < RPT; ++i)
-        if (lg[i] == j - 1 && tid + i * PT != prev_ph) lg[i] = pp;
+        if (lg[i] == j - 1 && tid + i * PT != prev_t) lg[i] = pp;
     }
     unsigned best = 0;
 #pragma unroll
     for (int q = 0; q < PT / 32; ++q) best = max(best, cand_k[par][q]);
-    const int phj = int(KEY_IMASK - (best & KEY_IMASK));
-    const int qw = (phj % PT) >> 5;
+    const int tj = int(KEY_IMASK - (best & KEY_IMASK));
+    const int qw = (tj % PT) >> 5;
     const double2 rcp = cand_r[par][qw];
 #pragma unroll
     for (int i = 0; i < RPT; ++i) {
-      if (tid + i * PT == phj) {  // this row becomes logical row j
+      if (tid + i * PT == tj) {  // this row becomes logical row j
         s_p[j] = lg[i];
         lg[i] = j;
         act[i] = false;
@@ -510,7 +565,7 @@ __global__ void __launch_bounds__(PT, 1)
         a[i][c] = x;
       }
     }
-    prev_ph = phj;
+    prev_t = tj;
     if (j + 1 < NB) publish(par ^ 1, j + 1);
   }
   __syncthreads();
@@ -518,40 +573,13 @@ __global__ void __launch_bounds__(PT, 1)
     const int pp = s_p[NB - 1];
 #pragma unroll
     for (int i = 0; i < RPT; ++i) {
-      const int ph = tid + i * PT;
-      if (lg[i] == NB - 1 && ph != prev_ph) lg[i] = pp;
-      if (ph < rows) s_map[lg[i]] = ph;
+      const int t = tid + i * PT;
+      if (lg[i] == NB - 1 && t != prev_t) lg[i] = pp;
+      if (t < rows) s_map[lg[i]] = t;
     }
   }
   __syncthreads();
-  panel_tail<NB>(cur, ld, n, n_true, k, b, S, status, s_lu, s_map, s_p, s_tol, &s_fail);
-}
-
-
-// After the last panel: column map that undoes the interchanges. With
-// X[:, c] = Y[:, q[c]] (q from the column swaps j = n-1 .. 0), the GEMM scatters
-// column c' of Y to colmap[c'] = q^{-1}(c').
-__global__ void build_colmap_kernel(const int* __restrict__ piv0, int* __restrict__ colmap0, int n) {
-  extern __shared__ int sq[];
-  const int b = blockIdx.x;
-  const int* piv = piv0 + (long long)b * n;
-  int* colmap = colmap0 + (long long)b * n;
-  int* spiv = sq + n;
-  for (int c = threadIdx.x; c < n; c += blockDim.x) {
-    sq[c] = c;
-    spiv[c] = piv[c];
-  }
-  __syncthreads();
-  if (threadIdx.x == 0) {
-    for (int j = n - 1; j >= 0; --j) {
-      const int p = spiv[j];
-      const int t = sq[j];
-      sq[j] = sq[p];
-      sq[p] = t;
-    }
-  }
-  __syncthreads();
-  for (int c = threadIdx.x; c < n; c += blockDim.x) colmap[sq[c]] = c;
+  panel_tail<NB>(cur, ld, n, n_true, k, b, last != 0, S, status, s_lu, s_map, s_act, s_tol, &s_fail, sv);
 }
 
 }  // namespace
@@ -560,98 +588,92 @@ extern "C" int bbsi_debug_zinv(long long* out) { return (int)cudaMemcpyFromSymbo
 
 size_t zinv_scratch_bytes(int n, int batch) {
   GjScratch s;
-  return carve(s, nullptr, n, pick_nb(n), batch) + 256;
+  return carve(s, nullptr, n, kNB, batch) + 256;
 }
 
 cudaError_t zinv_batched(double2* M, long long ld, long long bstride, int n, int n_true, int batch, void* scratch,
                          int* status, cudaStream_t stream) {
   if (n % 64 || n_true > n || n_true < 1) return cudaErrorInvalidValue;
   if (batch == 0) return cudaSuccess;
-  const int nb = pick_nb(n);
+  constexpr int nb = kNB;
   GjScratch S;
   carve(S, scratch, n, nb, batch);
-  const size_t smem = size_t(nb) * (n + 1) * sizeof(double2) + 2 * size_t(n) * sizeof(int);
-  static size_t attr16 = 0, attr32 = 0;
+  const size_t smem = size_t(nb) * (n + 1) * sizeof(double2) + 3 * size_t(n) * sizeof(int);
+  static size_t attr = 0;
   cudaError_t e;
-  if (nb == 32 && smem > attr32) {
-    if ((e = cudaFuncSetAttribute(gj_panel_kernel<32>, cudaFuncAttributeMaxDynamicSharedMemorySize, int(smem))))
+  if (smem > attr) {
+    if ((e = cudaFuncSetAttribute(gj_panel_kernel<kNB>, cudaFuncAttributeMaxDynamicSharedMemorySize, int(smem))))
       return e;
-    attr32 = smem;
+    attr = smem;
   }
-  if (nb == 16 && smem > attr16) {
-    if ((e = cudaFuncSetAttribute(gj_panel_kernel<16>, cudaFuncAttributeMaxDynamicSharedMemorySize, int(smem))))
+  const size_t rows_smem = size_t(nb) * (n + 2) * sizeof(double2);
+  static size_t attr_rows = 0;
+  if (rows_smem > attr_rows && use_rows_kernel()) {
+    if ((e = cudaFuncSetAttribute(gj_panel_rows_kernel<kNB, 1>, cudaFuncAttributeMaxDynamicSharedMemorySize,
+                                  int(rows_smem))))
       return e;
-    attr16 = smem;
+    if ((e = cudaFuncSetAttribute(gj_panel_rows_kernel<kNB, 2>, cudaFuncAttributeMaxDynamicSharedMemorySize,
+                                  int(rows_smem))))
+      return e;
+    attr_rows = rows_smem;
   }
   const long long nn = (long long)n * n;
   const int npan = n / nb;
   for (int pi = 0; pi < npan; ++pi) {
     const int k = pi * nb;
-    const bool last = pi == npan - 1;
-    const double2* cur = pi == 0 ? M : (pi % 2 ? S.s0 : S.s1);
+    const int last = pi == npan - 1;
+    // panel 0 reads the input block; the working matrix s0 is updated in place
+    const double2* cur = pi == 0 ? M : S.s0;
     const long long cld = pi == 0 ? ld : n, cbs = pi == 0 ? bstride : nn;
-    double2* nxt = last ? M : (pi % 2 ? S.s1 : S.s0);
+    double2* nxt = last ? M : S.s0;
     const long long nld = last ? ld : n, nbs = last ? bstride : nn;
     {
       ProfScope prof(stream, PROF_INV, 8.0 * double(n) * nb * nb * batch, 16.0 * (3.0 * n * nb) * batch);
-      // The panel is latency-bound and on the critical path of the sweep: launched at
-      // the greatest priority so its CTAs take SMs ahead of queued GEMM tiles of
-      // other streams (side-stream groups).
       cudaLaunchConfig_t cfg{};
       cfg.gridDim = dim3(batch);
       cfg.blockDim = dim3(PT);
-      cfg.dynamicSmemBytes = smem;
+      cfg.dynamicSmemBytes = 0;
       cfg.stream = stream;
-      cudaLaunchAttribute attr[1];
-      attr[0].id = cudaLaunchAttributePriority;
-      attr[0].val.priority = panel_priority();
-      cfg.attrs = attr;
+      cudaLaunchAttribute attr_[1];
+      attr_[0].id = cudaLaunchAttributePriority;
+      attr_[0].val.priority = panel_priority();
+      cfg.attrs = attr_;
       cfg.numAttrs = 1;
       const int rows = n - k;
-      const double2* cc = cur;
-      if (use_rows_kernel() && nb == 16 && rows <= PT) {
-        cfg.dynamicSmemBytes = 0;
-        e = cudaLaunchKernelEx(&cfg, gj_panel_rows_kernel<16, 1>, cc, cld, cbs, n, n_true, k, S, status);
-      } else if (use_rows_kernel() && nb == 16 && rows <= 2 * PT) {
-        cfg.dynamicSmemBytes = 0;
-        e = cudaLaunchKernelEx(&cfg, gj_panel_rows_kernel<16, 2>, cc, cld, cbs, n, n_true, k, S, status);
-      } else if (use_rows_kernel() && nb == 32 && rows <= PT) {
-        cfg.dynamicSmemBytes = 0;
-        e = cudaLaunchKernelEx(&cfg, gj_panel_rows_kernel<32, 1>, cc, cld, cbs, n, n_true, k, S, status);
-      } else if (nb == 32) {
-        e = cudaLaunchKernelEx(&cfg, gj_panel_kernel<32>, cc, cld, cbs, n, n_true, k, S, status);
+      cfg.dynamicSmemBytes = rows_smem;
+      if (use_rows_kernel() && rows <= PT) {
+        e = cudaLaunchKernelEx(&cfg, gj_panel_rows_kernel<kNB, 1>, cur, cld, cbs, n, n_true, k, last, S, status);
+      } else if (use_rows_kernel() && rows <= 2 * PT) {
+        e = cudaLaunchKernelEx(&cfg, gj_panel_rows_kernel<kNB, 2>, cur, cld, cbs, n, n_true, k, last, S, status);
       } else {
-        e = cudaLaunchKernelEx(&cfg, gj_panel_kernel<16>, cc, cld, cbs, n, n_true, k, S, status);
+        cfg.dynamicSmemBytes = smem;
+        e = cudaLaunchKernelEx(&cfg, gj_panel_kernel<kNB>, cur, cld, cbs, n, n_true, k, last, S, status);
       }
       if (e) return e;
-      if (last) {
-        build_colmap_kernel<<<batch, 256, 2 * n * sizeof(int), stream>>>(S.piv, S.colmap, n);
-        if ((e = cudaGetLastError())) return e;
-      }
     }
     ZGemmGroup g{};
     g.batch = batch;
     g.bs = 64;
     g.nprob = 1;
-    // GEMM 2: Next = Cur[rowmap] (zero on rows P, cols K) - Wz * V
-    ZGemmProblem& p2 = g.prob[0];
-    p2 = ZGemmProblem{};
-    p2.M = n;
-    p2.N = n;
-    p2.K = nb;
-    p2.alpha = make_double2(-1.0, 0.0);
-    p2.beta = make_double2(1.0, 0.0);
-    p2.A = ZOp{S.wz, n, 64, 64LL * n, (long long)n * nb};
-    p2.B = ZOp{S.vbuf, nb, 64, 64LL * nb, (long long)nb * n};
-    p2.C = ZOp{cur, cld, 64, 64LL * cld, cbs};
-    p2.D = ZOp{nxt, nld, 64, 64LL * nld, nbs};
-    p2.rowmap = S.rowmap;
-    p2.colmap = last ? S.colmap : nullptr;
-    p2.map_bstride = n;
-    p2.zr0 = k;
-    p2.zr1 = k + nb;
-    p2.zc0 = k;
-    p2.zc1 = k + nb;
+    // M <- M (0 on the pivot rows and the panel columns) - Wz V
+    ZGemmProblem& p = g.prob[0];
+    p = ZGemmProblem{};
+    p.M = n;
+    p.N = n;
+    p.K = nb;
+    p.alpha = make_double2(-1.0, 0.0);
+    p.beta = make_double2(1.0, 0.0);
+    p.A = ZOp{S.wz, n, 64, 64LL * n, (long long)n * nb};
+    p.B = ZOp{S.vbuf, nb, 64, 64LL * nb, (long long)nb * n};
+    p.C = ZOp{cur, cld, 64, 64LL * cld, cbs};
+    p.D = ZOp{nxt, nld, 64, 64LL * nld, nbs};
+    p.rowmap = S.rowmask;
+    p.rowscat = last ? S.rowscat : nullptr;
+    p.colmap = last ? S.colmap : nullptr;
+    p.map_bstride = n;
+    p.zr0 = p.zr1 = 0;
+    p.zc0 = k;
+    p.zc1 = k + nb;
     if ((e = zgemm_grouped(g, stream))) return e;
   }
   return cudaSuccess;

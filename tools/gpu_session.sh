@@ -1,7 +1,12 @@
+#!/bin/bash
 set -u
 O=gpurun_out
+echo "== pytest -m gpu"; timeout 1200 python -m pytest tests -x -q -m gpu 2>&1 | tail -3
+B="python bench.py --no-e2e --no-cpu-baseline --steps 3 --warmup 3"
+echo "== bench default";        timeout 600 $B 2>&1 | tail -1 | cut -c1-200
 P="python tools/prof_step.py --config 2 --layers 8 --energies 64"
-export BBSI_GROUPS=1
-timeout 300 $P > /dev/null 2>&1 || echo "prof_step failed"
-timeout 600 ncu --set full --import-source on --clock-control none -k regex:gj_panel_rows --launch-skip 20 -c 1 -o $O/panel_rows -f $P > $O/ncu_panel.log 2>&1; tail -2 $O/ncu_panel.log
-timeout 600 ncu --set full --import-source on --clock-control none -k regex:zgemm_grouped_kernel --launch-skip 40 -c 1 -o $O/gj_gemm -f $P > $O/ncu_gjgemm.log 2>&1; tail -2 $O/ncu_gjgemm.log
+N="ncu --metrics gpu__time_duration.sum --clock-control none --csv"
+echo "== launches groups 1"
+BBSI_GROUPS=1 timeout 300 $P > /dev/null 2>&1 && BBSI_GROUPS=1 timeout 600 $N --log-file $O/ll.csv $P > /dev/null 2>&1
+python tools/launches.py $O/ll.csv > $O/ll.txt; head -6 $O/ll.txt
+echo "== accuracy";             timeout 900 python tools/accuracy_probe.py --config 3 --energies 17 2>&1 | tail -1
