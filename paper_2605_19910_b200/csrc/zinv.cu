@@ -33,6 +33,12 @@
 
 namespace bbsi_gpu {
 __device__ long long g_zinv_dbg[64];
+#ifdef BBSI_ZINV_DEBUG
+#define ZDBG(i)                                                       \
+  if (blockIdx.x == 0 && threadIdx.x == 0 && k == 32) g_zinv_dbg[i] = clock64();
+#else
+#define ZDBG(i)
+#endif
 
 namespace {
 
@@ -129,6 +135,7 @@ __device__ __forceinline__ void panel_tail(const double2* __restrict__ cur, long
     s_src[tid] = act[lloc[tid]];
   }
   for (int r = tid; r < rows; r += PT) lmap[k + r] = act[lloc[r]];
+  ZDBG(3)
   // Wz (n x NB, ld n) = M[:,K] (rows are not permuted: coalesced); pivot rows fixed below
   for (int r = tid; r < n; r += PT) {
     rowmask[r] = r;
@@ -139,6 +146,7 @@ __device__ __forceinline__ void panel_tail(const double2* __restrict__ cur, long
     for (int c = 0; c < NB; ++c) wz[(long long)c * n + r] = v[c];
   }
   __syncthreads();
+  ZDBG(4)
   // Vs (pivot rows of M, identity in columns K) of this thread's first column, issued
   // now so the loads overlap the pivot-block inverse
   double2 xpre[NB];
@@ -154,31 +162,51 @@ __device__ __forceinline__ void panel_tail(const double2* __restrict__ cur, long
     wz[(long long)c * n + s_src[j]] = make_double2(j == c ? -1.0 : 0.0, 0.0);
     if (c == 0) rowmask[s_src[j]] = -1;
   }
-  // Pinv = (L U)^{-1} of the pivot block: warp w solves columns 2w, 2w+1 of the
-  // identity, one row per lane, values exchanged by shuffles.
+  ZDBG(5)
+  // Pinv = U^{-1} L^{-1} of the pivot block. Warp w solves columns 2w, 2w+1 of both
+  // triangular inverses at once (one row per lane, values exchanged by shuffles; the
+  // two 16-step chains interleave), then every thread forms one entry of the product.
+  __shared__ double2 s_li[NB][NB + 1];
+  __shared__ double2 s_ui[NB][NB + 1];
   if (warp < NB / 2) {
     const int r = lane & 15, c = 2 * warp + (lane >> 4), base = lane & 16;
-    double2 y = make_double2(r == c ? 1.0 : 0.0, 0.0);
+    double2 row[NB];
 #pragma unroll
-    for (int j = 0; j < NB - 1; ++j) {  // L y = e_c (unit lower)
-      double2 yj;
-      yj.x = __shfl_sync(0xffffffffu, y.x, base | j);
-      yj.y = __shfl_sync(0xffffffffu, y.y, base | j);
-      if (r > j) y = csub(y, cmul(lu[r][j], yj));
-    }
+    for (int q = 0; q < NB; ++q) row[q] = lu[r][q];
+    double2 yl = make_double2(r == c ? 1.0 : 0.0, 0.0), yu = yl;
 #pragma unroll
-    for (int j = NB - 1; j >= 0; --j) {  // U x = y
-      double2 yj;
-      yj.x = __shfl_sync(0xffffffffu, y.x, base | j);
-      yj.y = __shfl_sync(0xffffffffu, y.y, base | j);
-      const double2 xj = cmul(yj, s_uinv[j]);
-      if (r == j)
-        y = xj;
-      else if (r < j)
-        y = csub(y, cmul(lu[r][j], xj));
+    for (int j = 0; j < NB; ++j) {
+      if (j < NB - 1) {  // L yl = e_c (unit lower), forward step j
+        double2 t;
+        t.x = __shfl_sync(0xffffffffu, yl.x, base | j);
+        t.y = __shfl_sync(0xffffffffu, yl.y, base | j);
+        if (r > j) yl = csub(yl, cmul(row[j], t));
+      }
+      {  // U yu = e_c, backward step ju
+        const int ju = NB - 1 - j;
+        double2 t;
+        t.x = __shfl_sync(0xffffffffu, yu.x, base | ju);
+        t.y = __shfl_sync(0xffffffffu, yu.y, base | ju);
+        const double2 xj = cmul(t, s_uinv[ju]);
+        if (r == ju)
+          yu = xj;
+        else if (r < ju)
+          yu = csub(yu, cmul(row[ju], xj));
+      }
     }
-    s_pinv[r][c] = y;
+    s_li[r][c] = yl;
+    s_ui[r][c] = yu;
   }
+  __syncthreads();
+  for (int e = tid; e < NB * NB; e += PT) {  // Pinv[r][c] = sum_{q >= max(r, c)} Ui[r][q] Li[q][c]
+    const int r = e / NB, c = e % NB;
+    double2 acc = make_double2(0.0, 0.0);
+#pragma unroll
+    for (int q = 0; q < NB; ++q)
+      if (q >= r && q >= c) acc = cfma(s_ui[r][q], s_li[q][c], acc);
+    s_pinv[r][c] = acc;
+  }
+  ZDBG(6)
   if (sv) {
     // V = Pinv Vs on the tensor cores: Vs staged in smem (ld n + 2), each warp takes
     // 8-column tiles, 2 x 4 complex m8n8k4 steps (4 real DMMAs each) per tile.
@@ -192,7 +220,13 @@ __device__ __forceinline__ void panel_tail(const double2* __restrict__ cur, long
                                               : cur[(long long)col * ld + s_src[j]]);
     }
     __syncthreads();
+    ZDBG(7)
     const int lr = lane >> 2, lc = lane & 3;
+    double2 af[2][NB / 4];
+#pragma unroll
+    for (int mt = 0; mt < 2; ++mt)
+#pragma unroll
+      for (int ks = 0; ks < NB / 4; ++ks) af[mt][ks] = s_pinv[mt * 8 + lr][ks * 4 + lc];
     for (int nt = warp; nt < n / 8; nt += PT / 32) {
       double cr[2][2] = {{0.0, 0.0}, {0.0, 0.0}}, ci[2][2] = {{0.0, 0.0}, {0.0, 0.0}};
 #pragma unroll
@@ -200,7 +234,7 @@ __device__ __forceinline__ void panel_tail(const double2* __restrict__ cur, long
         const double2 bv = sv[(ks * 4 + lc) * svld + nt * 8 + lr];
 #pragma unroll
         for (int mt = 0; mt < 2; ++mt) {
-          const double2 av = s_pinv[mt * 8 + lr][ks * 4 + lc];
+          const double2 av = af[mt][ks];
           dmma884(cr[mt], av.x, bv.x);
           dmma884(cr[mt], -av.y, bv.y);
           dmma884(ci[mt], av.x, bv.y);
@@ -213,6 +247,7 @@ __device__ __forceinline__ void panel_tail(const double2* __restrict__ cur, long
         for (int q = 0; q < 2; ++q)
           vb[(long long)(nt * 8 + 2 * lc + q) * NB + mt * 8 + lr] = make_double2(cr[mt][q], ci[mt][q]);
     }
+    ZDBG(8)
   } else {
     __syncthreads();
     // V = Pinv Vs, one column per thread (tall panels: no smem left for Vs)
@@ -249,6 +284,7 @@ __device__ __forceinline__ void panel_tail(const double2* __restrict__ cur, long
   }
   __syncthreads();
   if (tid == 0 && *s_fail != INT_MAX && status[b] < 0) status[b] = *s_fail;
+  ZDBG(9)
 }
 
 // max |a_ij| (hypot) over the true n_true x n_true block -> eps * n_true * max (kernels.hpp:149-158)
@@ -466,6 +502,7 @@ __global__ void __launch_bounds__(PT, 1)
   const int b = blockIdx.x;
   const double2* __restrict__ cur = cur0 + (long long)b * bstride;
   const int rows = n - k;
+  ZDBG(0)
   const int* lmapg = S.lmap + (long long)b * n;
 
   double2 a[RPT][NB];
@@ -493,10 +530,11 @@ __global__ void __launch_bounds__(PT, 1)
     s_tol = S.tol[b];
   }
 
-  // publish this warp's best candidate for column J: key, reciprocal, row (c > J)
-  auto publish = [&](int par, int J) {
+  // This warp's best candidate for column J: its key (lane 0), and from the winning
+  // lane the reciprocal now and the row (c > J) once the row is fully updated.
+  auto publish_key = [&](int par, int J, int& wi) -> bool {
     unsigned key = 0;
-    int wi = 0;
+    wi = 0;
 #pragma unroll
     for (int i = 0; i < RPT; ++i)
       if (act[i]) {
@@ -508,18 +546,28 @@ __global__ void __launch_bounds__(PT, 1)
       }
     const unsigned wk = __reduce_max_sync(0xffffffffu, key);
     if (lane == 0) cand_k[par][warp] = wk;
-    if (wk != 0 && key == wk) {
+    const bool win = wk != 0 && key == wk;
+    if (win) {
 #pragma unroll
       for (int i = 0; i < RPT; ++i)
-        if (i == wi) {
-          cand_r[par][warp] = crcp_fast(a[i][J]);
-#pragma unroll
-          for (int c = 0; c < NB; ++c)
-            if (c > J) cand_row[par][warp][c] = a[i][c];
-        }
+        if (i == wi) cand_r[par][warp] = crcp_fast(a[i][J]);
     }
+    return win;
   };
-  publish(0, 0);
+  auto publish_row = [&](int par, int J, int wi) {
+#pragma unroll
+    for (int i = 0; i < RPT; ++i)
+      if (i == wi) {
+#pragma unroll
+        for (int c = 0; c < NB; ++c)
+          if (c > J) cand_row[par][warp][c] = a[i][c];
+      }
+  };
+  {
+    int wi;
+    if (publish_key(0, 0, wi)) publish_row(0, 0, wi);
+  }
+  ZDBG(1)
 
   int prev_t = -1;
 #pragma unroll
@@ -554,8 +602,7 @@ __global__ void __launch_bounds__(PT, 1)
       l[i] = act[i] ? cmul(a[i][j], rcp) : make_double2(0.0, 0.0);
       if (act[i]) a[i][j] = l[i];
     }
-#pragma unroll
-    for (int c = j + 1; c < NB; ++c) {
+    auto update = [&](int c) {
       const double2 u = cand_row[par][qw][c];
 #pragma unroll
       for (int i = 0; i < RPT; ++i) {
@@ -564,10 +611,19 @@ __global__ void __launch_bounds__(PT, 1)
         x.y = fma(-l[i].x, u.y, fma(-l[i].y, u.x, x.y));
         a[i][c] = x;
       }
-    }
+    };
     prev_t = tj;
-    if (j + 1 < NB) publish(par ^ 1, j + 1);
+    if (j + 1 < NB) {
+      // column j+1 first: its pivot search overlaps the rest of the update
+      update(j + 1);
+      int wi;
+      const bool win = publish_key(par ^ 1, j + 1, wi);
+#pragma unroll
+      for (int c = j + 2; c < NB; ++c) update(c);
+      if (win) publish_row(par ^ 1, j + 1, wi);
+    }
   }
+  ZDBG(2)
   __syncthreads();
   {
     const int pp = s_p[NB - 1];
