@@ -45,7 +45,7 @@ def parse():
     p.add_argument("--impl", default="ours", choices=["ours", "reference"])
     p.add_argument("--no-e2e", action="store_true")
     p.add_argument("--no-cpu-baseline", action="store_true")
-    p.add_argument("--chunk", type=int, default=0, help="energy chunk of the e2e path (0 = n/4)")
+    p.add_argument("--chunk", type=int, default=0, help="energy chunk of the e2e path (0 = all energies, memory permitting)")
     return p.parse_args()
 
 
@@ -250,11 +250,19 @@ def run_ours(args, rank, world, local_rank):
     flops_energy = D.algorithmic_flops(cfg)
     tflops = n_all * flops_energy / (ms_step * 1e-3) / 1e12
 
-    # ---- per-kernel breakdown of one step (CUDA events around every library launch)
+    # ---- per-kernel breakdown of one step (CUDA events around every library launch).
+    # One stream group, so every launch runs alone and its event time is its own
+    # duration (with two groups the events of concurrent launches overlap).
+    old_groups = os.environ.get("BBSI_GROUPS")
+    os.environ["BBSI_GROUPS"] = "1"
     L.bbsi_cuda_profile_enable(1)
     step()
     torch.cuda.synchronize()
     L.bbsi_cuda_profile_enable(0)
+    if old_groups is None:
+        del os.environ["BBSI_GROUPS"]
+    else:
+        os.environ["BBSI_GROUPS"] = old_groups
     prof = np.zeros(12)
     L.bbsi_cuda_profile_collect(prof.ctypes.data_as(C.c_void_p), 3)
     cats = {}
@@ -279,19 +287,17 @@ def run_ours(args, rank, world, local_rank):
     # ---- end to end through the host-buffer C ABI
     e2e = None
     if not args.no_e2e:
+        del G  # the resident result band (48 GiB at config 2): the host path allocates its own
+        torch.cuda.empty_cache()
         band = l * (2 * w + 1) * b * b
         Hh = torch.from_numpy(D.fill_h_host(cfg)).pin_memory()
         Gh = torch.empty((n_loc, l, 2 * w + 1, b, b), dtype=torch.complex128).pin_memory()
         zz = np.ascontiguousarray(zs, dtype=np.complex128)
-        sig = cfg.sigma()
-        fails = np.zeros(n_loc, dtype=np.int32)
 
-        def e2e_step():
-            rc = L.bbsi_cuda_dyson_rgf_z(l, w, b, n_loc, C.c_void_p(Hh.data_ptr()), zz.ctypes.data_as(C.c_void_p),
-                                         sig.ctypes.data_as(C.c_void_p), C.c_void_p(Gh.data_ptr()),
-                                         fails.ctypes.data_as(C.c_void_p), args.chunk)
-            if rc != 0:
-                raise RuntimeError(L.bbsi_cuda_last_error().decode())
+        Hn, Gn = Hh.numpy(), Gh.numpy()
+
+        def e2e_step():  # the public host-buffer API: H in, every G band streamed back
+            D.solve_host(cfg, H=Hn, z=zz, G=Gn, chunk=args.chunk)
 
         e2e_step()
         torch.cuda.synchronize()

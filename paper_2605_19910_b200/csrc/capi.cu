@@ -472,6 +472,13 @@ double bbsi_cuda_fp64_peak_tflops(double duration_ms, int reps) {
 // End-to-end Dyson batch from HOST buffers: H2D of H, energy chunks computed on
 // one stream while the finished chunks' G bands stream back to the host on a
 // second stream (pinned G_host gives full overlap).
+// Band rows per host hand-off of the streamed downward sweep (env BBSI_E2E_ROWS).
+static int e2e_rows() {
+  const char* e = getenv("BBSI_E2E_ROWS");
+  const int v = e ? atoi(e) : 0;
+  return v > 0 ? v : 8;
+}
+
 int bbsi_cuda_dyson_rgf_z(int l, int w, int bs, int n_energy, const double* H, const double* z, const double* sigma,
                           double* G, int* fail_layers, int chunk) {
   if (int rc = validate_layout(l, w, bs, nullptr)) return rc;
@@ -480,17 +487,24 @@ int bbsi_cuda_dyson_rgf_z(int l, int w, int bs, int n_energy, const double* H, c
   if (n_energy < 1) return fail(BBSI_INVALID_ARGUMENT, "n_energy must be >= 1");
   if (int rc = device_ok()) return rc;
   std::lock_guard<std::mutex> lk(g_call_mu);
-  if (chunk <= 0) chunk = (n_energy + 3) / 4;
-  if (chunk > n_energy) chunk = n_energy;
-  const int nchunk = (n_energy + chunk - 1) / chunk;
   const long long band = (long long)l * (2 * w + 1) * bs * bs;
   const size_t band_b = size_t(band) * sizeof(double2);
-  const int groups = default_groups(chunk, bs);
-  const size_t scr_b = sweep_scratch_bytes(l, w, bs, chunk, groups);
   size_t free_b = 0, total_b = 0;
   CK(cudaMemGetInfo(&free_b, &total_b));
+  free_b += arena_held({1, 4, 5});  // this call's own workspace slots are reused or regrown
+  // Default: every energy in one resident batch (finished band rows stream to the
+  // host during the downward sweep); smaller chunks only when HBM is short.
+  if (chunk <= 0 || chunk > n_energy) {
+    chunk = n_energy;
+    while (chunk > 1 && (size_t(chunk) * band_b + band_b +
+                         sweep_scratch_bytes(l, w, bs, chunk, default_groups(chunk, bs))) > free_b * 9 / 10)
+      chunk = (chunk + 1) / 2;
+  }
+  const int nchunk = (n_energy + chunk - 1) / chunk;
+  const int groups = default_groups(chunk, bs);
+  const size_t scr_b = sweep_scratch_bytes(l, w, bs, chunk, groups);
   int nbuf = nchunk;
-  while (nbuf > 2 && (size_t(nbuf) * chunk * band_b + band_b + scr_b) > free_b * 9 / 10) --nbuf;
+  while (nbuf > 1 && (size_t(nbuf) * chunk * band_b + band_b + scr_b) > free_b * 9 / 10) --nbuf;
   double2* dH = static_cast<double2*>(arena_get(4, band_b));
   double2* dG = static_cast<double2*>(arena_get(5, size_t(nbuf) * chunk * band_b));
   double2* dzs = static_cast<double2*>(arena_get(2, sizeof(double2) * (size_t(n_energy) + l)));
@@ -502,6 +516,9 @@ int bbsi_cuda_dyson_rgf_z(int l, int w, int bs, int n_energy, const double* H, c
   std::vector<cudaEvent_t> done(nchunk), freed(nbuf);
   for (auto& e : done) CK(cudaEventCreateWithFlags(&e, cudaEventDisableTiming));
   for (auto& e : freed) CK(cudaEventCreateWithFlags(&e, cudaEventDisableTiming));
+  cudaEvent_t rows_ev = nullptr;  // re-recorded per hand-off (each wait binds the current record)
+  CK(cudaEventCreateWithFlags(&rows_ev, cudaEventDisableTiming));
+  const size_t row_b = size_t(2 * w + 1) * bs * bs * sizeof(double2);
   std::vector<int> status(size_t(l) * n_energy, -1);
   int rc = BBSI_OK;
   auto body = [&]() -> int {
@@ -523,13 +540,24 @@ int bbsi_cuda_dyson_rgf_z(int l, int w, int bs, int n_energy, const double* H, c
       W.g_bstride = band;
       W.groups = groups;
       sweep_carve(W, scratch);
+      // finished band rows of the downward sweep -> host, on the copy stream, while the
+      // sweep continues (one 2D copy per hand-off: rows [r0, r1) of ne_g energies)
+      W.hook_rows = e2e_rows();
+      W.rows_done = [&, g, e0](int r0, int r1, int eg, int ne_g, cudaStream_t st) -> cudaError_t {
+        cudaError_t e = cudaEventRecord(rows_ev, st);
+        if (e == cudaSuccess) e = cudaStreamWaitEvent(sd, rows_ev, 0);
+        if (e != cudaSuccess) return e;
+        char* dst = reinterpret_cast<char*>(G) + size_t(e0 + eg) * band_b + size_t(r0) * row_b;
+        const char* src = reinterpret_cast<const char*>(g + size_t(eg) * band) + size_t(r0) * row_b;
+        return cudaMemcpy2DAsync(dst, band_b, src, band_b, size_t(r1 - r0) * row_b, size_t(ne_g),
+                                 cudaMemcpyDeviceToHost, sd);
+      };
       CK(rgf_sweeps(W, nt.data(), sc));
       // status rows [layer][ne] of this chunk -> host (pageable; tiny)
       std::vector<int> st(size_t(l) * ne);
       CK(cudaMemcpyAsync(st.data(), W.status, st.size() * sizeof(int), cudaMemcpyDeviceToHost, sc));
       CK(cudaEventRecord(done[c], sc));
       CK(cudaStreamWaitEvent(sd, done[c], 0));
-      CK(cudaMemcpyAsync(G + 2 * size_t(e0) * band, g, size_t(ne) * band_b, cudaMemcpyDeviceToHost, sd));
       CK(cudaEventRecord(freed[buf], sd));
       CK(cudaEventSynchronize(done[c]));  // st is filled (pageable copy); keeps the host one chunk ahead
       for (int j = 0; j < l; ++j)
@@ -542,6 +570,7 @@ int bbsi_cuda_dyson_rgf_z(int l, int w, int bs, int n_energy, const double* H, c
   rc = body();
   for (auto& e : done) cudaEventDestroy(e);
   for (auto& e : freed) cudaEventDestroy(e);
+  cudaEventDestroy(rows_ev);
   cudaStreamDestroy(sc);
   cudaStreamDestroy(sd);
   if (rc) return rc;

@@ -1,6 +1,9 @@
 // Internal declarations shared by the CUDA translation units of libbbsi_cuda.so.
 #pragma once
 #include <cuda_runtime.h>
+
+#include <functional>
+#include <initializer_list>
 #include <stdint.h>
 
 #include <string>
@@ -39,6 +42,12 @@ struct SweepWork {
   void* inv = nullptr;    // zinv scratch for `batch` matrices
   int groups = 1;         // independent batch groups swept concurrently on side streams
   int* status = nullptr;  // [l][batch]
+  // Optional: called (while enqueueing) once band rows [r0, r1) of batch entries
+  // [e0, e0 + ne) are final on stream s -- every `hook_rows` rows of the downward
+  // sweep and at its end. Used to stream results to the host during the sweep.
+  std::function<cudaError_t(int r0, int r1, int e0, int ne, cudaStream_t s)> rows_done;
+  int hook_rows = 8;
+  int e_off = 0;          // batch offset of this (group's) sub-batch, for rows_done
 };
 
 // Bytes of LM+UM+piv+wz+status for a sweep.
@@ -102,6 +111,8 @@ double fp64_dmma_peak(double duration_ms, int reps);
 
 // Grow-only device arena per (device, slot) with a mutex; returns nullptr on OOM.
 void* arena_get(int slot, size_t bytes);
+// Bytes currently held by the given arena slots on the current device (reusable).
+size_t arena_held(std::initializer_list<int> slots);
 void arena_release_all();
 
 }  // namespace bbsi_gpu

@@ -129,6 +129,16 @@ cudaError_t rgf_sweeps_one(const SweepWork& W, const int* n_true, int* status, i
   if ((e = inv(0)) != cudaSuccess) return e;
 
   // ---------------- downward sweep (rgf.hpp:117-135)
+  // Step j writes rows j (slots -t, 0) and j-t (slot +t), t <= w: after it, rows
+  // [0, j-w] are final.
+  int flushed = 0;
+  auto flush = [&](int upto) -> cudaError_t {
+    if (!W.rows_done || upto <= flushed) return cudaSuccess;
+    const cudaError_t r = W.rows_done(flushed, upto, W.e_off, W.batch, s);
+    flushed = upto;
+    return r;
+  };
+  if (l == 1 && (e = flush(1)) != cudaSuccess) return e;
   for (int j = 1; j < l; ++j) {
     const int k = j < w ? j : w;
     ZOp lmrow = c.mop(c.lm(j), 0, 1);
@@ -138,7 +148,10 @@ cudaError_t rgf_sweeps_one(const SweepWork& W, const int* n_true, int* status, i
     if ((e = launch(W, {p_row, p_col}, s)) != cudaSuccess) return e;
     ZGemmProblem p_diag = prob(b, b, k * b, -1.0, 1.0, lmrow, c.gop(c.slot(j - 1, +1), -two_w, 0), c.gop(c.slot(j, 0), 0, 0));
     if ((e = launch(W, {p_diag}, s)) != cudaSuccess) return e;
+    const int complete = j - w + 1;
+    if (W.rows_done && complete - flushed >= W.hook_rows && (e = flush(complete)) != cudaSuccess) return e;
   }
+  if ((e = flush(l)) != cudaSuccess) return e;
   return cudaSuccess;
 }
 
@@ -190,6 +203,7 @@ cudaError_t rgf_sweeps(const SweepWork& W, const int* n_true, cudaStream_t s) {
     Wg.LM = W.LM + (long long)e0 * W.l * W.w * bb;
     Wg.UM = W.UM + (long long)e0 * W.l * W.w * bb;
     Wg.inv = static_cast<char*>(W.inv) + size_t(g) * inv_b;
+    Wg.e_off = W.e_off + e0;
     if ((e = cudaStreamWaitEvent(P.s[g], P.ev[G], 0))) return e;
     if ((e = rgf_sweeps_one(Wg, n_true, W.status + e0, W.batch, P.s[g]))) return e;
     if ((e = cudaEventRecord(P.ev[g], P.s[g]))) return e;
@@ -246,6 +260,17 @@ void* arena_get(int slot, size_t bytes) {
   }
   b.n = bytes;
   return b.p;
+}
+
+size_t arena_held(std::initializer_list<int> slots) {
+  std::lock_guard<std::mutex> lk(g_arena_mu);
+  int dev = 0;
+  cudaGetDevice(&dev);
+  if (int(g_arena.size()) <= dev) return 0;
+  size_t n = 0;
+  for (int sl : slots)
+    if (sl < int(g_arena[dev].size()) && g_arena[dev][sl].p) n += g_arena[dev][sl].n;
+  return n;
 }
 
 void arena_release_all() {

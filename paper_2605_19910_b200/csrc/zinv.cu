@@ -50,13 +50,16 @@ constexpr int PT = 256;  // panel kernel threads
 // accuracy with the pivot-block width.
 constexpr int kNB = 16;
 
-// BBSI_PANEL_ROWS=0 selects the shared-memory panel kernel everywhere (A/B checks).
-bool use_rows_kernel() {
-  static bool on = [] {
-    const char* e = getenv("BBSI_PANEL_ROWS");
-    return !(e && atoi(e) == 0);
+// Panels of at most 2*PT active rows use the register-resident kernel; BBSI_PANEL=2
+// selects the tall-panel shared-memory kernel everywhere (A/B checks). A compact
+// variant with the rows in shared memory and rolled column loops measured slower on
+// B200 (41 k vs 15 k cycles for the 16 elimination steps at n = 256).
+int panel_kind() {
+  static int kind = [] {
+    const char* e = getenv("BBSI_PANEL");
+    return (e && atoi(e) == 2) ? 2 : 1;
   }();
-  return on;
+  return kind;
 }
 
 // The panel is latency-bound and on the critical path of the sweep: launched at the
@@ -170,29 +173,21 @@ __device__ __forceinline__ void panel_tail(const double2* __restrict__ cur, long
   __shared__ double2 s_ui[NB][NB + 1];
   if (warp < NB / 2) {
     const int r = lane & 15, c = 2 * warp + (lane >> 4), base = lane & 16;
-    double2 row[NB];
-#pragma unroll
-    for (int q = 0; q < NB; ++q) row[q] = lu[r][q];
     double2 yl = make_double2(r == c ? 1.0 : 0.0, 0.0), yu = yl;
-#pragma unroll
+#pragma unroll 1
     for (int j = 0; j < NB; ++j) {
-      if (j < NB - 1) {  // L yl = e_c (unit lower), forward step j
-        double2 t;
-        t.x = __shfl_sync(0xffffffffu, yl.x, base | j);
-        t.y = __shfl_sync(0xffffffffu, yl.y, base | j);
-        if (r > j) yl = csub(yl, cmul(row[j], t));
-      }
-      {  // U yu = e_c, backward step ju
-        const int ju = NB - 1 - j;
-        double2 t;
-        t.x = __shfl_sync(0xffffffffu, yu.x, base | ju);
-        t.y = __shfl_sync(0xffffffffu, yu.y, base | ju);
-        const double2 xj = cmul(t, s_uinv[ju]);
-        if (r == ju)
-          yu = xj;
-        else if (r < ju)
-          yu = csub(yu, cmul(row[ju], xj));
-      }
+      const int ju = NB - 1 - j;
+      double2 tl, tu;
+      tl.x = __shfl_sync(0xffffffffu, yl.x, base | (j < NB - 1 ? j : 0));
+      tl.y = __shfl_sync(0xffffffffu, yl.y, base | (j < NB - 1 ? j : 0));
+      tu.x = __shfl_sync(0xffffffffu, yu.x, base | ju);
+      tu.y = __shfl_sync(0xffffffffu, yu.y, base | ju);
+      if (j < NB - 1 && r > j) yl = csub(yl, cmul(lu[r][j], tl));  // L yl = e_c, forward step j
+      const double2 xj = cmul(tu, s_uinv[ju]);                      // U yu = e_c, backward step ju
+      if (r == ju)
+        yu = xj;
+      else if (r < ju)
+        yu = csub(yu, cmul(lu[r][ju], xj));
     }
     s_li[r][c] = yl;
     s_ui[r][c] = yu;
@@ -662,15 +657,12 @@ cudaError_t zinv_batched(double2* M, long long ld, long long bstride, int n, int
       return e;
     attr = smem;
   }
-  const size_t rows_smem = size_t(nb) * (n + 2) * sizeof(double2);
+  const size_t rows_smem = size_t(nb) * (n + 2) * sizeof(double2);  // Vs staging of the tail
   static size_t attr_rows = 0;
-  if (rows_smem > attr_rows && use_rows_kernel()) {
-    if ((e = cudaFuncSetAttribute(gj_panel_rows_kernel<kNB, 1>, cudaFuncAttributeMaxDynamicSharedMemorySize,
-                                  int(rows_smem))))
-      return e;
-    if ((e = cudaFuncSetAttribute(gj_panel_rows_kernel<kNB, 2>, cudaFuncAttributeMaxDynamicSharedMemorySize,
-                                  int(rows_smem))))
-      return e;
+  if (rows_smem > attr_rows) {
+    const void* fns[2] = {(const void*)gj_panel_rows_kernel<kNB, 1>, (const void*)gj_panel_rows_kernel<kNB, 2>};
+    for (const void* f : fns)
+      if ((e = cudaFuncSetAttribute(f, cudaFuncAttributeMaxDynamicSharedMemorySize, int(rows_smem)))) return e;
     attr_rows = rows_smem;
   }
   const long long nn = (long long)n * n;
@@ -696,10 +688,12 @@ cudaError_t zinv_batched(double2* M, long long ld, long long bstride, int n, int
       cfg.attrs = attr_;
       cfg.numAttrs = 1;
       const int rows = n - k;
-      cfg.dynamicSmemBytes = rows_smem;
-      if (use_rows_kernel() && rows <= PT) {
+      const int kind = panel_kind();
+      if (kind == 1 && rows <= PT) {
+        cfg.dynamicSmemBytes = rows_smem;
         e = cudaLaunchKernelEx(&cfg, gj_panel_rows_kernel<kNB, 1>, cur, cld, cbs, n, n_true, k, last, S, status);
-      } else if (use_rows_kernel() && rows <= 2 * PT) {
+      } else if (kind == 1 && rows <= 2 * PT) {
+        cfg.dynamicSmemBytes = rows_smem;
         e = cudaLaunchKernelEx(&cfg, gj_panel_rows_kernel<kNB, 2>, cur, cld, cbs, n, n_true, k, last, S, status);
       } else {
         cfg.dynamicSmemBytes = smem;

@@ -65,3 +65,19 @@ def test_config3_proxy(gpu):
 
 def test_config5_block_size_proxy(gpu):
     _check(D.scaled(D.CONFIGS[5], num_layers=6, n_energy=2))
+
+
+@pytest.mark.parametrize("cfg_id,layers,n_e,b,chunk", [(2, 20, 10, 64, 0), (2, 20, 10, 64, 3), (3, 11, 3, 64, 0)])
+def test_host_path_streams_identical_bands(gpu, cfg_id, layers, n_e, b, chunk):
+    """bbsi_cuda_dyson_rgf_z (host buffers, rows streamed during the downward sweep,
+    optional energy chunks) returns exactly the resident path's bands."""
+    cfg = D.scaled(D.CONFIGS[cfg_id], num_layers=layers, n_energy=n_e, block_size=b)
+    dev = np.swapaxes(_run_gpu(cfg), -1, -2)  # back to slot memory
+    got, fails = D.solve_host(cfg, chunk=chunk)
+    assert (fails == -1).all()
+    assert np.array_equal(got, dev)
+    lay = O.make_layout(cfg.num_layers, cfg.block_size, cfg.bandwidth)
+    for e in (0, n_e - 1):
+        a = _oracle_band(cfg, e)
+        ref = O.rgf_ndiag(a)[0] if cfg.bandwidth > 1 else O.rgf_tridiag(a)[0]
+        assert O.max_block_error(O.Band(lay, np.swapaxes(got[e], -1, -2)), ref) <= TOL
