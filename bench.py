@@ -263,10 +263,10 @@ def run_ours(args, rank, world, local_rank):
         del os.environ["BBSI_GROUPS"]
     else:
         os.environ["BBSI_GROUPS"] = old_groups
-    prof = np.zeros(12)
-    L.bbsi_cuda_profile_collect(prof.ctypes.data_as(C.c_void_p), 3)
+    prof = np.zeros(16)
+    L.bbsi_cuda_profile_collect(prof.ctypes.data_as(C.c_void_p), 4)
     cats = {}
-    for i, name in enumerate(["zgemm_dmma", "zinv_gj", "band_ops"]):
+    for i, name in enumerate(["zgemm_dmma", "gj_panel", "band_ops", "gj_gemm"]):
         cnt, tms, fl, by = prof[4 * i: 4 * i + 4]
         cats[name] = {"launches": int(cnt), "ms": round(tms, 3),
                       "tflops": round(fl / (tms * 1e-3) / 1e12, 3) if tms > 0 else None,
@@ -274,9 +274,12 @@ def run_ours(args, rank, world, local_rank):
     peak = L.bbsi_cuda_fp64_peak_tflops(50.0, 5)
     g = cats["zgemm_dmma"]
     step_kernel_ms = sum(c["ms"] for c in cats.values())
-    roofline = {"bound": "tensor", "kernel": "zgemm_grouped_kernel (DMMA f64)", "achieved": g["tflops"],
+    roofline = {"bound": "tensor", "kernel": "zgemm_grouped_kernel (DMMA f64), sweep launches "
+                "(its Gauss-Jordan launches are listed as gj_gemm)", "achieved": g["tflops"],
                 "peak": round(peak, 2), "unit": "TFLOP/s", "frac": round(g["tflops"] / peak, 4) if peak > 0 else None,
-                "traffic": None,
+                # dram read + write of one sweep-GEMM launch (2048 tiles) from the ncu
+                # --set full capture in profiles/r01_ncu_zgemm.md
+                "traffic": 436.73e6, "traffic_unit": "bytes per launch (win+um, 2048 tiles)",
                 "peak_source": "FP64 DMMA peak measured live in this run (bbsi_cuda_fp64_peak_tflops; "
                                "MEASURED_PEAKS.json has no FP64 entry)",
                 "share_of_step": round(g["ms"] / step_kernel_ms, 3) if step_kernel_ms else None,

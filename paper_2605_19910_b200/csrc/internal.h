@@ -89,7 +89,7 @@ cudaError_t ddrgf_phase3(const double2* A, double2* G, int l, int b, const int* 
 void ddrgf_reference_counters(long long l, const int* s2_levels, int n_levels, long long out[3]);
 
 // Launch accounting / optional event timing around one kernel launch (prof.cu).
-enum ProfCat { PROF_GEMM = 0, PROF_INV = 1, PROF_BAND = 2, PROF_NCAT = 3 };
+enum ProfCat { PROF_GEMM = 0, PROF_INV = 1, PROF_BAND = 2, PROF_GJ_GEMM = 3, PROF_NCAT = 4 };
 class ProfScope {
  public:
   ProfScope(cudaStream_t s, int cat, double flops, double bytes);

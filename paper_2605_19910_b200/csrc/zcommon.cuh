@@ -47,6 +47,7 @@ struct ZGemmGroup {
   int batch;
   int bs;
   int total_tiles;      // sum over problems of tiles_m * tiles_n * batch
+  int prof_cat;         // profiling category of the launch (0 = main GEMM)
 };
 
 __host__ __device__ inline long long zop_offset(const ZOp& o, int bs, int r, int c) {

@@ -315,7 +315,7 @@ cudaError_t zgemm_grouped(ZGemmGroup& g, cudaStream_t stream) {
     fl += 8.0 * P.M * P.N * double(P.K) * g.batch;
     by += 16.0 * g.batch * (double(P.M) * P.K + double(P.K) * P.N + double(P.M) * P.N * (rc ? 2 : 1));
   }
-  ProfScope prof(stream, PROF_GEMM, fl, by);
+  ProfScope prof(stream, g.prof_cat ? g.prof_cat : PROF_GEMM, fl, by);
   cudaError_t e;
   const bool three = gemm_minb() == 3;
   if (plain && three) {

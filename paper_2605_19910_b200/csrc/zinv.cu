@@ -50,14 +50,17 @@ constexpr int PT = 256;  // panel kernel threads
 // accuracy with the pivot-block width.
 constexpr int kNB = 16;
 
-// Panels of at most 2*PT active rows use the register-resident kernel; BBSI_PANEL=2
-// selects the tall-panel shared-memory kernel everywhere (A/B checks). A compact
-// variant with the rows in shared memory and rolled column loops measured slower on
-// B200 (41 k vs 15 k cycles for the 16 elimination steps at n = 256).
+// Panel kernels (A/B switch BBSI_PANEL): 1 (default) two register-resident panels per
+// step with one rank-32 update; 3 one register-resident panel per step; 2 the
+// tall-panel shared-memory kernel everywhere. Panels with more than 2*PT active rows
+// always use the tall-panel kernel. A compact variant with the rows in shared memory
+// and rolled column loops measured slower on B200 (41 k vs 15 k cycles for the 16
+// elimination steps at n = 256).
 int panel_kind() {
   static int kind = [] {
     const char* e = getenv("BBSI_PANEL");
-    return (e && atoi(e) == 2) ? 2 : 1;
+    const int v = e ? atoi(e) : 1;
+    return (v == 2 || v == 3) ? v : 1;
   }();
   return kind;
 }
@@ -101,14 +104,102 @@ size_t carve(GjScratch& s, void* base, int n, int nb, int batch) {
   s.rowscat = reinterpret_cast<int*>(take(sizeof(int) * size_t(batch) * n));
   s.colmap = reinterpret_cast<int*>(take(sizeof(int) * size_t(batch) * n));
   s.tol = reinterpret_cast<double*>(take(sizeof(double) * size_t(batch)));
-  s.wz = reinterpret_cast<double2*>(take(sizeof(double2) * size_t(batch) * n * nb));
-  s.vbuf = reinterpret_cast<double2*>(take(sizeof(double2) * size_t(batch) * nb * n));
+  s.wz = reinterpret_cast<double2*>(take(sizeof(double2) * size_t(batch) * n * 2 * nb));  // two panels
+  s.vbuf = reinterpret_cast<double2*>(take(sizeof(double2) * size_t(batch) * 2 * nb * n));
   s.s0 = reinterpret_cast<double2*>(take(sizeof(double2) * size_t(batch) * n * n));
   return off;
 }
 
 // Physical row of active-list entry t of the panel at k (the list is lmap[k..n-1]).
 __device__ __forceinline__ int active_row(const int* lmap, int k, int t) { return k == 0 ? t : lmap[k + t]; }
+
+// Pinv = U^{-1} L^{-1} of a factored NB x NB pivot block (lu: L \ U, uinv: 1/U_jj).
+// Warp w solves columns 2w, 2w+1 of both triangular inverses at once (one row per
+// lane, values exchanged by shuffles; the two 16-step chains interleave), then every
+// thread forms one entry of the product. Called by the whole CTA; ends synchronised.
+template <int NB>
+__device__ __forceinline__ void pivot_block_inverse(const double2 (*lu)[NB + 1], const double2* uinv,
+                                                    double2 (*pinv)[NB + 1]) {
+  static_assert(NB == 16, "the warp-level pivot-block inverse assumes NB = 16 (two columns per warp)");
+  __shared__ double2 s_li[NB][NB + 1];
+  __shared__ double2 s_ui[NB][NB + 1];
+  const int tid = threadIdx.x, lane = tid & 31, warp = tid >> 5;
+  if (warp < NB / 2) {
+    const int r = lane & 15, c = 2 * warp + (lane >> 4), base = lane & 16;
+    double2 yl = make_double2(r == c ? 1.0 : 0.0, 0.0), yu = yl;
+#pragma unroll 1
+    for (int j = 0; j < NB; ++j) {
+      const int ju = NB - 1 - j;
+      double2 tl, tu;
+      tl.x = __shfl_sync(0xffffffffu, yl.x, base | (j < NB - 1 ? j : 0));
+      tl.y = __shfl_sync(0xffffffffu, yl.y, base | (j < NB - 1 ? j : 0));
+      tu.x = __shfl_sync(0xffffffffu, yu.x, base | ju);
+      tu.y = __shfl_sync(0xffffffffu, yu.y, base | ju);
+      if (j < NB - 1 && r > j) yl = csub(yl, cmul(lu[r][j], tl));  // L yl = e_c, forward step j
+      const double2 xj = cmul(tu, uinv[ju]);                        // U yu = e_c, backward step ju
+      if (r == ju)
+        yu = xj;
+      else if (r < ju)
+        yu = csub(yu, cmul(lu[r][ju], xj));
+    }
+    s_li[r][c] = yl;
+    s_ui[r][c] = yu;
+  }
+  __syncthreads();
+  for (int e = tid; e < NB * NB; e += PT) {  // Pinv[r][c] = sum_{q >= max(r, c)} Ui[r][q] Li[q][c]
+    const int r = e / NB, c = e % NB;
+    double2 acc = make_double2(0.0, 0.0);
+#pragma unroll
+    for (int q = 0; q < NB; ++q)
+      if (q >= r && q >= c) acc = cfma(s_ui[r][q], s_li[q][c], acc);
+    pinv[r][c] = acc;
+  }
+  __syncthreads();
+}
+
+// V = Pinv Vs on the tensor cores, Vs (NB x n) staged in shared memory with ld svld.
+// Each warp takes 8-column tiles (2 x 4 complex m8n8k4 steps, 4 real DMMAs each).
+// dst != nullptr: V[j][col] -> dst[col * dld + j]; otherwise V overwrites Vs in place
+// (a warp reads all of its tile before writing it).
+template <int NB>
+__device__ __forceinline__ void apply_pinv_dmma(const double2 (*pinv)[NB + 1], double2* sv, int svld, int n,
+                                                double2* __restrict__ dst, int dld) {
+  const int lane = threadIdx.x & 31, warp = threadIdx.x >> 5;
+  const int lr = lane >> 2, lc = lane & 3;
+  double2 af[2][NB / 4];
+#pragma unroll
+  for (int mt = 0; mt < 2; ++mt)
+#pragma unroll
+    for (int ks = 0; ks < NB / 4; ++ks) af[mt][ks] = pinv[mt * 8 + lr][ks * 4 + lc];
+  for (int nt = warp; nt < n / 8; nt += PT / 32) {
+    double2 bv[NB / 4];
+#pragma unroll
+    for (int ks = 0; ks < NB / 4; ++ks) bv[ks] = sv[(ks * 4 + lc) * svld + nt * 8 + lr];
+    double cr[2][2] = {{0.0, 0.0}, {0.0, 0.0}}, ci[2][2] = {{0.0, 0.0}, {0.0, 0.0}};
+#pragma unroll
+    for (int ks = 0; ks < NB / 4; ++ks)
+#pragma unroll
+      for (int mt = 0; mt < 2; ++mt) {
+        const double2 av = af[mt][ks];
+        dmma884(cr[mt], av.x, bv[ks].x);
+        dmma884(cr[mt], -av.y, bv[ks].y);
+        dmma884(ci[mt], av.x, bv[ks].y);
+        dmma884(ci[mt], av.y, bv[ks].x);
+      }
+    __syncwarp();
+#pragma unroll
+    for (int mt = 0; mt < 2; ++mt)
+#pragma unroll
+      for (int q = 0; q < 2; ++q) {
+        const int col = nt * 8 + 2 * lc + q, row = mt * 8 + lr;
+        const double2 v = make_double2(cr[mt][q], ci[mt][q]);
+        if (dst)
+          dst[(long long)col * dld + row] = v;
+        else
+          sv[row * svld + col] = v;
+      }
+  }
+}
 
 // Everything after the pivot search, shared by both panel kernels.
 //   lu[j][c]   pivot row j (logical): L multipliers for c < j, U for c >= j
@@ -125,7 +216,7 @@ __device__ __forceinline__ void panel_tail(const double2* __restrict__ cur, long
   __shared__ double2 s_uinv[NB];
   __shared__ int s_src[NB];  // physical pivot rows
   __shared__ double2 s_pinv[NB][NB + 1];
-  const int tid = threadIdx.x, lane = tid & 31, warp = tid >> 5;
+  const int tid = threadIdx.x;
   const int rows = n - k;
   int* __restrict__ lmap = S.lmap + (long long)b * n;
   int* __restrict__ rowmask = S.rowmask + (long long)b * n;
@@ -166,41 +257,7 @@ __device__ __forceinline__ void panel_tail(const double2* __restrict__ cur, long
     if (c == 0) rowmask[s_src[j]] = -1;
   }
   ZDBG(5)
-  // Pinv = U^{-1} L^{-1} of the pivot block. Warp w solves columns 2w, 2w+1 of both
-  // triangular inverses at once (one row per lane, values exchanged by shuffles; the
-  // two 16-step chains interleave), then every thread forms one entry of the product.
-  __shared__ double2 s_li[NB][NB + 1];
-  __shared__ double2 s_ui[NB][NB + 1];
-  if (warp < NB / 2) {
-    const int r = lane & 15, c = 2 * warp + (lane >> 4), base = lane & 16;
-    double2 yl = make_double2(r == c ? 1.0 : 0.0, 0.0), yu = yl;
-#pragma unroll 1
-    for (int j = 0; j < NB; ++j) {
-      const int ju = NB - 1 - j;
-      double2 tl, tu;
-      tl.x = __shfl_sync(0xffffffffu, yl.x, base | (j < NB - 1 ? j : 0));
-      tl.y = __shfl_sync(0xffffffffu, yl.y, base | (j < NB - 1 ? j : 0));
-      tu.x = __shfl_sync(0xffffffffu, yu.x, base | ju);
-      tu.y = __shfl_sync(0xffffffffu, yu.y, base | ju);
-      if (j < NB - 1 && r > j) yl = csub(yl, cmul(lu[r][j], tl));  // L yl = e_c, forward step j
-      const double2 xj = cmul(tu, s_uinv[ju]);                      // U yu = e_c, backward step ju
-      if (r == ju)
-        yu = xj;
-      else if (r < ju)
-        yu = csub(yu, cmul(lu[r][ju], xj));
-    }
-    s_li[r][c] = yl;
-    s_ui[r][c] = yu;
-  }
-  __syncthreads();
-  for (int e = tid; e < NB * NB; e += PT) {  // Pinv[r][c] = sum_{q >= max(r, c)} Ui[r][q] Li[q][c]
-    const int r = e / NB, c = e % NB;
-    double2 acc = make_double2(0.0, 0.0);
-#pragma unroll
-    for (int q = 0; q < NB; ++q)
-      if (q >= r && q >= c) acc = cfma(s_ui[r][q], s_li[q][c], acc);
-    s_pinv[r][c] = acc;
-  }
+  pivot_block_inverse<NB>(lu, s_uinv, s_pinv);
   ZDBG(6)
   if (sv) {
     // V = Pinv Vs on the tensor cores: Vs staged in smem (ld n + 2), each warp takes
@@ -216,35 +273,9 @@ __device__ __forceinline__ void panel_tail(const double2* __restrict__ cur, long
     }
     __syncthreads();
     ZDBG(7)
-    const int lr = lane >> 2, lc = lane & 3;
-    double2 af[2][NB / 4];
-#pragma unroll
-    for (int mt = 0; mt < 2; ++mt)
-#pragma unroll
-      for (int ks = 0; ks < NB / 4; ++ks) af[mt][ks] = s_pinv[mt * 8 + lr][ks * 4 + lc];
-    for (int nt = warp; nt < n / 8; nt += PT / 32) {
-      double cr[2][2] = {{0.0, 0.0}, {0.0, 0.0}}, ci[2][2] = {{0.0, 0.0}, {0.0, 0.0}};
-#pragma unroll
-      for (int ks = 0; ks < NB / 4; ++ks) {
-        const double2 bv = sv[(ks * 4 + lc) * svld + nt * 8 + lr];
-#pragma unroll
-        for (int mt = 0; mt < 2; ++mt) {
-          const double2 av = af[mt][ks];
-          dmma884(cr[mt], av.x, bv.x);
-          dmma884(cr[mt], -av.y, bv.y);
-          dmma884(ci[mt], av.x, bv.y);
-          dmma884(ci[mt], av.y, bv.x);
-        }
-      }
-#pragma unroll
-      for (int mt = 0; mt < 2; ++mt)
-#pragma unroll
-        for (int q = 0; q < 2; ++q)
-          vb[(long long)(nt * 8 + 2 * lc + q) * NB + mt * 8 + lr] = make_double2(cr[mt][q], ci[mt][q]);
-    }
+    apply_pinv_dmma<NB>(s_pinv, sv, svld, n, vb, NB);
     ZDBG(8)
   } else {
-    __syncthreads();
     // V = Pinv Vs, one column per thread (tall panels: no smem left for Vs)
     for (int col = tid; col < n; col += PT) {
       double2 x[NB], acc[NB];
@@ -471,62 +502,37 @@ __device__ __forceinline__ unsigned piv_key(double2 v, int t) {
   return (unsigned(bits >> (63 - (32 - KEY_IB))) << KEY_IB) | (KEY_IMASK - unsigned(t));
 }
 
-// Register-resident panel (at most RPT * PT active rows). Thread t owns active-list
-// entries t + i*PT for good: the interchanges only relabel logical row numbers, so
-// the elimination never touches shared memory for its own data. Per column: one
-// barrier, the pivot resolved from the 8 published warp keys, the winning row and
-// its reciprocal read from the winner's warp slot, the update, and the next
-// column's warp keys by REDUX.
+// Shared memory of the register-resident panel LU.
 template <int NB, int RPT>
-__global__ void __launch_bounds__(PT, 1)
-    gj_panel_rows_kernel(const double2* __restrict__ cur0, long long ld, long long bstride, int n, int n_true, int k,
-                         int last, GjScratch S, int* __restrict__ status) {
-  extern __shared__ __align__(16) double2 sv[];  // Vs staging for the tail, NB x (n + 2)
-  __shared__ unsigned cand_k[2][PT / 32];
-  __shared__ double2 cand_r[2][PT / 32];
-  __shared__ __align__(16) double2 cand_row[2][PT / 32][NB];
-  __shared__ double2 s_lu[NB][NB + 1];
-  __shared__ int s_map[RPT * PT];
-  __shared__ int s_act[RPT * PT];
-  __shared__ int s_p[NB];
-  __shared__ double s_red[PT / 32];
-  __shared__ int s_fail;
-  __shared__ double s_tol;
+struct PanelSmem {
+  unsigned cand_k[2][PT / 32];
+  double2 cand_r[2][PT / 32];
+  __align__(16) double2 cand_row[2][PT / 32][NB];
+  double2 lu[NB][NB + 1];  // pivot rows (logical order): L \ U
+  int map[RPT * PT];       // panel-local logical row -> active-list entry
+  int act[RPT * PT];       // active-list entry -> physical row
+  int p[NB];               // interchange partner of step j (logical)
+};
 
+// Tall-panel LU with partial pivoting of register-resident rows (at most RPT * PT).
+// Thread t owns active-list entries t + i*PT for good: the interchanges only relabel
+// logical row numbers, so the elimination never touches shared memory for its own
+// data. Per column: one barrier, the pivot resolved from the 8 published warp keys,
+// the winning row and its reciprocal read from the winner's warp slot, column j+1
+// updated first so its REDUX pivot search overlaps the rest of the update.
+// Ends synchronised with sm.lu / sm.map complete.
+template <int NB, int RPT>
+__device__ __forceinline__ void panel_lu_regs(double2 (&a)[RPT][NB], int rows, PanelSmem<NB, RPT>& sm) {
   const int tid = threadIdx.x, lane = tid & 31, warp = tid >> 5;
-  const int b = blockIdx.x;
-  const double2* __restrict__ cur = cur0 + (long long)b * bstride;
-  const int rows = n - k;
-  ZDBG(0)
-  const int* lmapg = S.lmap + (long long)b * n;
-
-  double2 a[RPT][NB];
   int lg[RPT];
   bool act[RPT];
 #pragma unroll
   for (int i = 0; i < RPT; ++i) {
-    const int t = tid + i * PT;
-    act[i] = t < rows;
-    lg[i] = t;
-    const int ph = act[i] ? active_row(lmapg, k, t) : 0;
-    if (act[i]) s_act[t] = ph;
-#pragma unroll
-    for (int c = 0; c < NB; ++c) a[i][c] = act[i] ? cur[(long long)(k + c) * ld + ph] : make_double2(0.0, 0.0);
+    act[i] = tid + i * PT < rows;
+    lg[i] = tid + i * PT;
   }
-  if (tid == 0) s_fail = INT_MAX;
-  if (k == 0) {
-    const double t = panel_threshold(cur, ld, n_true, s_red);
-    if (tid == 0) {
-      s_tol = t;
-      S.tol[b] = t;
-      status[b] = -1;
-    }
-  } else if (tid == 0) {
-    s_tol = S.tol[b];
-  }
-
-  // This warp's best candidate for column J: its key (lane 0), and from the winning
-  // lane the reciprocal now and the row (c > J) once the row is fully updated.
+  // this warp's best candidate for column J: its key (lane 0), and from the winning
+  // lane the reciprocal now and the row (c > J) once the row is fully updated
   auto publish_key = [&](int par, int J, int& wi) -> bool {
     unsigned key = 0;
     wi = 0;
@@ -540,12 +546,12 @@ __global__ void __launch_bounds__(PT, 1)
         }
       }
     const unsigned wk = __reduce_max_sync(0xffffffffu, key);
-    if (lane == 0) cand_k[par][warp] = wk;
+    if (lane == 0) sm.cand_k[par][warp] = wk;
     const bool win = wk != 0 && key == wk;
     if (win) {
 #pragma unroll
       for (int i = 0; i < RPT; ++i)
-        if (i == wi) cand_r[par][warp] = crcp_fast(a[i][J]);
+        if (i == wi) sm.cand_r[par][warp] = crcp_fast(a[i][J]);
     }
     return win;
   };
@@ -555,40 +561,38 @@ __global__ void __launch_bounds__(PT, 1)
       if (i == wi) {
 #pragma unroll
         for (int c = 0; c < NB; ++c)
-          if (c > J) cand_row[par][warp][c] = a[i][c];
+          if (c > J) sm.cand_row[par][warp][c] = a[i][c];
       }
   };
   {
     int wi;
     if (publish_key(0, 0, wi)) publish_row(0, 0, wi);
   }
-  ZDBG(1)
-
   int prev_t = -1;
 #pragma unroll
   for (int j = 0; j < NB; ++j) {
     const int par = j & 1;
     __syncthreads();
     if (j > 0) {  // deferred relabel of step j-1: the old logical row j-1 takes the partner's number
-      const int pp = s_p[j - 1];
+      const int pp = sm.p[j - 1];
 #pragma unroll
       for (int i = 0; i < RPT; ++i)
         if (lg[i] == j - 1 && tid + i * PT != prev_t) lg[i] = pp;
     }
     unsigned best = 0;
 #pragma unroll
-    for (int q = 0; q < PT / 32; ++q) best = max(best, cand_k[par][q]);
+    for (int q = 0; q < PT / 32; ++q) best = max(best, sm.cand_k[par][q]);
     const int tj = int(KEY_IMASK - (best & KEY_IMASK));
     const int qw = (tj % PT) >> 5;
-    const double2 rcp = cand_r[par][qw];
+    const double2 rcp = sm.cand_r[par][qw];
 #pragma unroll
     for (int i = 0; i < RPT; ++i) {
       if (tid + i * PT == tj) {  // this row becomes logical row j
-        s_p[j] = lg[i];
+        sm.p[j] = lg[i];
         lg[i] = j;
         act[i] = false;
 #pragma unroll
-        for (int c = 0; c < NB; ++c) s_lu[j][c] = a[i][c];
+        for (int c = 0; c < NB; ++c) sm.lu[j][c] = a[i][c];
       }
     }
     double2 l[RPT];
@@ -598,7 +602,7 @@ __global__ void __launch_bounds__(PT, 1)
       if (act[i]) a[i][j] = l[i];
     }
     auto update = [&](int c) {
-      const double2 u = cand_row[par][qw][c];
+      const double2 u = sm.cand_row[par][qw][c];
 #pragma unroll
       for (int i = 0; i < RPT; ++i) {
         double2 x = a[i][c];
@@ -609,7 +613,6 @@ __global__ void __launch_bounds__(PT, 1)
     };
     prev_t = tj;
     if (j + 1 < NB) {
-      // column j+1 first: its pivot search overlaps the rest of the update
       update(j + 1);
       int wi;
       const bool win = publish_key(par ^ 1, j + 1, wi);
@@ -618,19 +621,228 @@ __global__ void __launch_bounds__(PT, 1)
       if (win) publish_row(par ^ 1, j + 1, wi);
     }
   }
-  ZDBG(2)
   __syncthreads();
   {
-    const int pp = s_p[NB - 1];
+    const int pp = sm.p[NB - 1];
 #pragma unroll
     for (int i = 0; i < RPT; ++i) {
       const int t = tid + i * PT;
       if (lg[i] == NB - 1 && t != prev_t) lg[i] = pp;
-      if (t < rows) s_map[lg[i]] = t;
+      if (t < rows) sm.map[lg[i]] = t;
     }
   }
   __syncthreads();
-  panel_tail<NB>(cur, ld, n, n_true, k, b, last != 0, S, status, s_lu, s_map, s_act, s_tol, &s_fail, sv);
+}
+
+// Threshold (k == 0) or the stored one; status reset on the first panel.
+__device__ __forceinline__ void panel_threshold_once(const double2* cur, long long ld, int n_true, int k, int b,
+                                                     const GjScratch& S, int* status, double* red, double* s_tol) {
+  if (k == 0) {
+    const double t = panel_threshold(cur, ld, n_true, red);
+    if (threadIdx.x == 0) {
+      *s_tol = t;
+      S.tol[b] = t;
+      status[b] = -1;
+    }
+  } else if (threadIdx.x == 0) {
+    *s_tol = S.tol[b];
+  }
+}
+
+// One panel (at most RPT * PT active rows): register LU + the shared tail.
+template <int NB, int RPT>
+__global__ void __launch_bounds__(PT, 1)
+    gj_panel_rows_kernel(const double2* __restrict__ cur0, long long ld, long long bstride, int n, int n_true, int k,
+                         int last, GjScratch S, int* __restrict__ status) {
+  extern __shared__ __align__(16) double2 sv[];  // Vs staging for the tail, NB x (n + 2)
+  __shared__ PanelSmem<NB, RPT> sm;
+  __shared__ double s_red[PT / 32];
+  __shared__ int s_fail;
+  __shared__ double s_tol;
+  const int tid = threadIdx.x, b = blockIdx.x;
+  const double2* __restrict__ cur = cur0 + (long long)b * bstride;
+  const int rows = n - k;
+  ZDBG(0)
+  const int* lmapg = S.lmap + (long long)b * n;
+  double2 a[RPT][NB];
+#pragma unroll
+  for (int i = 0; i < RPT; ++i) {
+    const int t = tid + i * PT;
+    const bool ok = t < rows;
+    const int ph = ok ? active_row(lmapg, k, t) : 0;
+    if (ok) sm.act[t] = ph;
+#pragma unroll
+    for (int c = 0; c < NB; ++c) a[i][c] = ok ? cur[(long long)(k + c) * ld + ph] : make_double2(0.0, 0.0);
+  }
+  if (tid == 0) s_fail = INT_MAX;
+  panel_threshold_once(cur, ld, n_true, k, b, S, status, s_red, &s_tol);
+  ZDBG(1)
+  panel_lu_regs<NB, RPT>(a, rows, sm);
+  ZDBG(2)
+  panel_tail<NB>(cur, ld, n, n_true, k, b, last != 0, S, status, sm.lu, sm.map, sm.act, s_tol, &s_fail, sv);
+}
+
+// Two consecutive panels K1 = [k, k+NB), K2 = [k+NB, k+2NB) and ONE rank-2NB update
+// (halves the full-matrix GEMM passes; same pivots and arithmetic as two panels).
+// From the current matrix M, Wz1 = M[:,K1] (-I on P1) and V1 = Pinv1 Vs1:
+//   M2[:,K2]  = M[:,K2] (0 on P1) - Wz1 V1[:,K2]          (panel 2's input, all rows)
+//   Vs2       = M[P2,:] (0 on K1) - Wz1[P2] V1, I on K2    (panel 2's pivot rows)
+//   M <- M (0 on rows P1, P2 and cols K1, K2) - [Wz1 (0 on P2) | Wz2] [V1 (0 on K2); V2]
+// with Wz2 = M2[:,K2] (-I on P2) and V2 = Pinv2 Vs2. Rows <= RPT * PT for both panels.
+template <int NB, int RPT>
+__global__ void __launch_bounds__(PT, 1)
+    gj_pair_kernel(const double2* __restrict__ cur0, long long ld, long long bstride, int n, int n_true, int k,
+                   int last, GjScratch S, int* __restrict__ status) {
+  constexpr int W2 = 2 * NB;
+  extern __shared__ __align__(16) double2 sv[];  // NB x (n + 2): Vs1 / V1, then Vs2 / V2
+  __shared__ PanelSmem<NB, RPT> sm;
+  __shared__ double2 s_pinv[NB][NB + 1];
+  __shared__ double2 s_uinv[NB];
+  __shared__ double2 s_wz1p2[NB][NB + 1];  // Wz1 on the rows P2
+  __shared__ int s_src1[NB], s_src2[NB];
+  __shared__ double s_red[PT / 32];
+  __shared__ int s_fail;
+  __shared__ double s_tol;
+  const int tid = threadIdx.x, b = blockIdx.x;
+  const double2* __restrict__ cur = cur0 + (long long)b * bstride;
+  const int k2 = k + NB, rows1 = n - k, rows2 = n - k2, svld = n + 2;
+  int* __restrict__ lmap = S.lmap + (long long)b * n;
+  int* __restrict__ rowmask = S.rowmask + (long long)b * n;
+  double2* __restrict__ wz = S.wz + (long long)b * n * W2;  // [W2][n], ld n
+  double2* __restrict__ vb = S.vbuf + (long long)b * W2 * n;  // [n][W2], ld W2
+  if (tid == 0) s_fail = INT_MAX;
+
+  // ---------------- panel 1
+  double2 a[RPT][NB];
+#pragma unroll
+  for (int i = 0; i < RPT; ++i) {
+    const int t = tid + i * PT;
+    const bool ok = t < rows1;
+    const int ph = ok ? active_row(lmap, k, t) : 0;
+    if (ok) sm.act[t] = ph;
+#pragma unroll
+    for (int c = 0; c < NB; ++c) a[i][c] = ok ? cur[(long long)(k + c) * ld + ph] : make_double2(0.0, 0.0);
+  }
+  panel_threshold_once(cur, ld, n_true, k, b, S, status, s_red, &s_tol);
+  panel_lu_regs<NB, RPT>(a, rows1, sm);
+  if (tid < NB) {
+    const double2 d = sm.lu[tid][tid];
+    if (k + tid < n_true && hypot(d.x, d.y) <= s_tol) atomicMin(&s_fail, k + tid);  // kernels.hpp:149-158
+    s_uinv[tid] = crcp_fast(d);
+    s_src1[tid] = sm.act[sm.map[tid]];
+  }
+  for (int r = tid; r < rows1; r += PT) lmap[k + r] = sm.act[sm.map[r]];
+  __syncthreads();
+  pivot_block_inverse<NB>(sm.lu, s_uinv, s_pinv);
+  for (int col = tid; col < n; col += PT) {  // Vs1: pivot rows of M, identity on K1
+    const bool kc = col >= k && col < k2;
+    double2 x[NB];
+#pragma unroll
+    for (int j = 0; j < NB; ++j)
+      x[j] = kc ? make_double2(col - k == j ? 1.0 : 0.0, 0.0) : cur[(long long)col * ld + s_src1[j]];
+#pragma unroll
+    for (int j = 0; j < NB; ++j) sv[j * svld + col] = x[j];
+  }
+  __syncthreads();
+  apply_pinv_dmma<NB>(s_pinv, sv, svld, n, nullptr, 0);  // sv = V1
+  __syncthreads();
+  // Wz1 (every row) and panel 2's input M2[:,K2] (every row), one row per thread
+  for (int r = tid; r < n; r += PT) {
+    int j1 = -1;
+#pragma unroll
+    for (int q = 0; q < NB; ++q)
+      if (s_src1[q] == r) j1 = q;
+    double2 w[NB], m2[NB];
+#pragma unroll
+    for (int c = 0; c < NB; ++c) {
+      w[c] = j1 >= 0 ? make_double2(j1 == c ? -1.0 : 0.0, 0.0) : cur[(long long)(k + c) * ld + r];
+      m2[c] = j1 >= 0 ? make_double2(0.0, 0.0) : cur[(long long)(k2 + c) * ld + r];
+    }
+#pragma unroll
+    for (int c = 0; c < NB; ++c) wz[(long long)c * n + r] = w[c];
+#pragma unroll 1
+    for (int q = 0; q < NB; ++q) {
+      double2 wq = w[0];
+#pragma unroll
+      for (int u = 1; u < NB; ++u)
+        if (u == q) wq = w[u];
+      const double2 nq = make_double2(-wq.x, -wq.y);
+#pragma unroll
+      for (int c = 0; c < NB; ++c) m2[c] = cfma(nq, sv[q * svld + k2 + c], m2[c]);
+    }
+#pragma unroll
+    for (int c = 0; c < NB; ++c) wz[(long long)(NB + c) * n + r] = m2[c];
+    rowmask[r] = j1 >= 0 ? -1 : r;
+  }
+  __syncthreads();
+
+  // ---------------- panel 2 on M2[:,K2]
+#pragma unroll
+  for (int i = 0; i < RPT; ++i) {
+    const int t = tid + i * PT;
+    const bool ok = t < rows2;
+    const int ph = ok ? lmap[k2 + t] : 0;
+    if (ok) sm.act[t] = ph;
+#pragma unroll
+    for (int c = 0; c < NB; ++c) a[i][c] = ok ? wz[(long long)(NB + c) * n + ph] : make_double2(0.0, 0.0);
+  }
+  panel_lu_regs<NB, RPT>(a, rows2, sm);
+  if (tid < NB) {
+    const double2 d = sm.lu[tid][tid];
+    if (k2 + tid < n_true && hypot(d.x, d.y) <= s_tol) atomicMin(&s_fail, k2 + tid);
+    s_uinv[tid] = crcp_fast(d);
+    s_src2[tid] = sm.act[sm.map[tid]];
+  }
+  for (int r = tid; r < rows2; r += PT) lmap[k2 + r] = sm.act[sm.map[r]];
+  __syncthreads();
+  for (int e = tid; e < NB * NB; e += PT) s_wz1p2[e / NB][e % NB] = wz[(long long)(e % NB) * n + s_src2[e / NB]];
+  __syncthreads();
+  for (int e = tid; e < NB * NB; e += PT) {  // rows P2: 0 in Wz1, -I in Wz2, 0 in C
+    const int j = e / NB, c = e % NB;
+    wz[(long long)c * n + s_src2[j]] = make_double2(0.0, 0.0);
+    wz[(long long)(NB + c) * n + s_src2[j]] = make_double2(j == c ? -1.0 : 0.0, 0.0);
+    if (c == 0) rowmask[s_src2[j]] = -1;
+  }
+  pivot_block_inverse<NB>(sm.lu, s_uinv, s_pinv);
+  // per column: V1 (0 on K2) -> vb rows 0..NB-1; Vs2 replaces V1 in sv
+  for (int col = tid; col < n; col += PT) {
+    double2 v1[NB], x[NB];
+    const bool c1 = col >= k && col < k2, c2 = col >= k2 && col < k2 + NB;
+#pragma unroll
+    for (int j = 0; j < NB; ++j) {
+      v1[j] = sv[j * svld + col];
+      vb[(long long)col * W2 + j] = c2 ? make_double2(0.0, 0.0) : v1[j];
+      x[j] = c2 ? make_double2(col - k2 == j ? 1.0 : 0.0, 0.0)
+                : (c1 ? make_double2(0.0, 0.0) : cur[(long long)col * ld + s_src2[j]]);
+    }
+    if (!c2) {
+#pragma unroll 1
+      for (int q = 0; q < NB; ++q) {
+        double2 vq = v1[0];
+#pragma unroll
+        for (int u = 1; u < NB; ++u)
+          if (u == q) vq = v1[u];
+        const double2 nq = make_double2(-vq.x, -vq.y);
+#pragma unroll
+        for (int j = 0; j < NB; ++j) x[j] = cfma(s_wz1p2[j][q], nq, x[j]);
+      }
+    }
+#pragma unroll
+    for (int j = 0; j < NB; ++j) sv[j * svld + col] = x[j];
+  }
+  __syncthreads();
+  apply_pinv_dmma<NB>(s_pinv, sv, svld, n, vb + NB, W2);  // V2 -> vb rows NB..2NB-1
+  if (last) {  // output scatters: row lmap[i] -> i, column c -> lmap[c]
+    int* __restrict__ rowscat = S.rowscat + (long long)b * n;
+    int* __restrict__ colmap = S.colmap + (long long)b * n;
+    for (int i = tid; i < n; i += PT) {
+      const int p = lmap[i];
+      rowscat[p] = i;
+      colmap[i] = p;
+    }
+  }
+  __syncthreads();
+  if (tid == 0 && s_fail != INT_MAX && status[b] < 0) status[b] = s_fail;
 }
 
 }  // namespace
@@ -660,40 +872,45 @@ cudaError_t zinv_batched(double2* M, long long ld, long long bstride, int n, int
   const size_t rows_smem = size_t(nb) * (n + 2) * sizeof(double2);  // Vs staging of the tail
   static size_t attr_rows = 0;
   if (rows_smem > attr_rows) {
-    const void* fns[2] = {(const void*)gj_panel_rows_kernel<kNB, 1>, (const void*)gj_panel_rows_kernel<kNB, 2>};
+    const void* fns[4] = {(const void*)gj_panel_rows_kernel<kNB, 1>, (const void*)gj_panel_rows_kernel<kNB, 2>,
+                          (const void*)gj_pair_kernel<kNB, 1>, (const void*)gj_pair_kernel<kNB, 2>};
     for (const void* f : fns)
       if ((e = cudaFuncSetAttribute(f, cudaFuncAttributeMaxDynamicSharedMemorySize, int(rows_smem)))) return e;
     attr_rows = rows_smem;
   }
   const long long nn = (long long)n * n;
-  const int npan = n / nb;
-  for (int pi = 0; pi < npan; ++pi) {
-    const int k = pi * nb;
-    const int last = pi == npan - 1;
-    // panel 0 reads the input block; the working matrix s0 is updated in place
-    const double2* cur = pi == 0 ? M : S.s0;
-    const long long cld = pi == 0 ? ld : n, cbs = pi == 0 ? bstride : nn;
+  // panel steps: two panels per step (pair kernel, one rank-2nb GEMM) wherever both
+  // fit the register kernel; single panels otherwise (tall panels, BBSI_PANEL=2/3)
+  const int kind = panel_kind();
+  for (int k = 0; k < n;) {
+    const int rows = n - k;
+    const bool pair = kind == 1 && rows <= 2 * PT && k + 2 * nb <= n;
+    const int kw = pair ? 2 * nb : nb;
+    const int last = k + kw == n;
+    // the first step reads the input block; the working matrix s0 is updated in place
+    const double2* cur = k == 0 ? M : S.s0;
+    const long long cld = k == 0 ? ld : n, cbs = k == 0 ? bstride : nn;
     double2* nxt = last ? M : S.s0;
     const long long nld = last ? ld : n, nbs = last ? bstride : nn;
     {
-      ProfScope prof(stream, PROF_INV, 8.0 * double(n) * nb * nb * batch, 16.0 * (3.0 * n * nb) * batch);
+      ProfScope prof(stream, PROF_INV, 8.0 * double(n) * nb * kw * batch, 16.0 * (3.0 * n * kw) * batch);
       cudaLaunchConfig_t cfg{};
       cfg.gridDim = dim3(batch);
       cfg.blockDim = dim3(PT);
-      cfg.dynamicSmemBytes = 0;
+      cfg.dynamicSmemBytes = rows_smem;
       cfg.stream = stream;
       cudaLaunchAttribute attr_[1];
       attr_[0].id = cudaLaunchAttributePriority;
       attr_[0].val.priority = panel_priority();
       cfg.attrs = attr_;
       cfg.numAttrs = 1;
-      const int rows = n - k;
-      const int kind = panel_kind();
-      if (kind == 1 && rows <= PT) {
-        cfg.dynamicSmemBytes = rows_smem;
+      if (pair && rows <= PT) {
+        e = cudaLaunchKernelEx(&cfg, gj_pair_kernel<kNB, 1>, cur, cld, cbs, n, n_true, k, last, S, status);
+      } else if (pair) {
+        e = cudaLaunchKernelEx(&cfg, gj_pair_kernel<kNB, 2>, cur, cld, cbs, n, n_true, k, last, S, status);
+      } else if (kind != 2 && rows <= PT) {
         e = cudaLaunchKernelEx(&cfg, gj_panel_rows_kernel<kNB, 1>, cur, cld, cbs, n, n_true, k, last, S, status);
-      } else if (kind == 1 && rows <= 2 * PT) {
-        cfg.dynamicSmemBytes = rows_smem;
+      } else if (kind != 2 && rows <= 2 * PT) {
         e = cudaLaunchKernelEx(&cfg, gj_panel_rows_kernel<kNB, 2>, cur, cld, cbs, n, n_true, k, last, S, status);
       } else {
         cfg.dynamicSmemBytes = smem;
@@ -705,16 +922,17 @@ cudaError_t zinv_batched(double2* M, long long ld, long long bstride, int n, int
     g.batch = batch;
     g.bs = 64;
     g.nprob = 1;
+    g.prof_cat = PROF_GJ_GEMM;
     // M <- M (0 on the pivot rows and the panel columns) - Wz V
     ZGemmProblem& p = g.prob[0];
     p = ZGemmProblem{};
     p.M = n;
     p.N = n;
-    p.K = nb;
+    p.K = kw;
     p.alpha = make_double2(-1.0, 0.0);
     p.beta = make_double2(1.0, 0.0);
-    p.A = ZOp{S.wz, n, 64, 64LL * n, (long long)n * nb};
-    p.B = ZOp{S.vbuf, nb, 64, 64LL * nb, (long long)nb * n};
+    p.A = ZOp{S.wz, n, 64, 64LL * n, (long long)n * kw};
+    p.B = ZOp{S.vbuf, kw, 64, 64LL * kw, (long long)kw * n};
     p.C = ZOp{cur, cld, 64, 64LL * cld, cbs};
     p.D = ZOp{nxt, nld, 64, 64LL * nld, nbs};
     p.rowmap = S.rowmask;
@@ -723,8 +941,9 @@ cudaError_t zinv_batched(double2* M, long long ld, long long bstride, int n, int
     p.map_bstride = n;
     p.zr0 = p.zr1 = 0;
     p.zc0 = k;
-    p.zc1 = k + nb;
+    p.zc1 = k + kw;
     if ((e = zgemm_grouped(g, stream))) return e;
+    k += kw;
   }
   return cudaSuccess;
 }
