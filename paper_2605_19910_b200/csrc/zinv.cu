@@ -705,105 +705,96 @@ __global__ void __launch_bounds__(PT, 1)
   __shared__ double s_tol;
   const int tid = threadIdx.x, b = blockIdx.x;
   const double2* __restrict__ cur = cur0 + (long long)b * bstride;
-  const int k2 = k + NB, rows1 = n - k, rows2 = n - k2, svld = n + 2;
+  const int k2 = k + NB, svld = n + 2;
   int* __restrict__ lmap = S.lmap + (long long)b * n;
   int* __restrict__ rowmask = S.rowmask + (long long)b * n;
   double2* __restrict__ wz = S.wz + (long long)b * n * W2;  // [W2][n], ld n
   double2* __restrict__ vb = S.vbuf + (long long)b * W2 * n;  // [n][W2], ld W2
   if (tid == 0) s_fail = INT_MAX;
 
-  // ---------------- panel 1
-  double2 a[RPT][NB];
-#pragma unroll
-  for (int i = 0; i < RPT; ++i) {
-    const int t = tid + i * PT;
-    const bool ok = t < rows1;
-    const int ph = ok ? active_row(lmap, k, t) : 0;
-    if (ok) sm.act[t] = ph;
-#pragma unroll
-    for (int c = 0; c < NB; ++c) a[i][c] = ok ? cur[(long long)(k + c) * ld + ph] : make_double2(0.0, 0.0);
-  }
-  panel_threshold_once(cur, ld, n_true, k, b, S, status, s_red, &s_tol);
-  panel_lu_regs<NB, RPT>(a, rows1, sm);
-  if (tid < NB) {
-    const double2 d = sm.lu[tid][tid];
-    if (k + tid < n_true && hypot(d.x, d.y) <= s_tol) atomicMin(&s_fail, k + tid);  // kernels.hpp:149-158
-    s_uinv[tid] = crcp_fast(d);
-    s_src1[tid] = sm.act[sm.map[tid]];
-  }
-  for (int r = tid; r < rows1; r += PT) lmap[k + r] = sm.act[sm.map[r]];
-  __syncthreads();
-  pivot_block_inverse<NB>(sm.lu, s_uinv, s_pinv);
-  for (int col = tid; col < n; col += PT) {  // Vs1: pivot rows of M, identity on K1
-    const bool kc = col >= k && col < k2;
-    double2 x[NB];
-#pragma unroll
-    for (int j = 0; j < NB; ++j)
-      x[j] = kc ? make_double2(col - k == j ? 1.0 : 0.0, 0.0) : cur[(long long)col * ld + s_src1[j]];
-#pragma unroll
-    for (int j = 0; j < NB; ++j) sv[j * svld + col] = x[j];
-  }
-  __syncthreads();
-  apply_pinv_dmma<NB>(s_pinv, sv, svld, n, nullptr, 0);  // sv = V1
-  __syncthreads();
-  // Wz1 (every row) and panel 2's input M2[:,K2] (every row), one row per thread
-  for (int r = tid; r < n; r += PT) {
-    int j1 = -1;
-#pragma unroll
-    for (int q = 0; q < NB; ++q)
-      if (s_src1[q] == r) j1 = q;
-    double2 w[NB], m2[NB];
-#pragma unroll
-    for (int c = 0; c < NB; ++c) {
-      w[c] = j1 >= 0 ? make_double2(j1 == c ? -1.0 : 0.0, 0.0) : cur[(long long)(k + c) * ld + r];
-      m2[c] = j1 >= 0 ? make_double2(0.0, 0.0) : cur[(long long)(k2 + c) * ld + r];
-    }
-#pragma unroll
-    for (int c = 0; c < NB; ++c) wz[(long long)c * n + r] = w[c];
+  // Both panels run through the same loop body (one copy of the unrolled elimination
+  // in the binary: the kernel executes its code once per SM, so code size is time).
 #pragma unroll 1
-    for (int q = 0; q < NB; ++q) {
-      double2 wq = w[0];
+  for (int ph = 0; ph < 2; ++ph) {
+    const int kk = ph ? k2 : k, rows = n - kk;
+    int* s_src = ph ? s_src2 : s_src1;
+    // panel 1 reads M[:,K1]; panel 2 reads its input M2[:,K2], computed into wz[NB..2NB)
+    const double2* src = ph ? wz + (long long)NB * n : cur + (long long)k * ld;
+    const long long sld = ph ? n : ld;
+    double2 a[RPT][NB];
 #pragma unroll
-      for (int u = 1; u < NB; ++u)
-        if (u == q) wq = w[u];
-      const double2 nq = make_double2(-wq.x, -wq.y);
+    for (int i = 0; i < RPT; ++i) {
+      const int t = tid + i * PT;
+      const bool ok = t < rows;
+      const int phys = ok ? active_row(lmap, kk, t) : 0;
+      if (ok) sm.act[t] = phys;
 #pragma unroll
-      for (int c = 0; c < NB; ++c) m2[c] = cfma(nq, sv[q * svld + k2 + c], m2[c]);
+      for (int c = 0; c < NB; ++c) a[i][c] = ok ? src[(long long)c * sld + phys] : make_double2(0.0, 0.0);
     }
+    if (ph == 0) panel_threshold_once(cur, ld, n_true, k, b, S, status, s_red, &s_tol);
+    panel_lu_regs<NB, RPT>(a, rows, sm);
+    if (tid < NB) {
+      const double2 d = sm.lu[tid][tid];
+      if (kk + tid < n_true && hypot(d.x, d.y) <= s_tol) atomicMin(&s_fail, kk + tid);  // kernels.hpp:149-158
+      s_uinv[tid] = crcp_fast(d);
+      s_src[tid] = sm.act[sm.map[tid]];
+    }
+    for (int r = tid; r < rows; r += PT) lmap[kk + r] = sm.act[sm.map[r]];
+    __syncthreads();
+    if (ph == 1) {
+      for (int e = tid; e < NB * NB; e += PT) s_wz1p2[e / NB][e % NB] = wz[(long long)(e % NB) * n + s_src2[e / NB]];
+      __syncthreads();
+      for (int e = tid; e < NB * NB; e += PT) {  // rows P2: 0 in Wz1, -I in Wz2, 0 in C
+        const int j = e / NB, c = e % NB;
+        wz[(long long)c * n + s_src2[j]] = make_double2(0.0, 0.0);
+        wz[(long long)(NB + c) * n + s_src2[j]] = make_double2(j == c ? -1.0 : 0.0, 0.0);
+        if (c == 0) rowmask[s_src2[j]] = -1;
+      }
+    }
+    pivot_block_inverse<NB>(sm.lu, s_uinv, s_pinv);
+    if (ph == 1) break;
+    for (int col = tid; col < n; col += PT) {  // Vs1: pivot rows of M, identity on K1
+      const bool kc = col >= k && col < k2;
+      double2 x[NB];
 #pragma unroll
-    for (int c = 0; c < NB; ++c) wz[(long long)(NB + c) * n + r] = m2[c];
-    rowmask[r] = j1 >= 0 ? -1 : r;
-  }
-  __syncthreads();
-
-  // ---------------- panel 2 on M2[:,K2]
+      for (int j = 0; j < NB; ++j)
+        x[j] = kc ? make_double2(col - k == j ? 1.0 : 0.0, 0.0) : cur[(long long)col * ld + s_src1[j]];
 #pragma unroll
-  for (int i = 0; i < RPT; ++i) {
-    const int t = tid + i * PT;
-    const bool ok = t < rows2;
-    const int ph = ok ? lmap[k2 + t] : 0;
-    if (ok) sm.act[t] = ph;
+      for (int j = 0; j < NB; ++j) sv[j * svld + col] = x[j];
+    }
+    __syncthreads();
+    apply_pinv_dmma<NB>(s_pinv, sv, svld, n, nullptr, 0);  // sv = V1
+    __syncthreads();
+    // Wz1 (every row) and panel 2's input M2[:,K2] (every row), one row per thread
+    for (int r = tid; r < n; r += PT) {
+      int j1 = -1;
 #pragma unroll
-    for (int c = 0; c < NB; ++c) a[i][c] = ok ? wz[(long long)(NB + c) * n + ph] : make_double2(0.0, 0.0);
+      for (int q = 0; q < NB; ++q)
+        if (s_src1[q] == r) j1 = q;
+      double2 w[NB], m2[NB];
+#pragma unroll
+      for (int c = 0; c < NB; ++c) {
+        w[c] = j1 >= 0 ? make_double2(j1 == c ? -1.0 : 0.0, 0.0) : cur[(long long)(k + c) * ld + r];
+        m2[c] = j1 >= 0 ? make_double2(0.0, 0.0) : cur[(long long)(k2 + c) * ld + r];
+      }
+#pragma unroll
+      for (int c = 0; c < NB; ++c) wz[(long long)c * n + r] = w[c];
+#pragma unroll 1
+      for (int q = 0; q < NB; ++q) {
+        double2 wq = w[0];
+#pragma unroll
+        for (int u = 1; u < NB; ++u)
+          if (u == q) wq = w[u];
+        const double2 nq = make_double2(-wq.x, -wq.y);
+#pragma unroll
+        for (int c = 0; c < NB; ++c) m2[c] = cfma(nq, sv[q * svld + k2 + c], m2[c]);
+      }
+#pragma unroll
+      for (int c = 0; c < NB; ++c) wz[(long long)(NB + c) * n + r] = m2[c];
+      rowmask[r] = j1 >= 0 ? -1 : r;
+    }
+    __syncthreads();
   }
-  panel_lu_regs<NB, RPT>(a, rows2, sm);
-  if (tid < NB) {
-    const double2 d = sm.lu[tid][tid];
-    if (k2 + tid < n_true && hypot(d.x, d.y) <= s_tol) atomicMin(&s_fail, k2 + tid);
-    s_uinv[tid] = crcp_fast(d);
-    s_src2[tid] = sm.act[sm.map[tid]];
-  }
-  for (int r = tid; r < rows2; r += PT) lmap[k2 + r] = sm.act[sm.map[r]];
-  __syncthreads();
-  for (int e = tid; e < NB * NB; e += PT) s_wz1p2[e / NB][e % NB] = wz[(long long)(e % NB) * n + s_src2[e / NB]];
-  __syncthreads();
-  for (int e = tid; e < NB * NB; e += PT) {  // rows P2: 0 in Wz1, -I in Wz2, 0 in C
-    const int j = e / NB, c = e % NB;
-    wz[(long long)c * n + s_src2[j]] = make_double2(0.0, 0.0);
-    wz[(long long)(NB + c) * n + s_src2[j]] = make_double2(j == c ? -1.0 : 0.0, 0.0);
-    if (c == 0) rowmask[s_src2[j]] = -1;
-  }
-  pivot_block_inverse<NB>(sm.lu, s_uinv, s_pinv);
   // per column: V1 (0 on K2) -> vb rows 0..NB-1; Vs2 replaces V1 in sv
   for (int col = tid; col < n; col += PT) {
     double2 v1[NB], x[NB];
