@@ -373,9 +373,14 @@ int bbsi_cuda_dyson_rgf_dev(int l, int w, int bs, int n_energy, const double* dH
   std::vector<int> nt(l, bs), fails;
   const std::string key = graph_key("dyson", {l, w, bs, n_energy, (long long)dH, (long long)dG, (long long)dzs,
                                               (long long)scratch, W.groups});
+  // tridiagonal: the sweeps read A's off-diagonal blocks (-H) from the shared H, so only
+  // the diagonal blocks of each energy's band are formed
+  if (w == 1) W.Hoff = reinterpret_cast<const double2*>(dH);
   CK(run_graphed(key, s, [&](cudaStream_t st) -> cudaError_t {
-    cudaError_t e = dyson_form_band(reinterpret_cast<double2*>(dG), reinterpret_cast<const double2*>(dH), l, w, bs,
-                                    n_energy, dzs, dzs + n_energy, st);
+    double2* g = reinterpret_cast<double2*>(dG);
+    const double2* h = reinterpret_cast<const double2*>(dH);
+    cudaError_t e = W.Hoff ? dyson_form_diag(g, h, l, w, bs, n_energy, dzs, dzs + n_energy, st)
+                           : dyson_form_band(g, h, l, w, bs, n_energy, dzs, dzs + n_energy, st);
     return e ? e : rgf_sweeps(W, nt.data(), st);
   }));
   CK(collect_failures(W, fails, s));
@@ -530,7 +535,10 @@ int bbsi_cuda_dyson_rgf_z(int l, int w, int bs, int n_energy, const double* H, c
       const int e0 = c * chunk, ne = std::min(chunk, n_energy - e0), buf = c % nbuf;
       if (c >= nbuf) CK(cudaStreamWaitEvent(sc, freed[buf], 0));
       double2* g = dG + size_t(buf) * chunk * band;
-      CK(dyson_form_band(g, dH, l, w, bs, ne, dzs + e0, dzs + n_energy, sc));
+      if (w == 1)
+        CK(dyson_form_diag(g, dH, l, w, bs, ne, dzs + e0, dzs + n_energy, sc));
+      else
+        CK(dyson_form_band(g, dH, l, w, bs, ne, dzs + e0, dzs + n_energy, sc));
       SweepWork W;
       W.l = l;
       W.w = w;
@@ -539,6 +547,7 @@ int bbsi_cuda_dyson_rgf_z(int l, int w, int bs, int n_energy, const double* H, c
       W.G = g;
       W.g_bstride = band;
       W.groups = groups;
+      if (w == 1) W.Hoff = dH;
       sweep_carve(W, scratch);
       // finished band rows of the downward sweep -> host, on the copy stream, while the
       // sweep continues (one 2D copy per hand-off: rows [r0, r1) of ne_g energies)

@@ -21,6 +21,10 @@ cudaError_t zinv_batched(double2* M, long long ld, long long bstride, int n, int
                          int* status, cudaStream_t stream);
 size_t zinv_scratch_bytes(int n, int batch);
 cudaError_t dyson_fill_h(double2* H, int l, int w, int b, uint64_t seed, cudaStream_t s);
+// Diagonal blocks only (A_aa = z I - H_aa - sigma_a I) plus zeroed out-of-range slots,
+// for sweeps that read the off-diagonal blocks from H (SweepWork::Hoff).
+cudaError_t dyson_form_diag(double2* G, const double2* H, int l, int w, int bs, int batch, const double2* z,
+                            const double2* sigma, cudaStream_t s);
 cudaError_t dyson_form_band(double2* G, const double2* H, int l, int w, int bs, int batch, const double2* z,
                             const double2* sigma, cudaStream_t s);
 
@@ -48,6 +52,10 @@ struct SweepWork {
   std::function<cudaError_t(int r0, int r1, int e0, int ne, cudaStream_t s)> rows_done;
   int hook_rows = 8;
   int e_off = 0;          // batch offset of this (group's) sub-batch, for rows_done
+  // Optional (w == 1 only): energy-independent band H with A's off-diagonal blocks
+  // = -H (Dyson batches). The sweeps then read those operands from H, shared by the
+  // whole batch, and G's off-diagonal slots need not hold A (see dyson_form_diag).
+  const double2* Hoff = nullptr;
 };
 
 // Bytes of LM+UM+piv+wz+status for a sweep.

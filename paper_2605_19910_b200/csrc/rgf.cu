@@ -71,6 +71,8 @@ struct Ctx {
   ZOp gop(const double2* p, long long rs_slots, long long cs_slots) const {
     return ZOp{p, W.bs, rs_slots * bb, cs_slots * bb, W.g_bstride};
   }
+  // block (a, off) of the shared H band (bstride 0: every batch entry reads the same block)
+  ZOp hop(int a, int off) const { return ZOp{W.Hoff + ((long long)a * nslot + off + W.w) * bb, W.bs, 0, 0, 0}; }
   ZOp mop(const double2* p, long long rs_blocks, long long cs_blocks) const {
     return ZOp{p, W.bs, rs_blocks * bb, cs_blocks * bb, lm_bstride()};
   }
@@ -118,12 +120,16 @@ cudaError_t rgf_sweeps_one(const SweepWork& W, const int* n_true, int* status, i
     if ((e = inv(j)) != cudaSuccess) return e;
     const ZOp X = c.gop(c.slot(j, 0), 0, 0);
     // lm[j] = X_j [M'(j,j-1) .. M'(j,j-k)]
-    ZGemmProblem p_lm = prob(b, k * b, b, 1.0, 0.0, X, c.gop(c.slot(j, -1), 0, -1), c.mop(c.lm(j), 0, 1));
+    // (tridiagonal Dyson batch: M'(j,j-1) = -H(j,j-1) is never modified, read from H)
+    const bool hs = W.Hoff && w == 1;
+    const double sg = hs ? -1.0 : 1.0;
+    ZGemmProblem p_lm = prob(b, k * b, b, sg, 0.0, X, hs ? c.hop(j, -1) : c.gop(c.slot(j, -1), 0, -1),
+                             c.mop(c.lm(j), 0, 1));
     if ((e = launch(W, {p_lm}, s)) != cudaSuccess) return e;
     // window M'(j-s, j-t) -= M'(j-s, j) lm[j][t];  um[j] = [M'(j-t, j)]_t X_j
-    ZOp upper = c.gop(c.slot(j - 1, +1), -two_w, 0);
-    ZGemmProblem p_win = prob(k * b, k * b, b, -1.0, 1.0, upper, c.mop(c.lm(j), 0, 1), c.gop(c.slot(j - 1, 0), -two_w, -1));
-    ZGemmProblem p_um = prob(k * b, b, b, 1.0, 0.0, upper, X, c.mop(c.um(j), 1, 0));
+    ZOp upper = hs ? c.hop(j - 1, +1) : c.gop(c.slot(j - 1, +1), -two_w, 0);
+    ZGemmProblem p_win = prob(k * b, k * b, b, -sg, 1.0, upper, c.mop(c.lm(j), 0, 1), c.gop(c.slot(j - 1, 0), -two_w, -1));
+    ZGemmProblem p_um = prob(k * b, b, b, sg, 0.0, upper, X, c.mop(c.um(j), 1, 0));
     if ((e = launch(W, {p_win, p_um}, s)) != cudaSuccess) return e;
   }
   if ((e = inv(0)) != cudaSuccess) return e;
