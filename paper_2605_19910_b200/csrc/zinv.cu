@@ -711,6 +711,7 @@ __global__ void __launch_bounds__(PT, 1)
   double2* __restrict__ wz = S.wz + (long long)b * n * W2;  // [W2][n], ld n
   double2* __restrict__ vb = S.vbuf + (long long)b * W2 * n;  // [n][W2], ld W2
   if (tid == 0) s_fail = INT_MAX;
+  ZDBG(10)
 
   // Both panels run through the same loop body (one copy of the unrolled elimination
   // in the binary: the kernel executes its code once per SM, so code size is time).
@@ -732,7 +733,9 @@ __global__ void __launch_bounds__(PT, 1)
       for (int c = 0; c < NB; ++c) a[i][c] = ok ? src[(long long)c * sld + phys] : make_double2(0.0, 0.0);
     }
     if (ph == 0) panel_threshold_once(cur, ld, n_true, k, b, S, status, s_red, &s_tol);
+    ZDBG(11 + 10 * ph)
     panel_lu_regs<NB, RPT>(a, rows, sm);
+    ZDBG(12 + 10 * ph)
     if (tid < NB) {
       const double2 d = sm.lu[tid][tid];
       if (kk + tid < n_true && hypot(d.x, d.y) <= s_tol) atomicMin(&s_fail, kk + tid);  // kernels.hpp:149-158
@@ -741,6 +744,7 @@ __global__ void __launch_bounds__(PT, 1)
     }
     for (int r = tid; r < rows; r += PT) lmap[kk + r] = sm.act[sm.map[r]];
     __syncthreads();
+    ZDBG(13 + 10 * ph)
     if (ph == 1) {
       for (int e = tid; e < NB * NB; e += PT) s_wz1p2[e / NB][e % NB] = wz[(long long)(e % NB) * n + s_src2[e / NB]];
       __syncthreads();
@@ -751,7 +755,9 @@ __global__ void __launch_bounds__(PT, 1)
         if (c == 0) rowmask[s_src2[j]] = -1;
       }
     }
+    ZDBG(14 + 10 * ph)
     pivot_block_inverse<NB>(sm.lu, s_uinv, s_pinv);
+    ZDBG(15 + 10 * ph)
     if (ph == 1) break;
     for (int col = tid; col < n; col += PT) {  // Vs1: pivot rows of M, identity on K1
       const bool kc = col >= k && col < k2;
@@ -763,8 +769,10 @@ __global__ void __launch_bounds__(PT, 1)
       for (int j = 0; j < NB; ++j) sv[j * svld + col] = x[j];
     }
     __syncthreads();
+    ZDBG(16)
     apply_pinv_dmma<NB>(s_pinv, sv, svld, n, nullptr, 0);  // sv = V1
     __syncthreads();
+    ZDBG(17)
     // Wz1 (every row) and panel 2's input M2[:,K2] (every row), one row per thread
     for (int r = tid; r < n; r += PT) {
       int j1 = -1;
@@ -794,6 +802,7 @@ __global__ void __launch_bounds__(PT, 1)
       rowmask[r] = j1 >= 0 ? -1 : r;
     }
     __syncthreads();
+    ZDBG(18)
   }
   // per column: V1 (0 on K2) -> vb rows 0..NB-1; Vs2 replaces V1 in sv
   for (int col = tid; col < n; col += PT) {
@@ -822,7 +831,9 @@ __global__ void __launch_bounds__(PT, 1)
     for (int j = 0; j < NB; ++j) sv[j * svld + col] = x[j];
   }
   __syncthreads();
+  ZDBG(26)
   apply_pinv_dmma<NB>(s_pinv, sv, svld, n, vb + NB, W2);  // V2 -> vb rows NB..2NB-1
+  ZDBG(27)
   if (last) {  // output scatters: row lmap[i] -> i, column c -> lmap[c]
     int* __restrict__ rowscat = S.rowscat + (long long)b * n;
     int* __restrict__ colmap = S.colmap + (long long)b * n;
@@ -834,6 +845,7 @@ __global__ void __launch_bounds__(PT, 1)
   }
   __syncthreads();
   if (tid == 0 && s_fail != INT_MAX && status[b] < 0) status[b] = s_fail;
+  ZDBG(28)
 }
 
 }  // namespace

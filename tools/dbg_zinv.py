@@ -1,4 +1,4 @@
-"""Phase timing of one GJ panel (matrix 0, panel k = 32) from clock64 marks.
+"""Phase timing of one Gauss-Jordan step (matrix 0, step k = 32) from clock64 marks.
 
 Needs the instrumented library: python paper_2605_19910_b200/build.py --debug-zinv, then
 BBSI_LIB=paper_2605_19910_b200/_lib/libbbsi_cuda_dbg.so python tools/dbg_zinv.py
@@ -14,7 +14,10 @@ import torch  # noqa: E402
 from paper_2605_19910_b200 import dyson as D  # noqa: E402
 from paper_2605_19910_b200._native import lib  # noqa: E402
 
-NAMES = ["load+tol", "LU loop", "lmap", "Wz+barrier", "Vs prefetch+fix", "Pinv", "Vs stage", "V dmma", "scatter+end"]
+PAIR = [(10, 11, "load"), (11, 12, "LU1"), (12, 13, "lmap1"), (13, 14, "-"), (14, 15, "Pinv1"),
+        (15, 16, "Vs1 stage"), (16, 17, "V1 dmma"), (17, 18, "Wz1 + M2"), (18, 21, "load2"), (21, 22, "LU2"),
+        (22, 23, "lmap2"), (23, 24, "Wz fixes"), (24, 25, "Pinv2"), (25, 26, "Vs2"), (26, 27, "V2 dmma"),
+        (27, 28, "end")]
 cfg = D.scaled(D.CONFIGS[2], num_layers=4, n_energy=64)
 l, w, b = cfg.num_layers, cfg.bandwidth, cfg.block_size
 H = torch.empty((l, 3, b, b), dtype=torch.complex128, device='cuda')
@@ -25,6 +28,5 @@ for rep in range(3):
     torch.cuda.synchronize()
     out = np.zeros(64, dtype=np.int64)
     lib().bbsi_debug_zinv(out.ctypes.data_as(C.c_void_p))
-    t = out[:10]
-    d = np.diff(t)
-    print("total", t[9] - t[0], "cycles |", " ".join(f"{n}={v}" for n, v in zip(NAMES, d)))
+    print("pair step total", out[28] - out[10], "cycles |",
+          " ".join(f"{name}={out[b_] - out[a_]}" for a_, b_, name in PAIR if name != "-"))
