@@ -136,6 +136,11 @@ int bbsi_cuda_dyson_ddrgf_dev(int l, int bs, const double* dH, const double* z, 
 int bbsi_cuda_dyson_fill_h_dev(int l, int w, int b, uint64_t seed, double* dH, void* stream);
 /* Same bytes on the host (for the end-to-end path and the parity tests). */
 void bbsi_dyson_fill_h_host(int l, int w, int b, uint64_t seed, double* H);
+/* random_spd_like<std::complex<double>> (block_banded.hpp:99-133, raw mt19937_64 bits,
+ * block_banded.hpp:70-91) into slot memory (l x (2w+1) slots of bs x bs column-major,
+ * bs = max block size; out-of-band slots zero). Host only; used by the CLI's generated
+ * inputs. Returns BBSI_INVALID_ARGUMENT for a bad layout or dominance <= 0. */
+int bbsi_random_spd_like_z(int l, int w, int bs, const int* sizes, uint64_t seed, double dominance, double* A);
 
 /* ---------------------------------------------------------------- kernel-level API (device pointers)
  * Batched C = alpha*A*B + beta*C on plain column-major complex128 matrices,

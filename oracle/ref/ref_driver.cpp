@@ -14,6 +14,7 @@
 
 #include "bbsi/cost_model.hpp"
 #include "bbsi/ddrgf.hpp"
+#include "bbsi/io.hpp"
 #include "bbsi/rgf.hpp"
 #include "bbsi/threading.hpp"
 #include "helpers.hpp"  // reference tests/helpers.hpp: random_hermitian
@@ -111,6 +112,28 @@ int ref_random_spd_like(int l, int w, int bs, const int* sizes, uint64_t seed, d
     return guarded(nullptr, [&] {
         auto m = random_spd_like<cd>(layout_of(l, w, bs, sizes), seed, dominance);
         to_slots(m, bs, A);
+    });
+}
+
+// .bbm files through the reference's own io.cpp (write_bbm / read_bbm).
+int ref_write_bbm(const char* path, int l, int w, int bs, const int* sizes, const double* A) {
+    return guarded(nullptr, [&] { write_bbm(path, from_slots(layout_of(l, w, bs, sizes), bs, A)); });
+}
+
+// Reads a .bbm file: dims[0..2] = (num_layers, bandwidth, max block size); with A null
+// only the dims (and sizes, when non-null and large enough) are filled.
+int ref_read_bbm(const char* path, int* dims, int* sizes, int max_layers, double* A) {
+    return guarded(nullptr, [&] {
+        auto m = read_bbm(path);
+        const auto& lay = m.layout();
+        int bs = 0;
+        for (int b : lay.block_sizes) bs = b > bs ? b : bs;
+        dims[0] = lay.num_layers;
+        dims[1] = lay.bandwidth;
+        dims[2] = bs;
+        if (sizes && max_layers >= lay.num_layers)
+            for (int a = 0; a < lay.num_layers; ++a) sizes[a] = lay.block_sizes[a];
+        if (A) to_slots(m, bs, A);
     });
 }
 

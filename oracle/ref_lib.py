@@ -172,3 +172,22 @@ def predict_ddrgf_counters(l, s2_levels):
     rc = lib().ref_predict_ddrgf_counters(C.c_longlong(l), _p(s2), len(s2), _p(out))
     _check(rc, C.c_int(-1))
     return O.KernelCounters(*map(int, out))
+
+
+def write_bbm(path: str, m: O.Band):
+    """bbsi::write_bbm (io.cpp:26-45) of the compiled reference."""
+    lay = m.layout
+    mem = to_slots(m)
+    rc = lib().ref_write_bbm(str(path).encode(), lay.num_layers, lay.bandwidth, lay.bs, _p(_sizes(lay)), _p(mem))
+    _check(rc, C.c_int(-1))
+
+
+def read_bbm(path: str) -> O.Band:
+    """bbsi::read_bbm (io.cpp:47-73) of the compiled reference."""
+    dims = np.zeros(3, dtype=np.int32)
+    _check(lib().ref_read_bbm(str(path).encode(), _p(dims), None, 0, None), C.c_int(-1))
+    l, w, bs = map(int, dims)
+    sizes = np.zeros(l, dtype=np.int32)
+    mem = np.zeros((l, 2 * w + 1, bs, bs), dtype=np.complex128)
+    _check(lib().ref_read_bbm(str(path).encode(), _p(dims), _p(sizes), l, _p(mem)), C.c_int(-1))
+    return from_slots(O.BlockLayout(l, [int(s) for s in sizes], w), mem)

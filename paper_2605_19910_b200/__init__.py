@@ -5,9 +5,9 @@ include/bbsi_cuda.h; this package is the host-side mirror of the reference
 ``bbsi`` interface plus the BASELINE Dyson workloads. No CPU fallback.
 """
 from .bbsi import (BlockBandedMatrix, BlockLayout, CudaError, DomainPlan, ExtendedInverse,  # noqa: F401
-                   InvalidArgumentError, KernelCounters, SingularMatrixError, ddrgf, make_layout, rgf_extended,
-                   rgf_fused, rgf_ndiag, rgf_tridiag)
+                   InvalidArgumentError, KernelCounters, SingularMatrixError, ddrgf, make_layout, random_spd_like,
+                   read_bbm, rgf_extended, rgf_fused, rgf_ndiag, rgf_tridiag, write_bbm)
 
 __all__ = ["BlockBandedMatrix", "BlockLayout", "CudaError", "DomainPlan", "ExtendedInverse", "InvalidArgumentError",
-           "KernelCounters", "SingularMatrixError", "ddrgf", "make_layout", "rgf_extended", "rgf_fused", "rgf_ndiag",
-           "rgf_tridiag"]
+           "KernelCounters", "SingularMatrixError", "ddrgf", "make_layout", "random_spd_like", "read_bbm",
+           "rgf_extended", "rgf_fused", "rgf_ndiag", "rgf_tridiag", "write_bbm"]

@@ -274,3 +274,84 @@ def ddrgf(m: BlockBandedMatrix, plan: DomainPlan):
                                  plan.n_threads, plan.terminal_threads, _ptr(g), _ptr(cnt), C.byref(fail))
     _raise(rc, fail.value)
     return BlockBandedMatrix._from_slots(lay, g), KernelCounters(*map(int, cnt))
+
+
+def random_spd_like(layout: BlockLayout, seed: int, dominance: float) -> BlockBandedMatrix:
+    """block_banded.hpp:99-133 (raw mt19937_64 stream of block_banded.hpp:70-91), generated
+    host-side by the C ABI (bbsi_random_spd_like_z) in the reference's draw order."""
+    sizes = np.array(layout.block_sizes, dtype=np.int32)
+    l, w, bs = layout.num_layers, layout.bandwidth, layout.slot_size
+    mem = np.zeros((l, 2 * w + 1, bs, bs), dtype=np.complex128)
+    _raise(lib().bbsi_random_spd_like_z(l, w, bs, _ptr(sizes), C.c_uint64(seed), float(dominance), _ptr(mem)))
+    return BlockBandedMatrix._from_slots(layout, mem)
+
+
+# ------------------------------------------------------------------ .bbm files (io.cpp:26-75)
+# One JSON header line {"version": 1, "num_layers", "block_sizes", "bandwidth",
+# "scalar": "c128"}, then every in-band block (layer ascending, offset ascending),
+# column-major, (re, im) little-endian float64 pairs.
+
+def _inband(layout: BlockLayout):
+    l, w = layout.num_layers, layout.bandwidth
+    for a in range(l):
+        for off in range(-w, w + 1):
+            if 0 <= a + off < l:
+                yield a, off
+
+
+def write_bbm(path: str, m: BlockBandedMatrix) -> None:
+    """io.cpp:26-45"""
+    import json
+
+    lay = m.layout
+    header = {"version": 1, "num_layers": lay.num_layers, "block_sizes": lay.block_sizes,
+              "bandwidth": lay.bandwidth, "scalar": "c128"}
+    try:
+        f = open(path, "wb")
+    except OSError:
+        raise InvalidArgumentError(f"write_bbm: cannot open {path}") from None
+    with f:
+        f.write((json.dumps(header, separators=(",", ":"), sort_keys=True) + "\n").encode())  # nlohmann dump order
+        for a, off in _inband(lay):
+            f.write(np.asarray(m.block(a, off), dtype="<c16").tobytes(order="F"))
+
+
+def read_bbm(path: str) -> BlockBandedMatrix:
+    """io.cpp:47-73 (same rejections: missing file, malformed header, version, scalar,
+    truncated payload)."""
+    import json
+
+    try:
+        f = open(path, "rb")
+    except OSError:
+        raise InvalidArgumentError(f"read_bbm: cannot open {path}") from None
+    with f:
+        line = f.readline()
+        if not line:
+            raise InvalidArgumentError("read_bbm: missing header")
+        try:
+            header = json.loads(line)
+        except ValueError:
+            header = None
+        if not isinstance(header, dict):
+            raise InvalidArgumentError("read_bbm: malformed header")
+        if header.get("version", 0) != 1:
+            raise InvalidArgumentError("read_bbm: unsupported version")
+        if header.get("scalar", "") != "c128":
+            raise InvalidArgumentError("read_bbm: unsupported scalar type")
+        try:
+            lay = BlockLayout(int(header["num_layers"]), list(header["block_sizes"]), int(header["bandwidth"]))
+        except (KeyError, TypeError) as e:
+            raise InvalidArgumentError(f"read_bbm: malformed header ({e})") from None
+        m = BlockBandedMatrix(lay)
+        payload = f.read()
+    pos = 0
+    for a, off in _inband(lay):
+        r, c = lay.block_sizes[a], lay.block_sizes[a + off]
+        nbytes = 16 * r * c
+        if pos + nbytes > len(payload):
+            raise InvalidArgumentError(f"read_bbm: truncated block data in {path}")
+        blk = np.frombuffer(payload, dtype="<c16", count=r * c, offset=pos).reshape((r, c), order="F")
+        m.data[a, off + lay.bandwidth, :r, :c] = blk
+        pos += nbytes
+    return m

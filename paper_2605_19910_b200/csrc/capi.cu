@@ -5,7 +5,9 @@
 #include <map>
 #include <cstdlib>
 #include <cstring>
+#include <complex>
 #include <mutex>
+#include <random>
 #include <string>
 #include <vector>
 
@@ -367,12 +369,13 @@ int bbsi_cuda_dyson_rgf_dev(int l, int w, int bs, int n_energy, const double* dH
   W.G = reinterpret_cast<double2*>(dG);
   W.g_bstride = (long long)l * (2 * w + 1) * bs * bs;
   W.groups = default_groups(W.batch, W.bs);
-  void* scratch = arena_get(1, sweep_scratch_bytes(W.l, W.w, W.bs, W.batch, W.groups));
+  W.two_ended = two_ended_default();
+  void* scratch = arena_get(1, sweep_scratch_bytes(W.l, W.w, W.bs, W.batch, W.groups, W.two_ended));
   if (!scratch) return fail(BBSI_OUT_OF_MEMORY, "sweep workspace allocation failed");
   sweep_carve(W, scratch);
   std::vector<int> nt(l, bs), fails;
   const std::string key = graph_key("dyson", {l, w, bs, n_energy, (long long)dH, (long long)dG, (long long)dzs,
-                                              (long long)scratch, W.groups});
+                                              (long long)scratch, W.groups, W.two_ended});
   // tridiagonal: the sweeps read A's off-diagonal blocks (-H) from the shared H, so only
   // the diagonal blocks of each energy's band are formed
   if (w == 1) W.Hoff = reinterpret_cast<const double2*>(dH);
@@ -414,6 +417,52 @@ void bbsi_dyson_fill_h_host(int l, int w, int b, uint64_t seed, double* H) {
           d[2 * ((long long)j * b + i) + 1] = im;
         }
     }
+}
+
+int bbsi_random_spd_like_z(int l, int w, int bs, const int* sizes, uint64_t seed, double dominance, double* A) {
+  if (int rc = validate_layout(l, w, bs, sizes)) return rc;
+  if (!(dominance > 0.0)) return fail(BBSI_INVALID_ARGUMENT, "random_spd_like: dominance must be positive");
+  using cd = std::complex<double>;
+  std::vector<int> sz(l, bs);
+  if (sizes)
+    for (int a = 0; a < l; ++a) sz[a] = sizes[a];
+  const long long bb = (long long)bs * bs;
+  cd* m = reinterpret_cast<cd*>(A);
+  std::memset(A, 0, sizeof(cd) * size_t(l) * (2 * w + 1) * bb);
+  auto blk = [&](int a, int off) { return m + ((long long)a * (2 * w + 1) + off + w) * bb; };
+  auto in_band = [&](int a, int off) { return a + off >= 0 && a + off < l; };
+  std::mt19937_64 rng(seed);
+  auto next_real = [&] { return double(rng() >> 11) * (2.0 / 9007199254740992.0) - 1.0; };
+  for (int a = 0; a < l; ++a)
+    for (int off = -w; off <= w; ++off)
+      if (in_band(a, off)) {
+        cd* p = blk(a, off);
+        for (int j = 0; j < sz[a + off]; ++j)
+          for (int i = 0; i < sz[a]; ++i) {
+            const double re = next_real();
+            const double im = next_real();
+            p[(long long)j * bs + i] = cd(re, im);
+          }
+      }
+  for (int a = 0; a < l; ++a) {
+    cd* diag = blk(a, 0);
+    for (int i = 0; i < sz[a]; ++i) {
+      double row_sum = 0.0;
+      for (int off = -w; off <= w; ++off) {
+        if (!in_band(a, off)) continue;
+        const cd* p = blk(a, off);
+        for (int j = 0; j < sz[a + off]; ++j) {
+          if (off == 0 && j == i) continue;
+          row_sum += std::abs(p[(long long)j * bs + i]);
+        }
+      }
+      const cd d = diag[(long long)i * bs + i];
+      const double mag = std::abs(d);
+      const cd phase = mag > 1e-12 ? d / cd(mag) : cd(1);
+      diag[(long long)i * bs + i] = d + phase * cd(dominance * row_sum);
+    }
+  }
+  return BBSI_OK;
 }
 
 int bbsi_cuda_zgemm_dev(int m, int n, int k, const double* alpha, const double* dA, long long lda, long long a_bstride,
@@ -502,12 +551,12 @@ int bbsi_cuda_dyson_rgf_z(int l, int w, int bs, int n_energy, const double* H, c
   if (chunk <= 0 || chunk > n_energy) {
     chunk = n_energy;
     while (chunk > 1 && (size_t(chunk) * band_b + band_b +
-                         sweep_scratch_bytes(l, w, bs, chunk, default_groups(chunk, bs))) > free_b * 9 / 10)
+                         sweep_scratch_bytes(l, w, bs, chunk, default_groups(chunk, bs), two_ended_default())) > free_b * 9 / 10)
       chunk = (chunk + 1) / 2;
   }
   const int nchunk = (n_energy + chunk - 1) / chunk;
   const int groups = default_groups(chunk, bs);
-  const size_t scr_b = sweep_scratch_bytes(l, w, bs, chunk, groups);
+  const size_t scr_b = sweep_scratch_bytes(l, w, bs, chunk, groups, two_ended_default());
   int nbuf = nchunk;
   while (nbuf > 1 && (size_t(nbuf) * chunk * band_b + band_b + scr_b) > free_b * 9 / 10) --nbuf;
   double2* dH = static_cast<double2*>(arena_get(4, band_b));
@@ -547,6 +596,7 @@ int bbsi_cuda_dyson_rgf_z(int l, int w, int bs, int n_energy, const double* H, c
       W.G = g;
       W.g_bstride = band;
       W.groups = groups;
+      W.two_ended = two_ended_default();
       if (w == 1) W.Hoff = dH;
       sweep_carve(W, scratch);
       // finished band rows of the downward sweep -> host, on the copy stream, while the

@@ -19,6 +19,10 @@ cudaError_t zgemm_grouped(ZGemmGroup& g, cudaStream_t stream);
 // zinv_scratch_bytes(n, batch) bytes; status[b] = -1 or the first negligible pivot.
 cudaError_t zinv_batched(double2* M, long long ld, long long bstride, int n, int n_true, int batch, void* scratch,
                          int* status, cudaStream_t stream);
+// Same over `outer` x `inner` matrices: matrix (o, i) at M + i*bstride + o*ostride,
+// status at status[i + o*sostride] (outer <= kMaxProblems; scratch for inner*outer).
+cudaError_t zinv_batched2(double2* M, long long ld, long long bstride, int n, int n_true, int inner, int outer,
+                          long long ostride, void* scratch, int* status, long long sostride, cudaStream_t stream);
 size_t zinv_scratch_bytes(int n, int batch);
 cudaError_t dyson_fill_h(double2* H, int l, int w, int b, uint64_t seed, cudaStream_t s);
 // Diagonal blocks only (A_aa = z I - H_aa - sigma_a I) plus zeroed out-of-range slots,
@@ -56,10 +60,17 @@ struct SweepWork {
   // = -H (Dyson batches). The sweeps then read those operands from H, shared by the
   // whole batch, and G's off-diagonal slots need not hold A (see dyson_form_diag).
   const double2* Hoff = nullptr;
+  // w == 1 only: two-ended sweep (left- and right-connected Schur chains run
+  // concurrently, meet at layer l/2, then two outward sweeps). Same output; twice the
+  // batch per latency-bound inversion launch and half the sequential steps. Set
+  // before sweep_carve (the inversion scratch doubles).
+  bool two_ended = false;
 };
 
 // Bytes of LM+UM+piv+wz+status for a sweep.
-size_t sweep_scratch_bytes(int l, int w, int bs, int batch, int groups = 1);
+size_t sweep_scratch_bytes(int l, int w, int bs, int batch, int groups = 1, bool two_ended = false);
+// Two-ended sweeps for Dyson batches (env BBSI_TWO_ENDED=0 turns them off).
+bool two_ended_default();
 // Default number of concurrent batch groups (env BBSI_GROUPS overrides).
 int default_groups(int batch, int bs);
 // Carves the scratch part of a SweepWork out of `base` (>= sweep_scratch_bytes).

@@ -37,10 +37,23 @@ int default_groups(int batch, int bs) {
   return batch >= 8 ? 2 : 1;
 }
 
-size_t sweep_scratch_bytes(int l, int w, int bs, int batch, int groups) {
+bool two_ended_default() {
+  static const bool on = [] {
+    const char* e = getenv("BBSI_TWO_ENDED");
+    return !(e && atoi(e) == 0);
+  }();
+  return on;
+}
+
+namespace {
+bool use_two_ended(const SweepWork& W) { return W.two_ended && W.w == 1 && W.l >= 3; }
+}  // namespace
+
+size_t sweep_scratch_bytes(int l, int w, int bs, int batch, int groups, bool two_ended) {
   const size_t bb = size_t(bs) * bs * sizeof(double2);
+  const int chains = (two_ended && w == 1 && l >= 3) ? 2 : 1;
   size_t s = 2 * size_t(batch) * l * w * bb;              // LM, UM
-  s += size_t(groups) * (zinv_scratch_bytes(bs, (batch + groups - 1) / groups) + 256);  // inversion scratch
+  s += size_t(groups) * (zinv_scratch_bytes(bs, chains * ((batch + groups - 1) / groups)) + 256);  // inversion scratch
   s += size_t(l) * batch * sizeof(int) + 256;             // status
   return s;
 }
@@ -54,7 +67,7 @@ void sweep_carve(SweepWork& W, void* base) {
   p += size_t(W.batch) * W.l * W.w * bb * sizeof(double2);
   W.inv = p;
   const int gs = (W.batch + W.groups - 1) / W.groups;
-  p += size_t(W.groups) * (zinv_scratch_bytes(W.bs, gs) + 256);
+  p += size_t(W.groups) * (zinv_scratch_bytes(W.bs, (use_two_ended(W) ? 2 : 1) * gs) + 256);
   W.status = reinterpret_cast<int*>(p);
 }
 
@@ -161,6 +174,121 @@ cudaError_t rgf_sweeps_one(const SweepWork& W, const int* n_true, int* status, i
   return cudaSuccess;
 }
 
+// Two-ended block-tridiagonal sweep (w = 1). The right-connected chain of
+// rgf_tridiag (rgf.hpp:58-64) runs from layer l-1 down to m+1 while its mirror, the
+// left-connected chain, runs from layer 0 up to m-1, in lockstep: every inversion
+// launch covers both chains (2 x batch matrices) and every GEMM launch both chains'
+// products. Layer m receives both Schur corrections and its inverse is G[m,m]; the
+// two outward sweeps (rgf.hpp:66-74 and its mirror) then run in lockstep as well.
+//   right, j = l-1 .. m+1:  X_j = inv(M'[j,j]),  lm[j] = X_j A[j,j-1],  um[j] = A[j-1,j] X_j,
+//                           M'[j-1,j-1] -= A[j-1,j] lm[j]
+//   left,  j = 0 .. m-1:    Y_j = inv(M'[j,j]),  lm[j] = Y_j A[j,j+1],  um[j] = A[j+1,j] Y_j,
+//                           M'[j+1,j+1] -= A[j+1,j] lm[j]
+//   G[m,m] = inv(M'[m,m])
+//   right, j = m+1 .. l-1:  G[j,j-1] = -lm[j] G[j-1,j-1],  G[j-1,j] = -G[j-1,j-1] um[j],
+//                           G[j,j] = X_j - lm[j] G[j-1,j]
+//   left,  j = m-1 .. 0:    G[j,j+1] = -lm[j] G[j+1,j+1],  G[j+1,j] = -G[j+1,j+1] um[j],
+//                           G[j,j] = Y_j - lm[j] G[j+1,j]
+// Same products and inverses per layer as the one-ended sweep. status[j] records the
+// pivot of layer j in this elimination order.
+cudaError_t rgf_sweeps_two(const SweepWork& W, const int* n_true, int* status, int status_stride, cudaStream_t s) {
+  Ctx c(W);
+  const int l = W.l, b = W.bs;
+  const int m = l / 2, nR = l - 1 - m, nL = m;
+  const bool hs = W.Hoff != nullptr;
+  const double sg = hs ? -1.0 : 1.0;  // A's off-diagonal blocks are -H when read from H
+  cudaError_t e;
+  auto blk = [&](const double2* p) { return c.gop(p, 0, 0); };
+  auto offd = [&](int a, int off) { return hs ? c.hop(a, off) : blk(c.slot(a, off)); };
+  auto lmo = [&](int j) { return c.mop(c.lm(j), 0, 0); };
+  auto umo = [&](int j) { return c.mop(c.um(j), 0, 0); };
+  auto grp = [&](const ZGemmProblem* ps, int np) {
+    ZGemmGroup g{};
+    g.batch = W.batch;
+    g.bs = b;
+    for (int i = 0; i < np; ++i) g.prob[g.nprob++] = ps[i];
+    return zgemm_grouped(g, s);
+  };
+  // inversion of layer jR (and jL when >= 0) for the whole batch in one launch
+  auto inv2 = [&](int jR, int jL) {
+    double2* mR = c.slot(jR, 0);
+    if (jL < 0 || n_true[jL] != n_true[jR]) {  // (ragged layers: one launch per chain)
+      cudaError_t r = zinv_batched2(mR, b, W.g_bstride, b, n_true[jR], W.batch, 1, 0, W.inv,
+                                    status + (long long)jR * status_stride, 0, s);
+      if (r != cudaSuccess || jL < 0) return r;
+      return zinv_batched2(c.slot(jL, 0), b, W.g_bstride, b, n_true[jL], W.batch, 1, 0, W.inv,
+                           status + (long long)jL * status_stride, 0, s);
+    }
+    return zinv_batched2(mR, b, W.g_bstride, b, n_true[jR], W.batch, 2, (long long)(c.slot(jL, 0) - mR), W.inv,
+                         status + (long long)jR * status_stride, (long long)(jL - jR) * status_stride, s);
+  };
+
+  // ---------------- two inward chains
+  const int nup = nR > nL ? nR : nL;
+  for (int t = 0; t < nup; ++t) {
+    const int jR = t < nR ? l - 1 - t : -1, jL = t < nL ? t : -1;
+    if ((e = jR >= 0 ? inv2(jR, jL) : inv2(jL, -1)) != cudaSuccess) return e;
+    ZGemmProblem p1[2], p2[4];
+    int n1 = 0, n2 = 0;
+    if (jR >= 0) {
+      p1[n1++] = prob(b, b, b, sg, 0.0, blk(c.slot(jR, 0)), offd(jR, -1), lmo(jR));
+      const ZOp up = offd(jR - 1, +1);
+      p2[n2++] = prob(b, b, b, -sg, 1.0, up, lmo(jR), blk(c.slot(jR - 1, 0)));
+      p2[n2++] = prob(b, b, b, sg, 0.0, up, blk(c.slot(jR, 0)), umo(jR));
+    }
+    if (jL >= 0) {
+      p1[n1++] = prob(b, b, b, sg, 0.0, blk(c.slot(jL, 0)), offd(jL, +1), lmo(jL));
+      const ZOp dn = offd(jL + 1, -1);
+      p2[n2++] = prob(b, b, b, -sg, 1.0, dn, lmo(jL), blk(c.slot(jL + 1, 0)));
+      p2[n2++] = prob(b, b, b, sg, 0.0, dn, blk(c.slot(jL, 0)), umo(jL));
+    }
+    if ((e = grp(p1, n1)) != cudaSuccess) return e;
+    if (jR >= 0 && jL >= 0 && jR - 1 == jL + 1) {  // both chains correct layer m: serialise
+      if ((e = grp(p2, 2)) != cudaSuccess) return e;
+      if ((e = grp(p2 + 2, 2)) != cudaSuccess) return e;
+    } else if ((e = grp(p2, n2)) != cudaSuccess) {
+      return e;
+    }
+  }
+  if ((e = inv2(m, -1)) != cudaSuccess) return e;
+
+  // ---------------- two outward sweeps; after step t rows [lo, hi) are final
+  int flo = m, fhi = m;  // rows [flo, fhi) already handed to rows_done
+  auto flush = [&](int lo, int hi, bool force) -> cudaError_t {
+    if (!W.rows_done) return cudaSuccess;
+    if (!force && (flo - lo) + (hi - fhi) < W.hook_rows) return cudaSuccess;
+    cudaError_t r = cudaSuccess;
+    if (lo < flo) r = W.rows_done(lo, flo, W.e_off, W.batch, s);
+    if (r == cudaSuccess && hi > fhi) r = W.rows_done(fhi, hi, W.e_off, W.batch, s);
+    flo = lo;
+    fhi = hi;
+    return r;
+  };
+  const int ndown = nR > nL ? nR : nL;
+  for (int t = 1; t <= ndown; ++t) {
+    const int jR = m + t <= l - 1 ? m + t : -1, jL = m - t >= 0 ? m - t : -1;
+    ZGemmProblem pa[4], pb[2];
+    int na = 0, nb = 0;
+    if (jR >= 0) {
+      const ZOp gprev = blk(c.slot(jR - 1, 0));
+      pa[na++] = prob(b, b, b, -1.0, 0.0, lmo(jR), gprev, blk(c.slot(jR, -1)));
+      pa[na++] = prob(b, b, b, -1.0, 0.0, gprev, umo(jR), blk(c.slot(jR - 1, +1)));
+      pb[nb++] = prob(b, b, b, -1.0, 1.0, lmo(jR), blk(c.slot(jR - 1, +1)), blk(c.slot(jR, 0)));
+    }
+    if (jL >= 0) {
+      const ZOp gnext = blk(c.slot(jL + 1, 0));
+      pa[na++] = prob(b, b, b, -1.0, 0.0, lmo(jL), gnext, blk(c.slot(jL, +1)));
+      pa[na++] = prob(b, b, b, -1.0, 0.0, gnext, umo(jL), blk(c.slot(jL + 1, -1)));
+      pb[nb++] = prob(b, b, b, -1.0, 1.0, lmo(jL), blk(c.slot(jL + 1, -1)), blk(c.slot(jL, 0)));
+    }
+    if ((e = grp(pa, na)) != cudaSuccess) return e;
+    if ((e = grp(pb, nb)) != cudaSuccess) return e;
+    const int lo = m - t <= 0 ? 0 : m - t + 1, hi = m + t >= l - 1 ? l : m + t;
+    if ((e = flush(lo, hi, false)) != cudaSuccess) return e;
+  }
+  return flush(0, l, true);
+}
+
 struct StreamPool {
   std::vector<cudaStream_t> s;
   std::vector<cudaEvent_t> ev;
@@ -191,7 +319,9 @@ StreamPool& pool_for(int n) {
 
 cudaError_t rgf_sweeps(const SweepWork& W, const int* n_true, cudaStream_t s) {
   const int G = W.groups < 1 ? 1 : (W.groups > W.batch ? W.batch : W.groups);
-  if (G == 1) return rgf_sweeps_one(W, n_true, W.status, W.batch, s);
+  if (G == 1)
+    return use_two_ended(W) ? rgf_sweeps_two(W, n_true, W.status, W.batch, s)
+                            : rgf_sweeps_one(W, n_true, W.status, W.batch, s);
   // Independent batch groups on side streams: one group's latency-bound pivot
   // inversions overlap the other groups' GEMMs.
   StreamPool& P = pool_for(G);
@@ -199,7 +329,7 @@ cudaError_t rgf_sweeps(const SweepWork& W, const int* n_true, cudaStream_t s) {
   if ((e = cudaEventRecord(P.ev[G], s))) return e;
   const int gs = (W.batch + G - 1) / G;
   const long long bb = (long long)W.bs * W.bs;
-  const size_t inv_b = zinv_scratch_bytes(W.bs, gs) + 256;
+  const size_t inv_b = zinv_scratch_bytes(W.bs, (use_two_ended(W) ? 2 : 1) * gs) + 256;
   for (int g = 0; g < G; ++g) {
     const int e0 = g * gs, ne = std::min(gs, W.batch - e0);
     if (ne <= 0) break;
@@ -211,7 +341,9 @@ cudaError_t rgf_sweeps(const SweepWork& W, const int* n_true, cudaStream_t s) {
     Wg.inv = static_cast<char*>(W.inv) + size_t(g) * inv_b;
     Wg.e_off = W.e_off + e0;
     if ((e = cudaStreamWaitEvent(P.s[g], P.ev[G], 0))) return e;
-    if ((e = rgf_sweeps_one(Wg, n_true, W.status + e0, W.batch, P.s[g]))) return e;
+    if ((e = use_two_ended(W) ? rgf_sweeps_two(Wg, n_true, W.status + e0, W.batch, P.s[g])
+                              : rgf_sweeps_one(Wg, n_true, W.status + e0, W.batch, P.s[g])))
+      return e;
     if ((e = cudaEventRecord(P.ev[g], P.s[g]))) return e;
     if ((e = cudaStreamWaitEvent(s, P.ev[g], 0))) return e;
   }

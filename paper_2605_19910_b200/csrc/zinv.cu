@@ -89,6 +89,16 @@ struct GjScratch {
   double2* s0;    // [batch][n*n]   working matrix
 };
 
+// Matrix b of a launch lives at base + (b % inner) * bstride + (b / inner) * ostride and
+// reports into status[(b % inner) + (b / inner) * sostride]: `outer` independent
+// batches with one uniform stride each (e.g. the two chains of a two-ended sweep).
+struct BatchIdx {
+  int inner;
+  long long bstride, ostride, sostride;
+  __host__ __device__ long long off(int b) const { return (long long)(b % inner) * bstride + (long long)(b / inner) * ostride; }
+  __host__ __device__ long long sidx(int b) const { return (long long)(b % inner) + (long long)(b / inner) * sostride; }
+};
+
 size_t align256(size_t x) { return (x + 255) & ~size_t(255); }
 
 size_t carve(GjScratch& s, void* base, int n, int nb, int batch) {
@@ -309,7 +319,7 @@ __device__ __forceinline__ void panel_tail(const double2* __restrict__ cur, long
     }
   }
   __syncthreads();
-  if (tid == 0 && *s_fail != INT_MAX && status[b] < 0) status[b] = *s_fail;
+  if (tid == 0 && *s_fail != INT_MAX && *status < 0) *status = *s_fail;
   ZDBG(9)
 }
 
@@ -353,7 +363,7 @@ __device__ __forceinline__ void argmax_merge(double& v, int& i, double v2, int i
 template <int NB>
 __global__ void __launch_bounds__(PT, 1)
     gj_panel_kernel(const double2* __restrict__ cur0, long long ld, long long bstride, int n, int n_true, int k, int last,
-                    GjScratch S, int* __restrict__ status) {
+                    GjScratch S, int* __restrict__ status0, BatchIdx bi) {
   extern __shared__ __align__(16) double2 pn[];  // NB columns x rows (ld = rows + 1), then perm[2][rows], act[rows]
   __shared__ double cand_v[2][PT / 32];
   __shared__ int cand_i[2][PT / 32];
@@ -362,7 +372,8 @@ __global__ void __launch_bounds__(PT, 1)
 
   const int tid = threadIdx.x, lane = tid & 31, warp = tid >> 5;
   const int b = blockIdx.x;
-  const double2* __restrict__ cur = cur0 + (long long)b * bstride;
+  const double2* __restrict__ cur = cur0 + (k == 0 ? bi.off(b) : (long long)b * bstride);
+  int* __restrict__ status = status0 + bi.sidx(b);
   const int rows = n - k;
   const int ldp = rows + 1;
   int* perm = reinterpret_cast<int*>(pn + NB * ldp);  // [2][rows]
@@ -379,7 +390,7 @@ __global__ void __launch_bounds__(PT, 1)
     if (tid == 0) {
       s_tol = t;
       S.tol[b] = t;
-      status[b] = -1;
+      *status = -1;
     }
   } else if (tid == 0) {
     s_tol = S.tol[b];
@@ -642,7 +653,7 @@ __device__ __forceinline__ void panel_threshold_once(const double2* cur, long lo
     if (threadIdx.x == 0) {
       *s_tol = t;
       S.tol[b] = t;
-      status[b] = -1;
+      *status = -1;
     }
   } else if (threadIdx.x == 0) {
     *s_tol = S.tol[b];
@@ -653,14 +664,15 @@ __device__ __forceinline__ void panel_threshold_once(const double2* cur, long lo
 template <int NB, int RPT>
 __global__ void __launch_bounds__(PT, 1)
     gj_panel_rows_kernel(const double2* __restrict__ cur0, long long ld, long long bstride, int n, int n_true, int k,
-                         int last, GjScratch S, int* __restrict__ status) {
+                         int last, GjScratch S, int* __restrict__ status0, BatchIdx bi) {
   extern __shared__ __align__(16) double2 sv[];  // Vs staging for the tail, NB x (n + 2)
   __shared__ PanelSmem<NB, RPT> sm;
   __shared__ double s_red[PT / 32];
   __shared__ int s_fail;
   __shared__ double s_tol;
   const int tid = threadIdx.x, b = blockIdx.x;
-  const double2* __restrict__ cur = cur0 + (long long)b * bstride;
+  const double2* __restrict__ cur = cur0 + (k == 0 ? bi.off(b) : (long long)b * bstride);
+  int* __restrict__ status = status0 + bi.sidx(b);
   const int rows = n - k;
   ZDBG(0)
   const int* lmapg = S.lmap + (long long)b * n;
@@ -692,7 +704,7 @@ __global__ void __launch_bounds__(PT, 1)
 template <int NB, int RPT>
 __global__ void __launch_bounds__(PT, 1)
     gj_pair_kernel(const double2* __restrict__ cur0, long long ld, long long bstride, int n, int n_true, int k,
-                   int last, GjScratch S, int* __restrict__ status) {
+                   int last, GjScratch S, int* __restrict__ status0, BatchIdx bi) {
   constexpr int W2 = 2 * NB;
   extern __shared__ __align__(16) double2 sv[];  // NB x (n + 2): Vs1 / V1, then Vs2 / V2
   __shared__ PanelSmem<NB, RPT> sm;
@@ -704,7 +716,8 @@ __global__ void __launch_bounds__(PT, 1)
   __shared__ int s_fail;
   __shared__ double s_tol;
   const int tid = threadIdx.x, b = blockIdx.x;
-  const double2* __restrict__ cur = cur0 + (long long)b * bstride;
+  const double2* __restrict__ cur = cur0 + (k == 0 ? bi.off(b) : (long long)b * bstride);
+  int* __restrict__ status = status0 + bi.sidx(b);
   const int k2 = k + NB, svld = n + 2;
   int* __restrict__ lmap = S.lmap + (long long)b * n;
   int* __restrict__ rowmask = S.rowmask + (long long)b * n;
@@ -844,7 +857,7 @@ __global__ void __launch_bounds__(PT, 1)
     }
   }
   __syncthreads();
-  if (tid == 0 && s_fail != INT_MAX && status[b] < 0) status[b] = s_fail;
+  if (tid == 0 && s_fail != INT_MAX && *status < 0) *status = s_fail;
   ZDBG(28)
 }
 
@@ -859,7 +872,13 @@ size_t zinv_scratch_bytes(int n, int batch) {
 
 cudaError_t zinv_batched(double2* M, long long ld, long long bstride, int n, int n_true, int batch, void* scratch,
                          int* status, cudaStream_t stream) {
-  if (n % 64 || n_true > n || n_true < 1) return cudaErrorInvalidValue;
+  return zinv_batched2(M, ld, bstride, n, n_true, batch, 1, 0, scratch, status, 0, stream);
+}
+
+cudaError_t zinv_batched2(double2* M, long long ld, long long bstride, int n, int n_true, int inner, int outer,
+                          long long ostride, void* scratch, int* status, long long sostride, cudaStream_t stream) {
+  if (n % 64 || n_true > n || n_true < 1 || outer < 1 || outer > kMaxProblems) return cudaErrorInvalidValue;
+  const int batch = inner * outer;
   if (batch == 0) return cudaSuccess;
   constexpr int nb = kNB;
   GjScratch S;
@@ -892,8 +911,8 @@ cudaError_t zinv_batched(double2* M, long long ld, long long bstride, int n, int
     const int last = k + kw == n;
     // the first step reads the input block; the working matrix s0 is updated in place
     const double2* cur = k == 0 ? M : S.s0;
+    const BatchIdx bi{inner, k == 0 ? bstride : nn, k == 0 ? ostride : nn * inner, sostride};
     const long long cld = k == 0 ? ld : n, cbs = k == 0 ? bstride : nn;
-    double2* nxt = last ? M : S.s0;
     const long long nld = last ? ld : n, nbs = last ? bstride : nn;
     {
       ProfScope prof(stream, PROF_INV, 8.0 * double(n) * nb * kw * batch, 16.0 * (3.0 * n * kw) * batch);
@@ -908,43 +927,48 @@ cudaError_t zinv_batched(double2* M, long long ld, long long bstride, int n, int
       cfg.attrs = attr_;
       cfg.numAttrs = 1;
       if (pair && rows <= PT) {
-        e = cudaLaunchKernelEx(&cfg, gj_pair_kernel<kNB, 1>, cur, cld, cbs, n, n_true, k, last, S, status);
+        e = cudaLaunchKernelEx(&cfg, gj_pair_kernel<kNB, 1>, cur, cld, cbs, n, n_true, k, last, S, status, bi);
       } else if (pair) {
-        e = cudaLaunchKernelEx(&cfg, gj_pair_kernel<kNB, 2>, cur, cld, cbs, n, n_true, k, last, S, status);
+        e = cudaLaunchKernelEx(&cfg, gj_pair_kernel<kNB, 2>, cur, cld, cbs, n, n_true, k, last, S, status, bi);
       } else if (kind != 2 && rows <= PT) {
-        e = cudaLaunchKernelEx(&cfg, gj_panel_rows_kernel<kNB, 1>, cur, cld, cbs, n, n_true, k, last, S, status);
+        e = cudaLaunchKernelEx(&cfg, gj_panel_rows_kernel<kNB, 1>, cur, cld, cbs, n, n_true, k, last, S, status, bi);
       } else if (kind != 2 && rows <= 2 * PT) {
-        e = cudaLaunchKernelEx(&cfg, gj_panel_rows_kernel<kNB, 2>, cur, cld, cbs, n, n_true, k, last, S, status);
+        e = cudaLaunchKernelEx(&cfg, gj_panel_rows_kernel<kNB, 2>, cur, cld, cbs, n, n_true, k, last, S, status, bi);
       } else {
         cfg.dynamicSmemBytes = smem;
-        e = cudaLaunchKernelEx(&cfg, gj_panel_kernel<kNB>, cur, cld, cbs, n, n_true, k, last, S, status);
+        e = cudaLaunchKernelEx(&cfg, gj_panel_kernel<kNB>, cur, cld, cbs, n, n_true, k, last, S, status, bi);
       }
       if (e) return e;
     }
     ZGemmGroup g{};
-    g.batch = batch;
+    g.batch = inner;
     g.bs = 64;
-    g.nprob = 1;
+    g.nprob = outer;
     g.prof_cat = PROF_GJ_GEMM;
-    // M <- M (0 on the pivot rows and the panel columns) - Wz V
-    ZGemmProblem& p = g.prob[0];
-    p = ZGemmProblem{};
-    p.M = n;
-    p.N = n;
-    p.K = kw;
-    p.alpha = make_double2(-1.0, 0.0);
-    p.beta = make_double2(1.0, 0.0);
-    p.A = ZOp{S.wz, n, 64, 64LL * n, (long long)n * kw};
-    p.B = ZOp{S.vbuf, kw, 64, 64LL * kw, (long long)kw * n};
-    p.C = ZOp{cur, cld, 64, 64LL * cld, cbs};
-    p.D = ZOp{nxt, nld, 64, 64LL * nld, nbs};
-    p.rowmap = S.rowmask;
-    p.rowscat = last ? S.rowscat : nullptr;
-    p.colmap = last ? S.colmap : nullptr;
-    p.map_bstride = n;
-    p.zr0 = p.zr1 = 0;
-    p.zc0 = k;
-    p.zc1 = k + kw;
+    // M <- M (0 on the pivot rows and the panel columns) - Wz V, one problem per outer batch
+    for (int o = 0; o < outer; ++o) {
+      const long long so = (long long)o * inner;  // first scratch entry of this outer batch
+      ZGemmProblem& p = g.prob[o];
+      p = ZGemmProblem{};
+      p.M = n;
+      p.N = n;
+      p.K = kw;
+      p.alpha = make_double2(-1.0, 0.0);
+      p.beta = make_double2(1.0, 0.0);
+      p.A = ZOp{S.wz + so * n * kw, n, 64, 64LL * n, (long long)n * kw};
+      p.B = ZOp{S.vbuf + so * kw * n, kw, 64, 64LL * kw, (long long)kw * n};
+      const double2* c0 = k == 0 ? M + o * ostride : S.s0 + so * nn;
+      double2* d0 = last ? M + o * ostride : S.s0 + so * nn;
+      p.C = ZOp{c0, cld, 64, 64LL * cld, cbs};
+      p.D = ZOp{d0, nld, 64, 64LL * nld, nbs};
+      p.rowmap = S.rowmask + so * n;
+      p.rowscat = last ? S.rowscat + so * n : nullptr;
+      p.colmap = last ? S.colmap + so * n : nullptr;
+      p.map_bstride = n;
+      p.zr0 = p.zr1 = 0;
+      p.zc0 = k;
+      p.zc1 = k + kw;
+    }
     if ((e = zgemm_grouped(g, stream))) return e;
     k += kw;
   }

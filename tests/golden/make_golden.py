@@ -68,6 +68,11 @@ def main():
         parts[f"inter_{l}_{s2}"] = np.array(inter)
         parts[f"sep_{l}_{s2}"] = np.array(sep)
     np.savez_compressed(OUT / "partition_orders.npz", **parts)
+    # .bbm files written by the reference io.cpp (test_io.cpp:22-38 shapes)
+    m = R.random_spd_like(O.make_layout(5, 3, 2), 99, 2.0)
+    m.data[0, 2, 0, 0] = complex(-0.0, 1e-308)
+    R.write_bbm(OUT / "io_l5_b3_w2_s99.bbm", m)
+    R.write_bbm(OUT / "io_ragged_l4_s123.bbm", R.random_spd_like(O.BlockLayout(4, [2, 5, 1, 3], 1), 123, 2.0))
     print("golden fixtures written to", OUT)
 
 

@@ -81,3 +81,11 @@ def test_host_path_streams_identical_bands(gpu, cfg_id, layers, n_e, b, chunk):
         a = _oracle_band(cfg, e)
         ref = O.rgf_ndiag(a)[0] if cfg.bandwidth > 1 else O.rgf_tridiag(a)[0]
         assert O.max_block_error(O.Band(lay, np.swapaxes(got[e], -1, -2)), ref) <= TOL
+
+
+@pytest.mark.parametrize("layers,n_e", [(3, 2), (4, 3), (5, 9), (8, 9), (33, 4)])
+def test_two_ended_sweep_layer_counts(gpu, layers, n_e):
+    """The Dyson batch runs the two-ended tridiagonal sweep (chains meet at l/2):
+    odd / even / minimal layer counts, one and two stream groups, against the
+    reference's one-ended RGF."""
+    _check(D.scaled(D.CONFIGS[2], num_layers=layers, n_energy=n_e, block_size=64))

@@ -13,7 +13,7 @@ ROOT = Path(__file__).resolve().parent.parent
 
 def _declared():
     text = (ROOT / "include" / "bbsi_cuda.h").read_text()
-    return sorted(set(re.findall(r"\b(bbsi_(?:cuda|dyson)_\w+)\s*\(", text)))
+    return sorted(set(re.findall(r"\b(bbsi_(?:cuda|dyson|random)_\w+)\s*\(", text)))
 
 
 def test_every_declared_symbol_is_exported():
