@@ -45,7 +45,7 @@ def parse():
     p.add_argument("--impl", default="ours", choices=["ours", "reference"])
     p.add_argument("--no-e2e", action="store_true")
     p.add_argument("--no-cpu-baseline", action="store_true")
-    p.add_argument("--chunk", type=int, default=0, help="energy chunk of the e2e path (0 = all energies, memory permitting)")
+    p.add_argument("--chunk", type=int, default=0, help="energy chunk of the e2e path (0 = library default: ~32 energies per chunk from 48 energies up)")
     return p.parse_args()
 
 

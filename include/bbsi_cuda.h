@@ -142,6 +142,12 @@ void bbsi_dyson_fill_h_host(int l, int w, int b, uint64_t seed, double* H);
  * inputs. Returns BBSI_INVALID_ARGUMENT for a bad layout or dominance <= 0. */
 int bbsi_random_spd_like_z(int l, int w, int bs, const int* sizes, uint64_t seed, double dominance, double* A);
 
+/* Kernel timings for the GPU cost model (the B200 counterpart of benchmark_kernels,
+ * microbench.hpp / cost_model.hpp:12-18): mean device time of ONE batched launch over
+ * `batch` n x n complex128 matrices, out[0] = GEMM (C = A*B) seconds, out[1] = inversion
+ * (zgetrf + zgetrs(I) equivalent) seconds, out[2] = timed samples. n % 64 == 0. */
+int bbsi_cuda_bench_kernels(int n, int batch, int samples, double* out);
+
 /* ---------------------------------------------------------------- kernel-level API (device pointers)
  * Batched C = alpha*A*B + beta*C on plain column-major complex128 matrices,
  * m, n % 64 == 0, k % 16 == 0 (the sm_100a DMMA GEMM of the sweeps). */

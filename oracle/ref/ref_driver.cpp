@@ -253,4 +253,43 @@ int ref_interleave_permutation(int l, int s1, int s2, int* order, int* interior,
     return rc == 0 ? n : -1;
 }
 
+// Cost model (cost_model.hpp:67-230) for pinning the product's restatement.
+// kind 0 rgf(l), 1 nrgf(l, w), 2 fused(l, w), 3 ddrgf(l, plan); out = {gemm_eq, seconds}.
+int ref_cost(int kind, long long l, long long w, const int* s2_levels, int n_levels, int n_threads,
+             int terminal_threads, double r_lu, double r_getrs, double t_gemm, int blas_cap, double* out) {
+    return guarded(nullptr, [&] {
+        KernelRatios r{64, t_gemm, r_lu, r_getrs, 1};
+        CostEstimate e;
+        if (kind == 0) e = cost_rgf(l, r);
+        else if (kind == 1) e = cost_nrgf(l, w, r);
+        else if (kind == 2) e = cost_fused(l, w, r);
+        else {
+            DomainPlan plan;
+            plan.s2_levels.assign(s2_levels, s2_levels + n_levels);
+            plan.n_threads = n_threads;
+            plan.terminal_threads = terminal_threads;
+            e = cost_ddrgf(l, plan, r, blas_cap);
+        }
+        out[0] = e.gemm_equivalents;
+        out[1] = e.predicted_seconds;
+    });
+}
+
+// autotune (cost_model.hpp:174-224): ints = {use_rgf, ddrgf_valid, n_levels, terminal_threads,
+// s2_0, s2_1, ...}; dbl = {rgf gemm_eq, ddrgf gemm_eq}.
+int ref_autotune(long long l, int n_threads, double r_lu, double r_getrs, double t_gemm, int max_levels,
+                 int s2_max, int blas_cap, int* ints, int max_ints, double* dbl) {
+    return guarded(nullptr, [&] {
+        KernelRatios r{64, t_gemm, r_lu, r_getrs, 1};
+        TuneResult t = autotune(l, n_threads, r, max_levels, s2_max, blas_cap);
+        ints[0] = t.use_rgf;
+        ints[1] = t.ddrgf_valid;
+        ints[2] = int(t.plan.s2_levels.size());
+        ints[3] = t.plan.terminal_threads;
+        for (size_t k = 0; k < t.plan.s2_levels.size() && int(4 + k) < max_ints; ++k) ints[4 + k] = t.plan.s2_levels[k];
+        dbl[0] = t.rgf_cost.gemm_equivalents;
+        dbl[1] = t.ddrgf_valid ? t.ddrgf_cost.gemm_equivalents : 0.0;
+    });
+}
+
 }  // extern "C"

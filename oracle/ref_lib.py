@@ -191,3 +191,28 @@ def read_bbm(path: str) -> O.Band:
     mem = np.zeros((l, 2 * w + 1, bs, bs), dtype=np.complex128)
     _check(lib().ref_read_bbm(str(path).encode(), _p(dims), _p(sizes), l, _p(mem)), C.c_int(-1))
     return from_slots(O.BlockLayout(l, [int(s) for s in sizes], w), mem)
+
+
+def cost(kind: str, l: int, w: int = 1, s2_levels=(), n_threads=1, terminal_threads=1, r_lu=0.0, r_getrs=0.0,
+         t_gemm=1.0, blas_cap=12):
+    """cost_rgf / cost_nrgf / cost_fused / cost_ddrgf (cost_model.hpp:67-130): (gemm_eq, seconds)."""
+    k = {"rgf": 0, "nrgf": 1, "fused": 2, "ddrgf": 3}[kind]
+    s2 = np.array(list(s2_levels) or [1], dtype=np.int32)
+    out = np.zeros(2)
+    rc = lib().ref_cost(k, C.c_longlong(l), C.c_longlong(w), _p(s2), len(s2_levels), n_threads, terminal_threads,
+                        C.c_double(r_lu), C.c_double(r_getrs), C.c_double(t_gemm), blas_cap, _p(out))
+    _check(rc, C.c_int(-1))
+    return float(out[0]), float(out[1])
+
+
+def autotune(l, n_threads, r_lu, r_getrs, t_gemm=1.0, max_levels=5, s2_max=4, blas_cap=12):
+    """autotune (cost_model.hpp:174-224): dict of the verdict."""
+    ints = np.zeros(64, dtype=np.int32)
+    dbl = np.zeros(2)
+    rc = lib().ref_autotune(C.c_longlong(l), n_threads, C.c_double(r_lu), C.c_double(r_getrs), C.c_double(t_gemm),
+                            max_levels, s2_max, blas_cap, _p(ints), 64, _p(dbl))
+    _check(rc, C.c_int(-1))
+    n = int(ints[2])
+    return {"use_rgf": bool(ints[0]), "ddrgf_valid": bool(ints[1]), "s2_levels": [int(x) for x in ints[4:4 + n]],
+            "terminal_threads": int(ints[3]), "rgf_gemm_equivalents": float(dbl[0]),
+            "ddrgf_gemm_equivalents": float(dbl[1])}

@@ -44,6 +44,7 @@ SIGNATURES = {
     "bbsi_cuda_profile_enable": (None, [_i]),
     "bbsi_cuda_profile_collect": (_i, [_vp, _i]),
     "bbsi_cuda_fp64_peak_tflops": (_d, [_d, _i]),
+    "bbsi_cuda_bench_kernels": (_i, [_i, _i, _i, _vp]),
 }
 
 _lib = None

@@ -3,6 +3,8 @@
     python -m paper_2605_19910_b200.cli solve    [flags]   run a solver, print a timing record
     python -m paper_2605_19910_b200.cli validate [flags]   same, plus the dense-inverse check
     python -m paper_2605_19910_b200.cli scale --axis layers --grid 20,40,80
+    python -m paper_2605_19910_b200.cli bench-kernels --sizes 64,128,256 [--batch B]
+    python -m paper_2605_19910_b200.cli tune --layers 4096 --block-size 256 [--execute]
 
 Flags, environment names (BBSI_*), record keys and exit codes follow the reference
 CLI (tools/bbsi.cpp:43-63, 149-181, 183-199): 0 ok, 1 validation failed, 2 usage /
@@ -155,6 +157,82 @@ def loglog_slope(xs, ys) -> float:
     return (n * sxy - sx * sy) / (n * sxx - sx * sx)
 
 
+def ratios_to_json(r) -> dict:
+    """tools/bbsi.cpp:216-222"""
+    return {"block_size": r.block_size, "t_gemm_us": r.t_gemm * 1e6, "r_lu": r.r_lu, "r_getrs": r.r_getrs,
+            "samples": r.sample_count}
+
+
+def ratios_from_json(j: dict):
+    """tools/bbsi.cpp:224-232"""
+    from .tuner import KernelRatios
+
+    return KernelRatios(int(j["block_size"]), float(j["t_gemm_us"]) * 1e-6, float(j["r_lu"]), float(j["r_getrs"]),
+                        int(j.get("samples", 0)))
+
+
+def _pad64(n: int) -> int:
+    return max(64, -(-n // 64) * 64)
+
+
+def bench_kernels(o) -> str:
+    """`bench-kernels` (tools/bbsi.cpp:279-290): per block size, the device time of one
+    b x b GEMM and the inversion / solve ratios the GPU solvers see, measured as one
+    batched launch over --batch blocks (sizes are padded to multiples of 64 as the solvers do)."""
+    from . import tuner as T
+
+    lines = ["block_size,t_gemm_us,r_lu,r_getrs,samples"]
+    for n in [int(t) for t in o.sizes.split(",") if t]:
+        t = T.measure_kernels(_pad64(n), batches=(o.batch,), samples=o.samples or 10)
+        r = T.kernel_ratios(t, o.batch)
+        lines.append(f"{n},{r.t_gemm * 1e6},{r.r_lu},{r.r_getrs},{o.samples or 10}")
+    return "\n".join(lines) + "\n"
+
+
+def tune(o) -> str:
+    """`tune` (tools/bbsi.cpp:318-360): the reference's autotune on GPU-measured ratios (or
+    --ratios-file), plus the B200 plan (plan_gpu: energy-batched RGF vs DDRGF domains,
+    with the NCCL term across --gpus). --execute times RGF and the chosen DDRGF plan."""
+    from . import tuner as T
+
+    times = None
+    if o.ratios_file:
+        try:
+            with open(o.ratios_file) as f:
+                ratios = ratios_from_json(json.load(f))
+        except OSError:
+            raise B.InvalidArgumentError(f"cannot open {o.ratios_file}") from None
+    else:
+        times = T.measure_kernels(_pad64(o.block_size), samples=o.samples or 5)
+        ratios = T.kernel_ratios(times, 1)
+    t = T.autotune(o.layers, o.threads, ratios, o.max_levels, o.s2_max)
+    out = {"ratios": ratios_to_json(ratios), "choice": "rgf" if t.use_rgf else "ddrgf",
+           "rgf_gemm_equivalents": t.rgf_cost.gemm_equivalents,
+           "rgf_predicted_seconds": t.rgf_cost.predicted_seconds}
+    if t.ddrgf_valid:
+        levels = [{"level": k + 1, "s2": s2, "threads": t.plan.n_threads} for k, s2 in enumerate(t.plan.s2_levels)]
+        levels.append({"level": len(t.plan.s2_levels) + 1, "terminal": True, "threads": t.plan.terminal_threads})
+        out.update({"plan": levels, "ddrgf_gemm_equivalents": t.ddrgf_cost.gemm_equivalents,
+                    "ddrgf_predicted_seconds": t.ddrgf_cost.predicted_seconds,
+                    "ddrgf_breakdown": t.ddrgf_cost.breakdown})
+    if times is not None and o.bandwidth == 1:
+        g = T.plan_gpu(o.layers, o.energies, times, o.gpus)
+        out["gpu_plan"] = {"solver": g.solver, "s2": g.s2, "domains": g.domains, "energy_batch": g.energy_batch,
+                           "gpus": o.gpus, "predicted_seconds": g.predicted_seconds, "breakdown": g.breakdown,
+                           "candidates": [{"solver": c[0], "s2": c[1], "predicted_seconds": c[2]}
+                                          for c in g.candidates]}
+    if o.execute:
+        m = load_or_generate(o)
+        run = argparse.Namespace(**vars(o))
+        run.solver, run.reps = "rgf", max(1, o.reps)
+        out["measured_rgf_ms"] = sum(run_solver(m, run)[2]) / run.reps
+        plan_s2 = out.get("gpu_plan", {}).get("s2") or (t.plan.s2_levels[0] if t.ddrgf_valid else 0)
+        if plan_s2:
+            run.solver, run.plan = "ddrgf", f"s2:{plan_s2}"
+            out["measured_ddrgf_ms"] = sum(run_solver(m, run)[2]) / run.reps
+    return json.dumps(out, indent=2) + "\n"
+
+
 def main(argv=None) -> int:
     ap = argparse.ArgumentParser(prog="bbsi", description="selected inversion of block banded matrices (B200)")
     sub = ap.add_subparsers(dest="cmd", required=True)
@@ -164,8 +242,28 @@ def main(argv=None) -> int:
     sc.add_argument("--axis", default="layers", help="layers | blocksize | bandwidth | threads")
     sc.add_argument("--grid", default="20,40,80,160")
     _common(sc)
+    bk = sub.add_parser("bench-kernels", help="time the GPU GEMM / inversion kernels, emit CSV")
+    bk.add_argument("--sizes", default="64,128,256")
+    bk.add_argument("--samples", type=int, default=0)
+    bk.add_argument("--batch", type=int, default=1, help="blocks per batched launch")
+    _common(bk)
+    tu = sub.add_parser("tune", help="pick the cheapest solver plan from the cost model")
+    tu.add_argument("--max-levels", type=int, default=5)
+    tu.add_argument("--s2-max", type=int, default=4)
+    tu.add_argument("--execute", action="store_true")
+    tu.add_argument("--ratios-file", default="")
+    tu.add_argument("--samples", type=int, default=0)
+    tu.add_argument("--energies", type=int, default=1, help="energy points of the B200 plan")
+    tu.add_argument("--gpus", type=int, default=1, help="GPUs of the B200 plan")
+    _common(tu)
     o = ap.parse_args(argv)
     try:
+        if o.cmd == "bench-kernels":
+            emit(o, bench_kernels(o))
+            return 0
+        if o.cmd == "tune":
+            emit(o, tune(o))
+            return 0
         if o.cmd in ("solve", "validate"):
             if o.cmd == "validate":
                 o.validate = True

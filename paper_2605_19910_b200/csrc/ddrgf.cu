@@ -176,8 +176,10 @@ struct Local {
 };
 
 // RGF sweeps over the chains of tasks [t, t+nt) (same length len), in place in G.
+// two_ended: the chains' G is all that is needed (phase 3), so the two-ended sweep
+// may run; phase 1 reads the right-connected multipliers afterwards and may not.
 cudaError_t chain_sweeps(const Local& X, const Part& P, int s2, int t, int nt, int len, int b, const int* n_true,
-                         SweepWork& W, int* fail_layer, cudaStream_t s) {
+                         SweepWork& W, int* fail_layer, cudaStream_t s, bool two_ended = false) {
   W = SweepWork{};
   W.l = len;
   W.w = 1;
@@ -186,7 +188,8 @@ cudaError_t chain_sweeps(const Local& X, const Part& P, int s2, int t, int nt, i
   W.G = X.gslot(P.first[t], -1);
   W.g_bstride = (long long)(s2 + 1) * 3 * X.bb;
   W.groups = default_groups(nt, b);
-  void* sc = arena_get(6, sweep_scratch_bytes(len, 1, b, nt, W.groups));
+  W.two_ended = two_ended && two_ended_default();
+  void* sc = arena_get(6, sweep_scratch_bytes(len, 1, b, nt, W.groups, W.two_ended));
   if (!sc) return cudaErrorMemoryAllocation;
   sweep_carve(W, sc);
   std::vector<int> ntr(len, b);
@@ -471,7 +474,7 @@ cudaError_t ddrgf_phase3(const double2* A, double2* G, int l, int b, const int* 
   }
   e = for_task_runs(P, s2, t0, t1, [&](int t, int nt, int len) -> cudaError_t {
     SweepWork W;
-    return chain_sweeps(X, P, s2, t, nt, len + 1, b, n_true, W, fail_layer, s);
+    return chain_sweeps(X, P, s2, t, nt, len + 1, b, n_true, W, fail_layer, s, true);
   });
   if (e || *fail_layer >= 0) return e;
   // couplings: G[x0_t, x0_t - 1] = -Y_t A[x0,-1] G_ss(t-1);  G[s_t, s_t + 1] = -G_ss(t) A[s,+1] Y_{t+1}

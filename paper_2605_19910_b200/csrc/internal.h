@@ -49,7 +49,8 @@ struct SweepWork {
   double2* UM = nullptr;  // [batch][l][w][bs*bs]: um[j][t-1] = M'[j-t, j] X_j
   void* inv = nullptr;    // zinv scratch for `batch` matrices
   int groups = 1;         // independent batch groups swept concurrently on side streams
-  int* status = nullptr;  // [l][batch]
+  int* status = nullptr;  // [l][status_stride] (entry b of layer j at status[j*stride + b])
+  int status_stride = 0;  // 0: batch
   // Optional: called (while enqueueing) once band rows [r0, r1) of batch entries
   // [e0, e0 + ne) are final on stream s -- every `hook_rows` rows of the downward
   // sweep and at its end. Used to stream results to the host during the sweep.

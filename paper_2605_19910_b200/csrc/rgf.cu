@@ -319,9 +319,10 @@ StreamPool& pool_for(int n) {
 
 cudaError_t rgf_sweeps(const SweepWork& W, const int* n_true, cudaStream_t s) {
   const int G = W.groups < 1 ? 1 : (W.groups > W.batch ? W.batch : W.groups);
+  const int sstride = W.status_stride > 0 ? W.status_stride : W.batch;
   if (G == 1)
-    return use_two_ended(W) ? rgf_sweeps_two(W, n_true, W.status, W.batch, s)
-                            : rgf_sweeps_one(W, n_true, W.status, W.batch, s);
+    return use_two_ended(W) ? rgf_sweeps_two(W, n_true, W.status, sstride, s)
+                            : rgf_sweeps_one(W, n_true, W.status, sstride, s);
   // Independent batch groups on side streams: one group's latency-bound pivot
   // inversions overlap the other groups' GEMMs.
   StreamPool& P = pool_for(G);
@@ -341,8 +342,8 @@ cudaError_t rgf_sweeps(const SweepWork& W, const int* n_true, cudaStream_t s) {
     Wg.inv = static_cast<char*>(W.inv) + size_t(g) * inv_b;
     Wg.e_off = W.e_off + e0;
     if ((e = cudaStreamWaitEvent(P.s[g], P.ev[G], 0))) return e;
-    if ((e = use_two_ended(W) ? rgf_sweeps_two(Wg, n_true, W.status + e0, W.batch, P.s[g])
-                              : rgf_sweeps_one(Wg, n_true, W.status + e0, W.batch, P.s[g])))
+    if ((e = use_two_ended(W) ? rgf_sweeps_two(Wg, n_true, W.status + e0, sstride, P.s[g])
+                              : rgf_sweeps_one(Wg, n_true, W.status + e0, sstride, P.s[g])))
       return e;
     if ((e = cudaEventRecord(P.ev[g], P.s[g]))) return e;
     if ((e = cudaStreamWaitEvent(s, P.ev[g], 0))) return e;

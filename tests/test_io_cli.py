@@ -139,3 +139,26 @@ def test_cli_matrix_file_and_scale(gpu, tmp_path, capsys):
     lines = capsys.readouterr().out.strip().splitlines()
     assert rc == 0 and lines[0].startswith("axis,value") and lines[-1].startswith("# loglog_slope")
     assert cli.main(["validate", "--layers", "90", "--block-size", "64", "--reps", "1"]) == 2  # above --oracle-cap
+
+
+def test_cli_tune_from_ratios_file(tmp_path, capsys):
+    """`tune --ratios-file` needs no GPU: the reference autotune on given ratios
+    (tools/bbsi.cpp:318-350 record layout)."""
+    f = tmp_path / "r.json"
+    f.write_text(json.dumps({"block_size": 64, "t_gemm_us": 10.0, "r_lu": 2.0, "r_getrs": 1.0, "samples": 5}))
+    rc = cli.main(["tune", "--ratios-file", str(f), "--layers", "512", "--threads", "64"])
+    rec = json.loads(capsys.readouterr().out)
+    assert rc == 0 and rec["choice"] == "ddrgf" and rec["plan"][-1]["terminal"]
+    assert rec["ratios"]["t_gemm_us"] == 10.0
+
+
+@pytest.mark.gpu
+def test_cli_bench_kernels_and_tune_on_gpu(gpu, capsys):
+    assert cli.main(["bench-kernels", "--sizes", "64,100", "--samples", "2", "--batch", "4"]) == 0
+    lines = capsys.readouterr().out.strip().splitlines()
+    assert lines[0] == "block_size,t_gemm_us,r_lu,r_getrs,samples" and len(lines) == 3
+    assert float(lines[1].split(",")[1]) > 0
+    rc = cli.main(["tune", "--layers", "64", "--block-size", "64", "--samples", "2", "--execute", "--reps", "1",
+                   "--threads", "4"])
+    rec = json.loads(capsys.readouterr().out)
+    assert rc == 0 and "gpu_plan" in rec and rec["measured_rgf_ms"] > 0
