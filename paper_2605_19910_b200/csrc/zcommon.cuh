@@ -35,6 +35,11 @@ struct ZGemmProblem {
   const int* rowscat;
   long long map_bstride;
   int zr0, zr1, zc0, zc1;
+  // optional (C-as-accumulator path, plain operands, identity row map): atomicMax of
+  // max |C_ij|^2 (as double bits) over the tile's entries of C as stored, row, column
+  // < amax_n, masked ones included, into amax[batch] (the first Gauss-Jordan step)
+  unsigned long long* amax;
+  int amax_n;
   int tiles_m, tiles_n; // filled by the launcher
   int tile_begin;       // first flattened tile index of this problem
 };

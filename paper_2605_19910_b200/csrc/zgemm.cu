@@ -121,15 +121,49 @@ __global__ void __launch_bounds__(128, MINB) zgemm_grouped_kernel(const __grid_c
       }
     const double2* __restrict__ rb = rmap ? cb + (long long)n0 * P.C.ld : ct;
     double2 cv[4][4][2];
+    if (PLAIN && P.amax) {
+      // first Gauss-Jordan step (identity row map): the whole tile as stored is read in
+      // the same batch of loads -- masked entries only feed max |C_ij|^2 (rows, columns
+      // < amax_n), the accumulator takes them as 0
+      const double2* __restrict__ raw = cb + (long long)n0 * P.C.ld;
+      double mx = 0.0;
 #pragma unroll
-    for (int mi = 0; mi < 4; ++mi)
+      for (int mi = 0; mi < 4; ++mi) {
+        const int r = m0 + wm + mi * 8 + lr;
 #pragma unroll
-      for (int ni = 0; ni < 4; ++ni)
+        for (int ni = 0; ni < 4; ++ni)
 #pragma unroll
-        for (int q = 0; q < 2; ++q) {
-          const int nl = wn + ni * 8 + lc * 2 + q;
-          cv[mi][ni][q] = (rowok[mi] && colok[ni][q]) ? rb[(long long)nl * P.C.ld + srow[mi]] : make_double2(0.0, 0.0);
-        }
+          for (int q = 0; q < 2; ++q) {
+            const int nl = wn + ni * 8 + lc * 2 + q;
+            cv[mi][ni][q] = (r < P.M && n0 + nl < P.N) ? raw[(long long)nl * P.C.ld + r] : make_double2(0.0, 0.0);
+          }
+      }
+#pragma unroll
+      for (int mi = 0; mi < 4; ++mi) {
+        const int r = m0 + wm + mi * 8 + lr;
+#pragma unroll
+        for (int ni = 0; ni < 4; ++ni)
+#pragma unroll
+          for (int q = 0; q < 2; ++q) {
+            const double2 v = cv[mi][ni][q];
+            if (r < P.amax_n && n0 + wn + ni * 8 + lc * 2 + q < P.amax_n) mx = fmax(mx, fma(v.x, v.x, v.y * v.y));
+            if (!(rowok[mi] && colok[ni][q])) cv[mi][ni][q] = make_double2(0.0, 0.0);
+          }
+      }
+#pragma unroll
+      for (int o = 16; o; o >>= 1) mx = fmax(mx, __shfl_xor_sync(0xffffffffu, mx, o));
+      if (lane == 0) atomicMax(P.amax + batch, (unsigned long long)__double_as_longlong(mx));
+    } else {
+#pragma unroll
+      for (int mi = 0; mi < 4; ++mi)
+#pragma unroll
+        for (int ni = 0; ni < 4; ++ni)
+#pragma unroll
+          for (int q = 0; q < 2; ++q) {
+            const int nl = wn + ni * 8 + lc * 2 + q;
+            cv[mi][ni][q] = (rowok[mi] && colok[ni][q]) ? rb[(long long)nl * P.C.ld + srow[mi]] : make_double2(0.0, 0.0);
+          }
+    }
 #pragma unroll
     for (int mi = 0; mi < 4; ++mi)
 #pragma unroll

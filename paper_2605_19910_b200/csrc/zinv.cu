@@ -68,6 +68,10 @@ int panel_kind() {
 // The panel is latency-bound and on the critical path of the sweep: launched at the
 // greatest stream priority so its CTAs take SMs ahead of queued GEMM tiles of the
 // other stream group (BBSI_PANEL_PRIORITY=0: lowest).
+// Pair kernel: panel 2's pivot rows get their own prefetch buffer when two NB x (n+2)
+// staging buffers fit next to the static shared memory (n <= 320).
+bool pair_pre2(int n) { return 2 * size_t(kNB) * (n + 2) * sizeof(double2) + 40 * 1024 <= 227 * 1024; }
+
 int panel_priority() {
   static int p = [] {
     int lo = 0, hi = 0;
@@ -83,7 +87,8 @@ struct GjScratch {
   int* rowmask;   // [batch][n]  GEMM C rows: r, or -1 on this panel's pivot rows
   int* rowscat;   // [batch][n]  last panel: physical row -> output row
   int* colmap;    // [batch][n]  last panel: column c -> output column lmap[c]
-  double* tol;    // [batch]
+  unsigned long long* amax;  // [batch]  bits of max |a_ij| over the input block (>= 0: ordered as integers)
+  double* piv;    // [batch][n]  |u_jj| of logical column j (tested against the threshold at the end)
   double2* wz;    // [batch][n*nb]  (col-major, ld n)
   double2* vbuf;  // [batch][nb*n]  (col-major, ld nb)
   double2* s0;    // [batch][n*n]   working matrix
@@ -113,7 +118,8 @@ size_t carve(GjScratch& s, void* base, int n, int nb, int batch) {
   s.rowmask = reinterpret_cast<int*>(take(sizeof(int) * size_t(batch) * n));
   s.rowscat = reinterpret_cast<int*>(take(sizeof(int) * size_t(batch) * n));
   s.colmap = reinterpret_cast<int*>(take(sizeof(int) * size_t(batch) * n));
-  s.tol = reinterpret_cast<double*>(take(sizeof(double) * size_t(batch)));
+  s.amax = reinterpret_cast<unsigned long long*>(take(sizeof(unsigned long long) * size_t(batch)));
+  s.piv = reinterpret_cast<double*>(take(sizeof(double) * size_t(batch) * n));
   s.wz = reinterpret_cast<double2*>(take(sizeof(double2) * size_t(batch) * n * 2 * nb));  // two panels
   s.vbuf = reinterpret_cast<double2*>(take(sizeof(double2) * size_t(batch) * 2 * nb * n));
   s.s0 = reinterpret_cast<double2*>(take(sizeof(double2) * size_t(batch) * n * n));
@@ -211,6 +217,22 @@ __device__ __forceinline__ void apply_pinv_dmma(const double2 (*pinv)[NB + 1], d
   }
 }
 
+// The negligible-pivot test |u_jj| <= eps * n_true * max|a| (kernels.hpp:149-158) runs
+// once, in the last panel kernel: every panel stores |u_jj|, and max |a|^2 over the input
+// block comes from the first GJ GEMM, which streams the whole block anyway
+// (ZGemmProblem::amax) -- no separate pass over the matrix on the critical path.
+__device__ __forceinline__ void final_status(const GjScratch& S, int b, int n, int n_true, int* status) {
+  __shared__ int s_first;
+  if (threadIdx.x == 0) s_first = INT_MAX;
+  __syncthreads();
+  const double tol = DBL_EPSILON * double(n_true) * sqrt(__longlong_as_double((long long)S.amax[b]));
+  const double* pv = S.piv + (long long)b * n;
+  for (int i = threadIdx.x; i < n_true; i += PT)
+    if (pv[i] <= tol) atomicMin(&s_first, i);
+  __syncthreads();
+  if (threadIdx.x == 0) *status = s_first == INT_MAX ? -1 : s_first;
+}
+
 // Everything after the pivot search, shared by both panel kernels.
 //   lu[j][c]   pivot row j (logical): L multipliers for c < j, U for c >= j
 //   lloc[r]    panel-local logical row r -> active-list entry
@@ -220,8 +242,8 @@ __device__ __forceinline__ void apply_pinv_dmma(const double2 (*pinv)[NB + 1], d
 template <int NB>
 __device__ __forceinline__ void panel_tail(const double2* __restrict__ cur, long long ld, int n, int n_true, int k, int b,
                                            bool last, const GjScratch& S, int* __restrict__ status,
-                                           const double2 (*lu)[NB + 1], const int* lloc, const int* act, double tol,
-                                           int* s_fail, double2* sv) {
+                                           const double2 (*lu)[NB + 1], const int* lloc, const int* act,
+                                           double2* sv) {
   static_assert(NB == 16, "the warp-level pivot-block inverse assumes NB = 16 (two columns per warp)");
   __shared__ double2 s_uinv[NB];
   __shared__ int s_src[NB];  // physical pivot rows
@@ -234,7 +256,7 @@ __device__ __forceinline__ void panel_tail(const double2* __restrict__ cur, long
   double2* __restrict__ vb = S.vbuf + (long long)b * NB * n;
   if (tid < NB) {
     const double2 d = lu[tid][tid];
-    if (k + tid < n_true && hypot(d.x, d.y) <= tol) atomicMin(s_fail, k + tid);  // kernels.hpp:149-158
+    S.piv[(long long)b * n + k + tid] = hypot(d.x, d.y);  // kernels.hpp:149-158, tested at the end
     s_uinv[tid] = crcp_fast(d);
     s_src[tid] = act[lloc[tid]];
   }
@@ -319,34 +341,13 @@ __device__ __forceinline__ void panel_tail(const double2* __restrict__ cur, long
     }
   }
   __syncthreads();
-  if (tid == 0 && *s_fail != INT_MAX && *status < 0) *status = *s_fail;
+  if (last) final_status(S, b, n, n_true, status);
   ZDBG(9)
 }
 
-// max |a_ij| (hypot) over the true n_true x n_true block -> eps * n_true * max (kernels.hpp:149-158)
-__device__ __forceinline__ double panel_threshold(const double2* __restrict__ cur, long long ld, int n_true,
-                                                  double* red) {
-  const int tid = threadIdx.x, lane = tid & 31, warp = tid >> 5;
-  double mx = 0.0;
-  for (int r = tid; r < n_true; r += PT) {
-#pragma unroll 1
-    for (int c0 = 0; c0 < n_true; c0 += 16) {
-      double2 v[16];
-#pragma unroll
-      for (int u = 0; u < 16; ++u)
-        v[u] = (c0 + u < n_true) ? cur[(long long)(c0 + u) * ld + r] : make_double2(0.0, 0.0);
-#pragma unroll
-      for (int u = 0; u < 16; ++u) mx = fmax(mx, hypot(v[u].x, v[u].y));
-    }
-  }
-#pragma unroll
-  for (int o = 16; o; o >>= 1) mx = fmax(mx, __shfl_xor_sync(0xffffffffu, mx, o));
-  if (lane == 0) red[warp] = mx;
-  __syncthreads();
-  double m = 0.0;
-#pragma unroll
-  for (int q = 0; q < PT / 32; ++q) m = fmax(m, red[q]);
-  return DBL_EPSILON * double(n_true) * m;
+// First panel: reset of the max |a|^2 the first GJ GEMM accumulates.
+__device__ __forceinline__ void panel_threshold_once(int k, int b, const GjScratch& S) {
+  if (k == 0 && threadIdx.x == 0) S.amax[b] = 0ull;
 }
 
 __device__ __forceinline__ void argmax_merge(double& v, int& i, double v2, int i2) {
@@ -367,8 +368,6 @@ __global__ void __launch_bounds__(PT, 1)
   extern __shared__ __align__(16) double2 pn[];  // NB columns x rows (ld = rows + 1), then perm[2][rows], act[rows]
   __shared__ double cand_v[2][PT / 32];
   __shared__ int cand_i[2][PT / 32];
-  __shared__ int s_fail;
-  __shared__ double s_tol;
 
   const int tid = threadIdx.x, lane = tid & 31, warp = tid >> 5;
   const int b = blockIdx.x;
@@ -380,21 +379,11 @@ __global__ void __launch_bounds__(PT, 1)
   int* act = perm + 2 * rows;                          // [rows]
   const int* lmapg = S.lmap + (long long)b * n;
 
-  if (tid == 0) s_fail = INT_MAX;
   for (int r = tid; r < rows; r += PT) {
     act[r] = active_row(lmapg, k, r);
     perm[r] = r;
   }
-  if (k == 0) {
-    const double t = panel_threshold(cur, ld, n_true, cand_v[1]);
-    if (tid == 0) {
-      s_tol = t;
-      S.tol[b] = t;
-      *status = -1;
-    }
-  } else if (tid == 0) {
-    s_tol = S.tol[b];
-  }
+  panel_threshold_once(k, b, S);
   __syncthreads();
   for (int r = tid; r < rows; r += PT) {
     const int ph = act[r];
@@ -405,7 +394,6 @@ __global__ void __launch_bounds__(PT, 1)
     for (int c = 0; c < NB; ++c) pn[c * ldp + r] = v[c];
   }
   __syncthreads();
-  const double tol = s_tol;
 
   // warp-level argmax of |re|+|im| over the rows this thread offers; lane 0 publishes
   auto publish = [&](int par, double bv, int bi) {
@@ -498,7 +486,7 @@ __global__ void __launch_bounds__(PT, 1)
   __shared__ double2 s_lu[NB][NB + 1];
   for (int e = tid; e < NB * NB; e += PT) s_lu[e / NB][e % NB] = pn[(e % NB) * ldp + fperm[e / NB]];
   __syncthreads();
-  panel_tail<NB>(cur, ld, n, n_true, k, b, last != 0, S, status, s_lu, fperm, act, tol, &s_fail, nullptr);
+  panel_tail<NB>(cur, ld, n, n_true, k, b, last != 0, S, status, s_lu, fperm, act, nullptr);
 }
 
 // Pivot-search key: |re|+|im| truncated to sign, exponent and 11 mantissa bits of
@@ -645,21 +633,6 @@ __device__ __forceinline__ void panel_lu_regs(double2 (&a)[RPT][NB], int rows, P
   __syncthreads();
 }
 
-// Threshold (k == 0) or the stored one; status reset on the first panel.
-__device__ __forceinline__ void panel_threshold_once(const double2* cur, long long ld, int n_true, int k, int b,
-                                                     const GjScratch& S, int* status, double* red, double* s_tol) {
-  if (k == 0) {
-    const double t = panel_threshold(cur, ld, n_true, red);
-    if (threadIdx.x == 0) {
-      *s_tol = t;
-      S.tol[b] = t;
-      *status = -1;
-    }
-  } else if (threadIdx.x == 0) {
-    *s_tol = S.tol[b];
-  }
-}
-
 // One panel (at most RPT * PT active rows): register LU + the shared tail.
 template <int NB, int RPT>
 __global__ void __launch_bounds__(PT, 1)
@@ -667,9 +640,6 @@ __global__ void __launch_bounds__(PT, 1)
                          int last, GjScratch S, int* __restrict__ status0, BatchIdx bi) {
   extern __shared__ __align__(16) double2 sv[];  // Vs staging for the tail, NB x (n + 2)
   __shared__ PanelSmem<NB, RPT> sm;
-  __shared__ double s_red[PT / 32];
-  __shared__ int s_fail;
-  __shared__ double s_tol;
   const int tid = threadIdx.x, b = blockIdx.x;
   const double2* __restrict__ cur = cur0 + (k == 0 ? bi.off(b) : (long long)b * bstride);
   int* __restrict__ status = status0 + bi.sidx(b);
@@ -686,12 +656,11 @@ __global__ void __launch_bounds__(PT, 1)
 #pragma unroll
     for (int c = 0; c < NB; ++c) a[i][c] = ok ? cur[(long long)(k + c) * ld + ph] : make_double2(0.0, 0.0);
   }
-  if (tid == 0) s_fail = INT_MAX;
-  panel_threshold_once(cur, ld, n_true, k, b, S, status, s_red, &s_tol);
+  panel_threshold_once(k, b, S);
   ZDBG(1)
   panel_lu_regs<NB, RPT>(a, rows, sm);
   ZDBG(2)
-  panel_tail<NB>(cur, ld, n, n_true, k, b, last != 0, S, status, sm.lu, sm.map, sm.act, s_tol, &s_fail, sv);
+  panel_tail<NB>(cur, ld, n, n_true, k, b, last != 0, S, status, sm.lu, sm.map, sm.act, sv);
 }
 
 // Two consecutive panels K1 = [k, k+NB), K2 = [k+NB, k+2NB) and ONE rank-2NB update
@@ -704,17 +673,15 @@ __global__ void __launch_bounds__(PT, 1)
 template <int NB, int RPT>
 __global__ void __launch_bounds__(PT, 1)
     gj_pair_kernel(const double2* __restrict__ cur0, long long ld, long long bstride, int n, int n_true, int k,
-                   int last, GjScratch S, int* __restrict__ status0, BatchIdx bi) {
+                   int last, GjScratch S, int* __restrict__ status0, BatchIdx bi, int pre2) {
   constexpr int W2 = 2 * NB;
-  extern __shared__ __align__(16) double2 sv[];  // NB x (n + 2): Vs1 / V1, then Vs2 / V2
+  extern __shared__ __align__(16) double2 sv[];  // NB x (n + 2): Vs1 / V1, then Vs2 / V2; then sv2
+  double2* const sv2 = pre2 ? sv + NB * (n + 2) : nullptr;  // NB x (n + 2): pivot rows P2 of M
   __shared__ PanelSmem<NB, RPT> sm;
   __shared__ double2 s_pinv[NB][NB + 1];
   __shared__ double2 s_uinv[NB];
   __shared__ double2 s_wz1p2[NB][NB + 1];  // Wz1 on the rows P2
   __shared__ int s_src1[NB], s_src2[NB];
-  __shared__ double s_red[PT / 32];
-  __shared__ int s_fail;
-  __shared__ double s_tol;
   const int tid = threadIdx.x, b = blockIdx.x;
   const double2* __restrict__ cur = cur0 + (k == 0 ? bi.off(b) : (long long)b * bstride);
   int* __restrict__ status = status0 + bi.sidx(b);
@@ -723,7 +690,7 @@ __global__ void __launch_bounds__(PT, 1)
   int* __restrict__ rowmask = S.rowmask + (long long)b * n;
   double2* __restrict__ wz = S.wz + (long long)b * n * W2;  // [W2][n], ld n
   double2* __restrict__ vb = S.vbuf + (long long)b * W2 * n;  // [n][W2], ld W2
-  if (tid == 0) s_fail = INT_MAX;
+  if (k == 0 && tid == 0) S.amax[b] = 0ull;  // the first GJ GEMM accumulates max |a|^2
   ZDBG(10)
 
   // Both panels run through the same loop body (one copy of the unrolled elimination
@@ -745,13 +712,12 @@ __global__ void __launch_bounds__(PT, 1)
 #pragma unroll
       for (int c = 0; c < NB; ++c) a[i][c] = ok ? src[(long long)c * sld + phys] : make_double2(0.0, 0.0);
     }
-    if (ph == 0) panel_threshold_once(cur, ld, n_true, k, b, S, status, s_red, &s_tol);
     ZDBG(11 + 10 * ph)
     panel_lu_regs<NB, RPT>(a, rows, sm);
     ZDBG(12 + 10 * ph)
     if (tid < NB) {
       const double2 d = sm.lu[tid][tid];
-      if (kk + tid < n_true && hypot(d.x, d.y) <= s_tol) atomicMin(&s_fail, kk + tid);  // kernels.hpp:149-158
+      S.piv[(long long)b * n + kk + tid] = hypot(d.x, d.y);  // kernels.hpp:149-158, tested at the end
       s_uinv[tid] = crcp_fast(d);
       s_src[tid] = sm.act[sm.map[tid]];
     }
@@ -769,19 +735,25 @@ __global__ void __launch_bounds__(PT, 1)
       }
     }
     ZDBG(14 + 10 * ph)
+    // the pivot rows of M this panel needs (Vs1 into sv; panel 2's raw rows into sv2)
+    // are copied asynchronously so that the loads overlap the pivot-block inverse
+    for (int col = tid; col < n; col += PT) {
+      const bool k1c = col >= k && col < k2, k2c = col >= k2 && col < k2 + NB;
+      double2* dst = ph ? sv2 : sv;
+#pragma unroll
+      for (int j = 0; j < NB; ++j) {
+        if (ph == 0 && k1c)
+          dst[j * svld + col] = make_double2(col - k == j ? 1.0 : 0.0, 0.0);
+        else if (ph == 0 || (pre2 && !(k1c || k2c)))
+          cp_async16(&dst[j * svld + col], &cur[(long long)col * ld + s_src[j]]);
+      }
+    }
+    cp_async_commit();
     pivot_block_inverse<NB>(sm.lu, s_uinv, s_pinv);
     ZDBG(15 + 10 * ph)
-    if (ph == 1) break;
-    for (int col = tid; col < n; col += PT) {  // Vs1: pivot rows of M, identity on K1
-      const bool kc = col >= k && col < k2;
-      double2 x[NB];
-#pragma unroll
-      for (int j = 0; j < NB; ++j)
-        x[j] = kc ? make_double2(col - k == j ? 1.0 : 0.0, 0.0) : cur[(long long)col * ld + s_src1[j]];
-#pragma unroll
-      for (int j = 0; j < NB; ++j) sv[j * svld + col] = x[j];
-    }
+    cp_async_wait<0>();
     __syncthreads();
+    if (ph == 1) break;
     ZDBG(16)
     apply_pinv_dmma<NB>(s_pinv, sv, svld, n, nullptr, 0);  // sv = V1
     __syncthreads();
@@ -826,7 +798,7 @@ __global__ void __launch_bounds__(PT, 1)
       v1[j] = sv[j * svld + col];
       vb[(long long)col * W2 + j] = c2 ? make_double2(0.0, 0.0) : v1[j];
       x[j] = c2 ? make_double2(col - k2 == j ? 1.0 : 0.0, 0.0)
-                : (c1 ? make_double2(0.0, 0.0) : cur[(long long)col * ld + s_src2[j]]);
+                : (c1 ? make_double2(0.0, 0.0) : (pre2 ? sv2[j * svld + col] : cur[(long long)col * ld + s_src2[j]]));
     }
     if (!c2) {
 #pragma unroll 1
@@ -857,7 +829,7 @@ __global__ void __launch_bounds__(PT, 1)
     }
   }
   __syncthreads();
-  if (tid == 0 && s_fail != INT_MAX && *status < 0) *status = s_fail;
+  if (last) final_status(S, b, n, n_true, status);
   ZDBG(28)
 }
 
@@ -896,8 +868,10 @@ cudaError_t zinv_batched2(double2* M, long long ld, long long bstride, int n, in
   if (rows_smem > attr_rows) {
     const void* fns[4] = {(const void*)gj_panel_rows_kernel<kNB, 1>, (const void*)gj_panel_rows_kernel<kNB, 2>,
                           (const void*)gj_pair_kernel<kNB, 1>, (const void*)gj_pair_kernel<kNB, 2>};
-    for (const void* f : fns)
-      if ((e = cudaFuncSetAttribute(f, cudaFuncAttributeMaxDynamicSharedMemorySize, int(rows_smem)))) return e;
+    for (int i = 0; i < 4; ++i)
+      if ((e = cudaFuncSetAttribute(fns[i], cudaFuncAttributeMaxDynamicSharedMemorySize,
+                                    int((i >= 2 && pair_pre2(n) ? 2 : 1) * rows_smem))))
+        return e;
     attr_rows = rows_smem;
   }
   const long long nn = (long long)n * n;
@@ -926,10 +900,12 @@ cudaError_t zinv_batched2(double2* M, long long ld, long long bstride, int n, in
       attr_[0].val.priority = panel_priority();
       cfg.attrs = attr_;
       cfg.numAttrs = 1;
+      const int pre2 = pair_pre2(n) ? 1 : 0;
+      if (pair && pre2) cfg.dynamicSmemBytes = 2 * rows_smem;  // Vs staging + panel 2's pivot rows
       if (pair && rows <= PT) {
-        e = cudaLaunchKernelEx(&cfg, gj_pair_kernel<kNB, 1>, cur, cld, cbs, n, n_true, k, last, S, status, bi);
+        e = cudaLaunchKernelEx(&cfg, gj_pair_kernel<kNB, 1>, cur, cld, cbs, n, n_true, k, last, S, status, bi, pre2);
       } else if (pair) {
-        e = cudaLaunchKernelEx(&cfg, gj_pair_kernel<kNB, 2>, cur, cld, cbs, n, n_true, k, last, S, status, bi);
+        e = cudaLaunchKernelEx(&cfg, gj_pair_kernel<kNB, 2>, cur, cld, cbs, n, n_true, k, last, S, status, bi, pre2);
       } else if (kind != 2 && rows <= PT) {
         e = cudaLaunchKernelEx(&cfg, gj_panel_rows_kernel<kNB, 1>, cur, cld, cbs, n, n_true, k, last, S, status, bi);
       } else if (kind != 2 && rows <= 2 * PT) {
@@ -968,6 +944,10 @@ cudaError_t zinv_batched2(double2* M, long long ld, long long bstride, int n, in
       p.zr0 = p.zr1 = 0;
       p.zc0 = k;
       p.zc1 = k + kw;
+      if (k == 0) {  // completes max |a| of the input block for the deferred pivot test
+        p.amax = S.amax + so;
+        p.amax_n = n_true;
+      }
     }
     if ((e = zgemm_grouped(g, stream))) return e;
     k += kw;

@@ -26,12 +26,16 @@ def main():
     H = torch.empty((l, 2 * w + 1, b, b), dtype=torch.complex128, device="cuda")
     D.fill_h_device(cfg, H)
     G = torch.empty((cfg.n_energy, l, 2 * w + 1, b, b), dtype=torch.complex128, device="cuda")
+    from paper_2605_19910_b200._native import lib
+
     for r in range(a.reps):
         torch.cuda.synchronize()
+        n0 = lib().bbsi_cuda_launch_count()
         t0 = time.perf_counter()
         D.solve_device(cfg, H, G)
         torch.cuda.synchronize()
-        print(f"rep {r}: {1e3 * (time.perf_counter() - t0):.2f} ms", flush=True)
+        print(f"rep {r}: {1e3 * (time.perf_counter() - t0):.2f} ms, {lib().bbsi_cuda_launch_count() - n0} launches",
+              flush=True)
 
 
 if __name__ == "__main__":
