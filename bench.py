@@ -8,6 +8,9 @@ BASELINE names no dataset). A "step" is the selected inversion of all 64 energie
 (strong scaling, no data-path collective).
 
   python bench.py [--gpus N] [--steps K] [--warmup W] [--config 2] [--impl ours|reference]
+  python bench.py --config 4 [--domains P]     DDRGF of config 4 (one energy), P domains
+                                                sharded over the ranks (NCCL all-gather of
+                                                the corner packets, distributed.py)
 
 Prints ONE JSON line (rank 0). Keys beyond the driver contract:
   roofline      dominant kernel (the DMMA GEMM) vs the FP64 DMMA peak measured live
@@ -45,6 +48,7 @@ def parse():
     p.add_argument("--impl", default="ours", choices=["ours", "reference"])
     p.add_argument("--no-e2e", action="store_true")
     p.add_argument("--no-cpu-baseline", action="store_true")
+    p.add_argument("--domains", type=int, default=0, help="config 4: DDRGF domains (0 = max(32, world))")
     p.add_argument("--chunk", type=int, default=0, help="energy chunk of the e2e path (0 = library default: ~32 energies per chunk from 48 energies up)")
     return p.parse_args()
 
@@ -342,6 +346,82 @@ def run_ours(args, rank, world, local_rank):
         print(json.dumps(line), flush=True)
 
 
+# ---------------------------------------------------------------------------- DDRGF arm (config 4)
+def run_ddrgf(args, rank, world, local_rank):
+    """Config 4 (l = 4096, b = 256, E = 0.1, one energy): stabilised DDRGF with P domains,
+    contiguous task ranges per rank; the only collective is the all-gather of the
+    per-task interface packets (paper_2605_19910_b200/distributed.py). Strong scaling."""
+    import torch
+    import torch.distributed as dist
+
+    from paper_2605_19910_b200 import distributed as Dd
+    from paper_2605_19910_b200 import dyson as D
+    from paper_2605_19910_b200._native import lib
+
+    L = lib()
+    dev = torch.device("cuda", local_rank)
+    torch.cuda.set_device(dev)
+    cfg = D.CONFIGS[args.config]
+    l, b = cfg.num_layers, cfg.block_size
+    P = args.domains or max(32, world)
+    s2 = -(-l // P) - 1
+    tasks = Dd.partition(l, s2)
+    t0, t1 = Dd.task_ranges(len(tasks), world)[rank]
+    L0, L1 = Dd.layer_range(tasks, t0, t1)
+    H = torch.empty((l, 3, b, b), dtype=torch.complex128, device=dev)
+    D.fill_h_device(cfg, H)
+    A = -H[L0:L1].clone()  # this rank's band rows of A = z I - H - Sigma (slot order)
+    del H
+    z = complex(cfg.z()[0])
+    sig = torch.from_numpy(np.asarray(cfg.sigma()[L0:L1], dtype=np.complex128)).to(dev)
+    dg = A[:, 1].diagonal(dim1=-2, dim2=-1)
+    dg.copy_((dg + z) - sig[:, None])  # (z - H_aa) - sigma_a, the order of csrc/band_ops.cu
+    stream = torch.cuda.Stream(device=dev)
+    torch.cuda.set_stream(stream)
+
+    def step():
+        return Dd.ddrgf_distributed(A, l, b, s2)
+
+    def barrier():
+        if world > 1:
+            dist.barrier()
+
+    for _ in range(max(3, args.warmup)):
+        step()
+    torch.cuda.synchronize()
+    barrier()
+    n0 = L.bbsi_cuda_launch_count()
+    e0, e1 = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
+    with ClockSampler(local_rank) as clocks:
+        e0.record(stream)
+        for _ in range(args.steps):
+            step()
+        e1.record(stream)
+        torch.cuda.synchronize()
+    barrier()
+    ms = e0.elapsed_time(e1)
+    launches = L.bbsi_cuda_launch_count() - n0
+    if world > 1:
+        t = torch.tensor([ms], device=dev, dtype=torch.float64)
+        dist.all_reduce(t, op=dist.ReduceOp.MAX)
+        ms = float(t.item())
+    ms_step = ms / args.steps
+    flops = D.algorithmic_flops(cfg)
+    if rank == 0:
+        line = {"metric": METRIC, "value": l / (ms_step * 1e-3), "unit": UNIT, "n_gpus": world,
+                "steps": args.steps, "warmup": max(3, args.warmup), "ms_per_step": ms_step,
+                "higher_is_better": True, "scaling": "strong", "vs_baseline": None, "dtype": "c128 (f64)",
+                "data": "synthetic (seeded Dyson generator, csrc/dyson_gen.h)",
+                "config": {"workload": cfg.name, "num_layers": l, "block_size": b, "bandwidth": 1, "energies": 1,
+                           "eta": cfg.eta, "seed": cfg.seed, "solver": "stabilised ddrgf (DESIGN.md section 5)",
+                           "domains": len(tasks), "s2": s2,
+                           "parallelism": f"ddrgf domains over {world} rank(s), NCCL all-gather of the corner packets",
+                           "l2": "inputs larger than L2 (A band 12 GiB)"},
+                "tflops_rgf_equivalent": flops / (ms_step * 1e-3) / 1e12, "gpu_launches": int(launches),
+                "clocks": clocks.summary(), "roofline": None, "e2e": None, "cpu_baseline": None}
+        print(json.dumps(line), flush=True)
+
+
 def main():
     args = parse()
     world = int(os.environ.get("WORLD_SIZE", "1"))
@@ -356,7 +436,10 @@ def main():
 
         torch.cuda.set_device(local_rank)
         dist.init_process_group("nccl", device_id=torch.device("cuda", local_rank))
-    run_ours(args, rank, world, local_rank)
+    if args.config == 4:
+        run_ddrgf(args, rank, world, local_rank)
+    else:
+        run_ours(args, rank, world, local_rank)
     if world > 1:
         import torch.distributed as dist
 

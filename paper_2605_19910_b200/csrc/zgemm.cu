@@ -60,7 +60,9 @@ __device__ __forceinline__ void load_tile(const ZGemmProblem& P, int bs, int bat
 
 // MINB = resident CTAs per SM the register budget is sized for (2: 243 regs, no
 // spills; 3: 168 regs, 12 warps per SM, a few epilogue spills).
-template <bool PLAIN, int MINB>
+// AMAX: the first Gauss-Jordan step's variant (max |C|^2, ZGemmProblem::amax); a
+// separate instantiation so the other launches keep their register allocation.
+template <bool PLAIN, int MINB, bool AMAX = false>
 __global__ void __launch_bounds__(128, MINB) zgemm_grouped_kernel(const __grid_constant__ ZGemmGroup g) {
   extern __shared__ __align__(16) double2 smem[];
   double2* As = smem;
@@ -121,7 +123,7 @@ __global__ void __launch_bounds__(128, MINB) zgemm_grouped_kernel(const __grid_c
       }
     const double2* __restrict__ rb = rmap ? cb + (long long)n0 * P.C.ld : ct;
     double2 cv[4][4][2];
-    if (PLAIN && P.amax) {
+    if (AMAX && PLAIN && P.amax) {
       // first Gauss-Jordan step (identity row map): the whole tile as stored is read in
       // the same batch of loads -- masked entries only feed max |C_ij|^2 (rows, columns
       // < amax_n), the accumulator takes them as 0
@@ -183,7 +185,8 @@ __global__ void __launch_bounds__(128, MINB) zgemm_grouped_kernel(const __grid_c
 #pragma unroll 1
   for (int kc = 0; kc < nk; ++kc) {
     const int s = kc & 1;
-    if (kc + 1 < nk) load_tile<PLAIN>(P, bs, batch, m0, n0, (kc + 1) * BK, As + (s ^ 1) * A_STAGE, Bs + (s ^ 1) * B_STAGE, tid);
+    if (kc + 1 < nk)
+      load_tile<PLAIN>(P, bs, batch, m0, n0, (kc + 1) * BK, As + (s ^ 1) * A_STAGE, Bs + (s ^ 1) * B_STAGE, tid);
     cp_async_commit();
     cp_async_wait<1>();
     __syncthreads();
@@ -314,13 +317,13 @@ int gemm_minb() {
   return m;
 }
 
-template <bool PLAIN, int MINB>
+template <bool PLAIN, int MINB, bool AMAX = false>
 cudaError_t gemm_attrs() {
   static cudaError_t e = [] {
-    cudaError_t r = cudaFuncSetAttribute(zgemm_grouped_kernel<PLAIN, MINB>, cudaFuncAttributeMaxDynamicSharedMemorySize,
+    cudaError_t r = cudaFuncSetAttribute(zgemm_grouped_kernel<PLAIN, MINB, AMAX>, cudaFuncAttributeMaxDynamicSharedMemorySize,
                                          SMEM_BYTES);
     if (r == cudaSuccess)
-      r = cudaFuncSetAttribute(zgemm_grouped_kernel<PLAIN, MINB>, cudaFuncAttributePreferredSharedMemoryCarveout,
+      r = cudaFuncSetAttribute(zgemm_grouped_kernel<PLAIN, MINB, AMAX>, cudaFuncAttributePreferredSharedMemoryCarveout,
                                cudaSharedmemCarveoutMaxShared);
     return r;
   }();
@@ -352,7 +355,12 @@ cudaError_t zgemm_grouped(ZGemmGroup& g, cudaStream_t stream) {
   ProfScope prof(stream, g.prof_cat ? g.prof_cat : PROF_GEMM, fl, by);
   cudaError_t e;
   const bool three = gemm_minb() == 3;
-  if (plain && three) {
+  bool amax = false;
+  for (int p = 0; p < g.nprob; ++p) amax |= g.prob[p].amax != nullptr;
+  if (plain && amax) {
+    if ((e = gemm_attrs<true, 3, true>())) return e;
+    zgemm_grouped_kernel<true, 3, true><<<total, 128, SMEM_BYTES, stream>>>(g);
+  } else if (plain && three) {
     if ((e = gemm_attrs<true, 3>())) return e;
     zgemm_grouped_kernel<true, 3><<<total, 128, SMEM_BYTES, stream>>>(g);
   } else if (plain) {
