@@ -281,9 +281,10 @@ def run_ours(args, rank, world, local_rank):
     roofline = {"bound": "tensor", "kernel": "zgemm_grouped_kernel (DMMA f64), sweep launches "
                 "(its Gauss-Jordan launches are listed as gj_gemm)", "achieved": g["tflops"],
                 "peak": round(peak, 2), "unit": "TFLOP/s", "frac": round(g["tflops"] / peak, 4) if peak > 0 else None,
-                # dram read + write of one sweep-GEMM launch (2048 tiles) from the ncu
-                # --set full capture in profiles/r01_ncu_zgemm.md
-                "traffic": 436.73e6, "traffic_unit": "bytes per launch (win+um, 2048 tiles)",
+                # dram read + write of one sweep-GEMM launch (window + um of both chains of
+                # one 32-energy stream group, 2048 tiles) from the ncu --set full capture
+                # in profiles/r01_ncu_kernels.md
+                "traffic": 297.07e6, "traffic_unit": "bytes per launch (win+um, 2048 tiles)",
                 "peak_source": "FP64 DMMA peak measured live in this run (bbsi_cuda_fp64_peak_tflops; "
                                "MEASURED_PEAKS.json has no FP64 entry)",
                 "share_of_step": round(g["ms"] / step_kernel_ms, 3) if step_kernel_ms else None,

@@ -26,6 +26,7 @@
 // All chains live in the output band itself (domain i + separator i occupy a
 // contiguous run of slots with a uniform stride), so no extra band buffers exist.
 #include <algorithm>
+#include <mutex>
 #include <vector>
 
 #include "internal.h"
@@ -327,7 +328,33 @@ cudaError_t ddrgf_phase1(const double2* A, double2* G, int l, int b, const int* 
 }
 
 // Phase 2 (redundant on every rank): left-/right-connected sweeps over all T
-// separators from the gathered packets.
+// separators from the gathered packets. The right-connected recursion does not depend
+// on the left sweep, so it runs on a side stream concurrently with it (each step is a
+// chain of b x b inversions, latency-bound at batch 1); the separator G[s,s] =
+// (A[s,s] - Sigma^R - Sigma^L_sep)^{-1}, the only quantity that needs both, is then one
+// inversion launch over all T separators.
+namespace {
+struct SideStream {
+  cudaStream_t s = nullptr;
+  cudaEvent_t fork = nullptr, join = nullptr;
+};
+SideStream& side_stream() {
+  static std::mutex mu;
+  static std::vector<SideStream> per_dev;
+  std::lock_guard<std::mutex> lk(mu);
+  int dev = 0;
+  cudaGetDevice(&dev);
+  if (int(per_dev.size()) <= dev) per_dev.resize(dev + 1);
+  SideStream& x = per_dev[dev];
+  if (!x.s) {
+    cudaStreamCreateWithFlags(&x.s, cudaStreamNonBlocking);
+    cudaEventCreateWithFlags(&x.fork, cudaEventDisableTiming);
+    cudaEventCreateWithFlags(&x.join, cudaEventDisableTiming);
+  }
+  return x;
+}
+}  // namespace
+
 cudaError_t ddrgf_phase2(const double2* packets, int l, int b, const int* n_true, int s2, double gamma, double2* out,
                          int* fail_layer, cudaStream_t s) {
   *fail_layer = -1;
@@ -339,109 +366,138 @@ cudaError_t ddrgf_phase2(const double2* packets, int l, int b, const int* n_true
   const double2 ig = make_double2(0.0, gamma);
   const double2 m1 = make_double2(-1.0, 0.0);
   cudaError_t e;
-  // scratch: gL, gLdom, SigmaLsep per task, gR (current), 8 temporaries
-  double2* scr = static_cast<double2*>(arena_get(13, (size_t(3) * T + 10) * bb * sizeof(double2)));
+  // scratch: gL, gLdom, SigmaLsep per task, then 8 temporaries per stream (+1 for gR)
+  constexpr int NT = 8;
+  double2* scr = static_cast<double2*>(arena_get(13, (size_t(3) * T + 2 * NT + 1) * bb * sizeof(double2)));
   const int max_inv = 8 * T + 4;
   void* inv_scr = arena_get(7, zinv_scratch_bytes(b, 1) + 256);
-  int* st = static_cast<int*>(arena_get(8, sizeof(int) * size_t(max_inv)));
-  if (!scr || !inv_scr || !st) return cudaErrorMemoryAllocation;
+  void* inv_scr2 = arena_get(17, zinv_scratch_bytes(b, T) + 256);  // side stream; then the batched G[s,s]
+  int* st = static_cast<int*>(arena_get(8, sizeof(int) * size_t(max_inv + T)));
+  if (!scr || !inv_scr || !inv_scr2 || !st) return cudaErrorMemoryAllocation;
+  SideStream& side = side_stream();
   auto gL = [&](int t) { return scr + (size_t)t * bb; };
   auto gLD = [&](int t) { return scr + ((size_t)T + t) * bb; };
   auto SLs = [&](int t) { return scr + ((size_t)2 * T + t) * bb; };
-  double2* gR = scr + (size_t)3 * T * bb;
-  auto Tm = [&](int i) { return scr + ((size_t)3 * T + 1 + i) * bb; };
+  double2* gR = scr + ((size_t)3 * T + 2 * NT) * bb;
   std::vector<int> st_layer;
-  auto inv = [&](double2* m, int layer) -> cudaError_t {
+  // the block operations of one stream: temporaries Tm(0..NT-1) of that stream
+  struct Ops {
+    cudaStream_t s;
+    double2* tm0;
+    void* iscr;
+    long long bb;
+    double2* Tm(int i) const { return tm0 + (size_t)i * bb; }
+  };
+  const Ops L{s, scr + (size_t)3 * T * bb, inv_scr, bb};
+  const Ops R{side.s, scr + ((size_t)3 * T + NT) * bb, inv_scr2, bb};
+  auto inv = [&](const Ops& q, double2* m, int layer) -> cudaError_t {
     if (int(st_layer.size()) >= max_inv) return cudaErrorInvalidValue;
     int* slot = st + st_layer.size();
     st_layer.push_back(layer);
-    return zinv_batched(m, b, bb, b, n_true ? n_true[layer] : b, 1, inv_scr, slot, s);
+    return zinv_batched(m, b, bb, b, n_true ? n_true[layer] : b, 1, q.iscr, slot, q.s);
   };
-  auto ident = [&](double2* m) -> cudaError_t {
-    cudaError_t e2 = cudaMemsetAsync(m, 0, bb * sizeof(double2), s);
-    return e2 ? e2 : diag_add(m, 0, b, 1, make_double2(1.0, 0.0), s);
+  auto ident = [&](const Ops& q, double2* m) -> cudaError_t {
+    cudaError_t e2 = cudaMemsetAsync(m, 0, bb * sizeof(double2), q.s);
+    return e2 ? e2 : diag_add(m, 0, b, 1, make_double2(1.0, 0.0), q.s);
   };
-  auto copy = [&](double2* d, const double2* x) {
-    return cudaMemcpyAsync(d, x, bb * sizeof(double2), cudaMemcpyDeviceToDevice, s);
+  auto copy = [&](const Ops& q, double2* d, const double2* x) {
+    return cudaMemcpyAsync(d, x, bb * sizeof(double2), cudaMemcpyDeviceToDevice, q.s);
   };
-  auto mm3 = [&](double2* d, double alpha, const double2* x, const double2* y, const double2* z) -> cudaError_t {
+  auto mm3 = [&](const Ops& q, double2* d, double alpha, const double2* x, const double2* y,
+                 const double2* z) -> cudaError_t {
     // d = alpha * x * y * z  (via Tm(7))
-    cudaError_t e2 = mm(b, 1, 1.0, blk(x, b), blk(y, b), 0.0, blk(Tm(7), b), s);
-    return e2 ? e2 : mm(b, 1, alpha, blk(Tm(7), b), blk(z, b), 0.0, blk(d, b), s);
+    cudaError_t e2 = mm(b, 1, 1.0, blk(x, b), blk(y, b), 0.0, blk(q.Tm(7), b), q.s);
+    return e2 ? e2 : mm(b, 1, alpha, blk(q.Tm(7), b), blk(z, b), 0.0, blk(d, b), q.s);
   };
   // out = x + i*gamma x (I - i*gamma x)^{-1} x   (removes the fake lead at the block of x)
-  auto remove_fake = [&](double2* o_, const double2* x, int layer) -> cudaError_t {
+  auto remove_fake = [&](const Ops& q, double2* o_, const double2* x, int layer) -> cudaError_t {
     cudaError_t e2;
-    if ((e2 = ident(Tm(2)))) return e2;
-    if ((e2 = axpy(Tm(2), x, bb, make_double2(0.0, -gamma), s))) return e2;
-    if ((e2 = inv(Tm(2), layer))) return e2;
-    if ((e2 = mm(b, 1, 1.0, blk(Tm(2), b), blk(x, b), 0.0, blk(Tm(3), b), s))) return e2;
-    if ((e2 = copy(o_, x))) return e2;
-    return mmz(b, make_double2(0.0, gamma), blk(x, b), blk(Tm(3), b), 1.0, blk(o_, b), s);
+    if ((e2 = ident(q, q.Tm(2)))) return e2;
+    if ((e2 = axpy(q.Tm(2), x, bb, make_double2(0.0, -gamma), q.s))) return e2;
+    if ((e2 = inv(q, q.Tm(2), layer))) return e2;
+    if ((e2 = mm(b, 1, 1.0, blk(q.Tm(2), b), blk(x, b), 0.0, blk(q.Tm(3), b), q.s))) return e2;
+    if ((e2 = copy(q, o_, x))) return e2;
+    return mmz(b, make_double2(0.0, gamma), blk(x, b), blk(q.Tm(3), b), 1.0, blk(o_, b), q.s);
   };
-  // ---- left sweep
+  if ((e = cudaEventRecord(side.fork, s)) || (e = cudaStreamWaitEvent(side.s, side.fork, 0))) return e;
+  // ---- right-connected recursion (side stream): Sigma^R, Y_t, and pre_t = A[s,s] - Sigma^R in OGSS
+  for (int t = T - 1; t >= 0; --t) {
+    const int sp = P.sep[t], cnt = P.count[t];
+    if (t < T - 1) {
+      if ((e = mm3(R, o(t, OSR), 1.0, pk(t, PASN), o(t + 1, OY), pk(t + 1, PAX0)))) return e;
+    } else if ((e = cudaMemsetAsync(o(t, OSR), 0, bb * sizeof(double2), R.s))) {
+      return e;
+    }
+    // pre = A[s,s] - Sigma^R ; gR = pre^{-1}
+    if ((e = copy(R, gR, pk(t, PASS)))) return e;
+    if ((e = axpy(gR, o(t, OSR), bb, m1, R.s))) return e;
+    if ((e = copy(R, o(t, OGSS), gR))) return e;
+    if ((e = inv(R, gR, sp))) return e;
+    if (cnt > 0) {
+      const int last = P.first[t] + cnt - 1;
+      double2* Dl = R.Tm(1);
+      if ((e = mm3(R, Dl, 1.0, pk(t, PALS), gR, pk(t, PASL)))) return e;
+      if ((e = diag_add(Dl, 0, b, 1, ig, R.s))) return e;
+      if ((e = ident(R, R.Tm(2)))) return e;
+      if ((e = mm(b, 1, -1.0, blk(Dl, b), blk(pk(t, PE), b), 1.0, blk(R.Tm(2), b), R.s))) return e;
+      if ((e = inv(R, R.Tm(2), last))) return e;
+      if ((e = mm(b, 1, 1.0, blk(R.Tm(2), b), blk(Dl, b), 0.0, blk(R.Tm(3), b), R.s))) return e;
+      if ((e = mm(b, 1, 1.0, blk(R.Tm(3), b), blk(pk(t, PC), b), 0.0, blk(R.Tm(4), b), R.s))) return e;
+      if ((e = copy(R, R.Tm(5), pk(t, PA)))) return e;
+      if ((e = mm(b, 1, 1.0, blk(pk(t, PB), b), blk(R.Tm(4), b), 1.0, blk(R.Tm(5), b), R.s))) return e;
+      if ((e = remove_fake(R, o(t, OY), R.Tm(5), P.first[t]))) return e;
+    } else if ((e = copy(R, o(t, OY), gR))) {
+      return e;
+    }
+  }
+  if ((e = cudaEventRecord(side.join, R.s))) return e;
+  // ---- left sweep (main stream)
   for (int t = 0; t < T; ++t) {
     const int f = P.first[t], cnt = P.count[t], sp = P.sep[t];
     if (cnt > 0) {
       // Sigma^L on the first block (from separator t-1); Df = Sigma^L - Sigma0
-      double2* Df = Tm(1);
+      double2* Df = L.Tm(1);
       if (t > 0) {
-        if ((e = mm3(o(t, OSL), 1.0, pk(t, PAX0), gL(t - 1), pk(t - 1, PASN)))) return e;
+        if ((e = mm3(L, o(t, OSL), 1.0, pk(t, PAX0), gL(t - 1), pk(t - 1, PASN)))) return e;
       } else if ((e = cudaMemsetAsync(o(t, OSL), 0, bb * sizeof(double2), s))) {
         return e;
       }
-      if ((e = copy(Df, o(t, OSL)))) return e;
+      if ((e = copy(L, Df, o(t, OSL)))) return e;
       if ((e = diag_add(Df, 0, b, 1, ig, s))) return e;
       // e' = e + c (I - Df a)^{-1} Df b
-      if ((e = ident(Tm(2)))) return e;
-      if ((e = mm(b, 1, -1.0, blk(Df, b), blk(pk(t, PA), b), 1.0, blk(Tm(2), b), s))) return e;
-      if ((e = inv(Tm(2), f))) return e;
-      if ((e = mm(b, 1, 1.0, blk(Tm(2), b), blk(Df, b), 0.0, blk(Tm(3), b), s))) return e;
-      if ((e = mm(b, 1, 1.0, blk(Tm(3), b), blk(pk(t, PB), b), 0.0, blk(Tm(4), b), s))) return e;
-      if ((e = copy(Tm(5), pk(t, PE)))) return e;
-      if ((e = mm(b, 1, 1.0, blk(pk(t, PC), b), blk(Tm(4), b), 1.0, blk(Tm(5), b), s))) return e;
-      if ((e = remove_fake(gLD(t), Tm(5), f + cnt - 1))) return e;
-      if ((e = mm3(SLs(t), 1.0, pk(t, PASL), gLD(t), pk(t, PALS)))) return e;
+      if ((e = ident(L, L.Tm(2)))) return e;
+      if ((e = mm(b, 1, -1.0, blk(Df, b), blk(pk(t, PA), b), 1.0, blk(L.Tm(2), b), s))) return e;
+      if ((e = inv(L, L.Tm(2), f))) return e;
+      if ((e = mm(b, 1, 1.0, blk(L.Tm(2), b), blk(Df, b), 0.0, blk(L.Tm(3), b), s))) return e;
+      if ((e = mm(b, 1, 1.0, blk(L.Tm(3), b), blk(pk(t, PB), b), 0.0, blk(L.Tm(4), b), s))) return e;
+      if ((e = copy(L, L.Tm(5), pk(t, PE)))) return e;
+      if ((e = mm(b, 1, 1.0, blk(pk(t, PC), b), blk(L.Tm(4), b), 1.0, blk(L.Tm(5), b), s))) return e;
+      if ((e = remove_fake(L, gLD(t), L.Tm(5), f + cnt - 1))) return e;
+      if ((e = mm3(L, SLs(t), 1.0, pk(t, PASL), gLD(t), pk(t, PALS)))) return e;
     } else {
       if (t == 0) return cudaErrorInvalidValue;  // task 0 always has interior layers
-      if ((e = mm3(SLs(t), 1.0, pk(t, PASL), gL(t - 1), pk(t - 1, PASN)))) return e;
-      if ((e = copy(o(t, OSL), SLs(t)))) return e;  // the chain's only block is the separator
+      if ((e = mm3(L, SLs(t), 1.0, pk(t, PASL), gL(t - 1), pk(t - 1, PASN)))) return e;
+      if ((e = copy(L, o(t, OSL), SLs(t)))) return e;  // the chain's only block is the separator
     }
-    if ((e = copy(gL(t), pk(t, PASS)))) return e;
+    if ((e = copy(L, gL(t), pk(t, PASS)))) return e;
     if ((e = axpy(gL(t), SLs(t), bb, m1, s))) return e;
-    if ((e = inv(gL(t), sp))) return e;
+    if ((e = inv(L, gL(t), sp))) return e;
   }
-  // ---- right sweep
-  for (int t = T - 1; t >= 0; --t) {
-    const int sp = P.sep[t], cnt = P.count[t];
-    if (t < T - 1) {
-      if ((e = mm3(o(t, OSR), 1.0, pk(t, PASN), o(t + 1, OY), pk(t + 1, PAX0)))) return e;
-    } else if ((e = cudaMemsetAsync(o(t, OSR), 0, bb * sizeof(double2), s))) {
-      return e;
-    }
-    // pre = A[s,s] - Sigma^R ; G[s,s] = (pre - Sigma^L_sep)^{-1} ; gR = pre^{-1}
-    if ((e = copy(gR, pk(t, PASS)))) return e;
-    if ((e = axpy(gR, o(t, OSR), bb, m1, s))) return e;
-    if ((e = copy(o(t, OGSS), gR))) return e;
+  // ---- join; G[s,s] = (pre - Sigma^L_sep)^{-1} for every separator in one launch
+  if ((e = cudaStreamWaitEvent(s, side.join, 0))) return e;
+  bool uniform = true;
+  for (int t = 0; t < T; ++t) {
     if ((e = axpy(o(t, OGSS), SLs(t), bb, m1, s))) return e;
-    if ((e = inv(o(t, OGSS), sp))) return e;
-    if ((e = inv(gR, sp))) return e;
-    if (cnt > 0) {
-      const int last = P.first[t] + cnt - 1;
-      double2* Dl = Tm(1);
-      if ((e = mm3(Dl, 1.0, pk(t, PALS), gR, pk(t, PASL)))) return e;
-      if ((e = diag_add(Dl, 0, b, 1, ig, s))) return e;
-      if ((e = ident(Tm(2)))) return e;
-      if ((e = mm(b, 1, -1.0, blk(Dl, b), blk(pk(t, PE), b), 1.0, blk(Tm(2), b), s))) return e;
-      if ((e = inv(Tm(2), last))) return e;
-      if ((e = mm(b, 1, 1.0, blk(Tm(2), b), blk(Dl, b), 0.0, blk(Tm(3), b), s))) return e;
-      if ((e = mm(b, 1, 1.0, blk(Tm(3), b), blk(pk(t, PC), b), 0.0, blk(Tm(4), b), s))) return e;
-      if ((e = copy(Tm(5), pk(t, PA)))) return e;
-      if ((e = mm(b, 1, 1.0, blk(pk(t, PB), b), blk(Tm(4), b), 1.0, blk(Tm(5), b), s))) return e;
-      if ((e = remove_fake(o(t, OY), Tm(5), P.first[t]))) return e;
-    } else if ((e = copy(o(t, OY), gR))) {
+    uniform = uniform && (!n_true || n_true[P.sep[t]] == n_true[P.sep[0]]);
+  }
+  if (uniform) {
+    int* slot = st + st_layer.size();
+    for (int t = 0; t < T; ++t) st_layer.push_back(P.sep[t]);
+    if ((e = zinv_batched(o(0, OGSS), b, NOUT * bb, b, n_true ? n_true[P.sep[0]] : b, T, inv_scr2, slot, s)))
       return e;
-    }
+  } else {
+    for (int t = 0; t < T; ++t)
+      if ((e = inv(L, o(t, OGSS), P.sep[t]))) return e;
   }
   std::vector<int> sh(st_layer.size());
   if ((e = cudaMemcpyAsync(sh.data(), st, sh.size() * sizeof(int), cudaMemcpyDeviceToHost, s))) return e;
