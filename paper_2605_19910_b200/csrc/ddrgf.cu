@@ -251,7 +251,7 @@ cudaError_t ddrgf_phase1(const double2* A, double2* G, int l, int b, const int* 
   e = for_task_runs(P, s2, t0, t1, [&](int t, int nt, int len) -> cudaError_t {
     if (len == 0) return cudaSuccess;
     SweepWork W;
-    cudaError_t e2 = chain_sweeps(X, P, s2, t, nt, len, b, n_true, W, fail_layer, s);
+    cudaError_t e2 = chain_sweeps(X, P, s2, t, nt, len, b, n_true, W, fail_layer, s, true);
     if (e2 || *fail_layer >= 0) return e2;
     // a = G[f,f], e = G[l,l]; b = G[f,l], c = G[l,f] by the first row / column chains
     const long long gs = W.g_bstride;
@@ -271,6 +271,53 @@ cudaError_t ddrgf_phase1(const double2* A, double2* G, int l, int b, const int* 
     }
     double2* pr = rc;
     double2* pc = rc + (size_t)nt * bb;
+    if (sweep_is_two_ended(W)) {
+      // two-ended multipliers (m = len/2): from G[m,m],
+      //   b: G[i, m] = -lm[i] G[i+1, m] (i = m-1 .. 0), then G[0, a] = -G[0, a-1] um[a] (a = m+1 ..)
+      //   c: G[a, m] = -lm[a] G[a-1, m] (a = m+1 ..),   then G[l-1, i] = -G[l-1, i+1] um[i] (i = m-1 .. 0)
+      const int m = len / 2, nr = len - 1 - m;
+      const double2* v = X.gslot(P.first[t] + m, 0);
+      const double2* u = v;
+      long long vs = gs, us = gs;
+      auto mult = [&](const double2* base, int j) { return blk(base + (long long)j * bb, b, (long long)W.l * bb); };
+      for (int st = 0; st < len - 1; ++st) {
+        const bool to_out = ((len - 2 - st) % 2) == 0;  // the last step lands in the packet
+        double2* r_nxt = to_out ? pk(t, PB) : pr;
+        double2* c_nxt = to_out ? pk(t, PC) : pc;
+        const long long nstride = to_out ? PK * bb : bb;
+        ZGemmGroup g{};
+        g.batch = nt;
+        g.bs = 64;
+        g.nprob = 2;
+        ZGemmProblem& p0 = g.prob[0];
+        p0.M = p0.N = p0.K = b;
+        p0.alpha = make_double2(-1.0, 0.0);
+        p0.beta = make_double2(0.0, 0.0);
+        ZGemmProblem& p1 = g.prob[1];
+        p1 = p0;
+        if (st < m) {
+          p0.A = mult(W.LM, m - 1 - st);
+          p0.B = blk(v, b, vs);
+        } else {
+          p0.A = blk(v, b, vs);
+          p0.B = mult(W.UM, m + 1 + (st - m));
+        }
+        p0.C = p0.D = blk(r_nxt, b, nstride);
+        if (st < nr) {
+          p1.A = mult(W.LM, m + 1 + st);
+          p1.B = blk(u, b, us);
+        } else {
+          p1.A = blk(u, b, us);
+          p1.B = mult(W.UM, m - 1 - (st - nr));
+        }
+        p1.C = p1.D = blk(c_nxt, b, nstride);
+        if ((e2 = zgemm_grouped(g, s))) return e2;
+        v = r_nxt;
+        u = c_nxt;
+        vs = us = nstride;
+      }
+      return cudaSuccess;
+    }
     const double2* r_cur = pk(t, PA);
     const double2* c_cur = pk(t, PA);
     long long rstride = PK * bb, cstride = PK * bb;

@@ -66,12 +66,17 @@ struct SweepWork {
   // batch per latency-bound inversion launch and half the sequential steps. Set
   // before sweep_carve (the inversion scratch doubles).
   bool two_ended = false;
+  int lm_layers = 0;      // layers per batch entry of LM / UM (0: l; a sub-band view keeps the parent's)
 };
 
 // Bytes of LM+UM+piv+wz+status for a sweep.
 size_t sweep_scratch_bytes(int l, int w, int bs, int batch, int groups = 1, bool two_ended = false);
 // Two-ended sweeps for Dyson batches (env BBSI_TWO_ENDED=0 turns them off).
 bool two_ended_default();
+// Whether rgf_sweeps runs the two-ended variant for this workspace (two_ended set and
+// the layer count allows it); its multipliers then hold the right chain for layers
+// > m and the left chain (lm = Y A[j, j+1], um = A[j+1, j] Y) for layers < m = l/2 (w = 1).
+bool sweep_is_two_ended(const SweepWork& W);
 // Default number of concurrent batch groups (env BBSI_GROUPS overrides).
 int default_groups(int batch, int bs);
 // Carves the scratch part of a SweepWork out of `base` (>= sweep_scratch_bytes).

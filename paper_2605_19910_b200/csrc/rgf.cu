@@ -46,12 +46,16 @@ bool two_ended_default() {
 }
 
 namespace {
-bool use_two_ended(const SweepWork& W) { return W.two_ended && W.w == 1 && W.l >= 3; }
+bool use_two_ended(const SweepWork& W) {
+  return W.two_ended && ((W.w == 1 && W.l >= 3) || (W.w >= 2 && !W.Hoff && W.l >= 3 * W.w + 2));
+}
 }  // namespace
+
+bool sweep_is_two_ended(const SweepWork& W) { return use_two_ended(W); }
 
 size_t sweep_scratch_bytes(int l, int w, int bs, int batch, int groups, bool two_ended) {
   const size_t bb = size_t(bs) * bs * sizeof(double2);
-  const int chains = (two_ended && w == 1 && l >= 3) ? 2 : 1;
+  const int chains = (two_ended && ((w == 1 && l >= 3) || (w >= 2 && l >= 3 * w + 2))) ? 2 : 1;
   size_t s = 2 * size_t(batch) * l * w * bb;              // LM, UM
   s += size_t(groups) * (zinv_scratch_bytes(bs, chains * ((batch + groups - 1) / groups)) + 256);  // inversion scratch
   s += size_t(l) * batch * sizeof(int) + 256;             // status
@@ -80,7 +84,7 @@ struct Ctx {
   double2* slot(int a, int off) const { return W.G + ((long long)a * nslot + off + W.w) * bb; }
   double2* lm(int j) const { return W.LM + (long long)j * W.w * bb; }
   double2* um(int j) const { return W.UM + (long long)j * W.w * bb; }
-  long long lm_bstride() const { return (long long)W.l * W.w * bb; }
+  long long lm_bstride() const { return (long long)(W.lm_layers > 0 ? W.lm_layers : W.l) * W.w * bb; }
   ZOp gop(const double2* p, long long rs_slots, long long cs_slots) const {
     return ZOp{p, W.bs, rs_slots * bb, cs_slots * bb, W.g_bstride};
   }
@@ -289,6 +293,136 @@ cudaError_t rgf_sweeps_two(const SweepWork& W, const int* n_true, int* status, i
   return flush(0, l, true);
 }
 
+// Two-ended sweep of the block n-diagonal recursion (w >= 2, A's band in G). The
+// right chain of rgf_ndiag (rgf.hpp:98-114) eliminates layers l-1 .. m+w, its mirror
+// eliminates 0 .. m-1 from the top, in lockstep (one inversion launch for both, the
+// products of both in the same grouped launches while their windows are disjoint):
+//   left, layer j:  Y_j = inv(M'[j,j]),  lm[j][t] = Y_j M'[j, j+t],  um[j][t] = M'[j+t, j] Y_j,
+//                   M'[j+s, j+t] -= M'[j+s, j] lm[j][t]          (s, t = 1..w)
+// The w middle layers [m, m+w) then hold the Schur complement of both sides; the
+// one-ended recursion on that w-layer sub-band gives its full inverse, and the two
+// outward sweeps (rgf.hpp:117-135 and its mirror) finish the band:
+//   left, j = m-1 .. 0:  G[j, j+t] = -sum_s lm[j][s] G[j+s, j+t],
+//                        G[j+t, j] = -sum_s G[j+t, j+s] um[j][s],
+//                        G[j, j]   = Y_j - sum_s lm[j][s] G[j+s, j]
+cudaError_t rgf_sweeps_two_w(const SweepWork& W, const int* n_true, int* status, int status_stride, cudaStream_t s) {
+  Ctx c(W);
+  const int l = W.l, w = W.w, b = W.bs, kb = w * b;
+  const long long two_w = 2LL * w;
+  const int m = (l - w) / 2, nR = l - (m + w), nL = m;
+  cudaError_t e;
+  auto grp = [&](const ZGemmProblem* ps, int np) {
+    ZGemmGroup g{};
+    g.batch = W.batch;
+    g.bs = b;
+    for (int i = 0; i < np; ++i) g.prob[g.nprob++] = ps[i];
+    return zgemm_grouped(g, s);
+  };
+  auto inv1 = [&](int j) {
+    return zinv_batched2(c.slot(j, 0), b, W.g_bstride, b, n_true[j], W.batch, 1, 0, W.inv,
+                         status + (long long)j * status_stride, 0, s);
+  };
+  auto inv2 = [&](int jR, int jL) {
+    if (jR < 0) return inv1(jL);
+    if (jL < 0) return inv1(jR);
+    if (n_true[jL] != n_true[jR]) {
+      cudaError_t r = inv1(jR);
+      return r != cudaSuccess ? r : inv1(jL);
+    }
+    double2* mR = c.slot(jR, 0);
+    return zinv_batched2(mR, b, W.g_bstride, b, n_true[jR], W.batch, 2, (long long)(c.slot(jL, 0) - mR), W.inv,
+                         status + (long long)jR * status_stride, (long long)(jL - jR) * status_stride, s);
+  };
+  // ---------------- inward chains
+  const int nup = nR > nL ? nR : nL;
+  for (int t = 0; t < nup; ++t) {
+    const int jR = t < nR ? l - 1 - t : -1, jL = t < nL ? t : -1;
+    if ((e = inv2(jR, jL)) != cudaSuccess) return e;
+    ZGemmProblem p1[2], pR[2], pL[2];
+    int n1 = 0;
+    if (jR >= 0) {
+      p1[n1++] = prob(b, kb, b, 1.0, 0.0, c.gop(c.slot(jR, 0), 0, 0), c.gop(c.slot(jR, -1), 0, -1),
+                      c.mop(c.lm(jR), 0, 1));
+      const ZOp upper = c.gop(c.slot(jR - 1, +1), -two_w, 0);
+      pR[0] = prob(kb, kb, b, -1.0, 1.0, upper, c.mop(c.lm(jR), 0, 1), c.gop(c.slot(jR - 1, 0), -two_w, -1));
+      pR[1] = prob(kb, b, b, 1.0, 0.0, upper, c.gop(c.slot(jR, 0), 0, 0), c.mop(c.um(jR), 1, 0));
+    }
+    if (jL >= 0) {
+      p1[n1++] = prob(b, kb, b, 1.0, 0.0, c.gop(c.slot(jL, 0), 0, 0), c.gop(c.slot(jL, +1), 0, +1),
+                      c.mop(c.lm(jL), 0, 1));
+      const ZOp lower = c.gop(c.slot(jL + 1, -1), two_w, 0);
+      pL[0] = prob(kb, kb, b, -1.0, 1.0, lower, c.mop(c.lm(jL), 0, 1), c.gop(c.slot(jL + 1, 0), two_w, +1));
+      pL[1] = prob(kb, b, b, 1.0, 0.0, lower, c.gop(c.slot(jL, 0), 0, 0), c.mop(c.um(jL), 1, 0));
+    }
+    if ((e = grp(p1, n1)) != cudaSuccess) return e;
+    // windows: right rows/cols [jR-w, jR-1], left [jL+1, jL+w]; disjoint -> one launch
+    if (jR >= 0 && jL >= 0 && jR - w > jL + w) {
+      ZGemmProblem p2[4] = {pR[0], pR[1], pL[0], pL[1]};
+      if ((e = grp(p2, 4)) != cudaSuccess) return e;
+    } else {
+      if (jR >= 0 && (e = grp(pR, 2)) != cudaSuccess) return e;
+      if (jL >= 0 && (e = grp(pL, 2)) != cudaSuccess) return e;
+    }
+  }
+  // ---------------- the w middle layers: one-ended recursion on the sub-band [m, m+w)
+  {
+    SweepWork Wm = W;
+    Wm.l = w;
+    Wm.lm_layers = W.lm_layers > 0 ? W.lm_layers : l;
+    Wm.G = c.slot(m, -w);
+    Wm.LM = c.lm(m);
+    Wm.UM = c.um(m);
+    Wm.rows_done = nullptr;
+    Wm.two_ended = false;
+    if ((e = rgf_sweeps_one(Wm, n_true + m, status + (long long)m * status_stride, status_stride, s)) != cudaSuccess)
+      return e;
+  }
+  // ---------------- outward sweeps; after step t rows [lo, hi) are final
+  int flo = m + w, fhi = m + w;
+  bool any = false;
+  auto flush = [&](int lo, int hi, bool force) -> cudaError_t {
+    if (!W.rows_done || lo >= hi) return cudaSuccess;
+    if (!any) {  // first complete range
+      if (!force && hi - lo < W.hook_rows) return cudaSuccess;
+      any = true;
+      flo = lo;
+      fhi = hi;
+      return W.rows_done(lo, hi, W.e_off, W.batch, s);
+    }
+    if (!force && (flo - lo) + (hi - fhi) < W.hook_rows) return cudaSuccess;
+    cudaError_t r = cudaSuccess;
+    if (lo < flo) r = W.rows_done(lo, flo, W.e_off, W.batch, s);
+    if (r == cudaSuccess && hi > fhi) r = W.rows_done(fhi, hi, W.e_off, W.batch, s);
+    flo = lo;
+    fhi = hi;
+    return r;
+  };
+  const int ndown = nR > nL ? nR : nL;
+  for (int t = 1; t <= ndown; ++t) {
+    const int jR = t <= nR ? m + w - 1 + t : -1, jL = t <= nL ? m - t : -1;
+    ZGemmProblem pa[4], pb[2];
+    int na = 0, nb = 0;
+    if (jR >= 0) {
+      const ZOp lmrow = c.mop(c.lm(jR), 0, 1), window = c.gop(c.slot(jR - 1, 0), -two_w, -1);
+      pa[na++] = prob(b, kb, kb, -1.0, 0.0, lmrow, window, c.gop(c.slot(jR, -1), 0, -1));
+      pa[na++] = prob(kb, b, kb, -1.0, 0.0, window, c.mop(c.um(jR), 1, 0), c.gop(c.slot(jR - 1, +1), -two_w, 0));
+      pb[nb++] = prob(b, b, kb, -1.0, 1.0, lmrow, c.gop(c.slot(jR - 1, +1), -two_w, 0), c.gop(c.slot(jR, 0), 0, 0));
+    }
+    if (jL >= 0) {
+      const ZOp lmrow = c.mop(c.lm(jL), 0, 1), window = c.gop(c.slot(jL + 1, 0), two_w, +1);
+      pa[na++] = prob(b, kb, kb, -1.0, 0.0, lmrow, window, c.gop(c.slot(jL, +1), 0, +1));
+      pa[na++] = prob(kb, b, kb, -1.0, 0.0, window, c.mop(c.um(jL), 1, 0), c.gop(c.slot(jL + 1, -1), two_w, 0));
+      pb[nb++] = prob(b, b, kb, -1.0, 1.0, lmrow, c.gop(c.slot(jL + 1, -1), two_w, 0), c.gop(c.slot(jL, 0), 0, 0));
+    }
+    if ((e = grp(pa, na)) != cudaSuccess) return e;
+    if ((e = grp(pb, nb)) != cudaSuccess) return e;
+    const int rdone = t <= nR ? jR : l - 1, ldone = t <= nL ? jL : 0;
+    const int hi = rdone >= l - 1 ? l : rdone - w + 1, lo = ldone <= 0 ? 0 : ldone + w;
+    if ((e = flush(lo, hi, false)) != cudaSuccess) return e;
+  }
+  return flush(0, l, true);
+}
+
 struct StreamPool {
   std::vector<cudaStream_t> s;
   std::vector<cudaEvent_t> ev;
@@ -320,9 +454,11 @@ StreamPool& pool_for(int n) {
 cudaError_t rgf_sweeps(const SweepWork& W, const int* n_true, cudaStream_t s) {
   const int G = W.groups < 1 ? 1 : (W.groups > W.batch ? W.batch : W.groups);
   const int sstride = W.status_stride > 0 ? W.status_stride : W.batch;
-  if (G == 1)
-    return use_two_ended(W) ? rgf_sweeps_two(W, n_true, W.status, sstride, s)
-                            : rgf_sweeps_one(W, n_true, W.status, sstride, s);
+  auto sweep = [&](const SweepWork& X, int* st, cudaStream_t q) {
+    if (!use_two_ended(X)) return rgf_sweeps_one(X, n_true, st, sstride, q);
+    return X.w == 1 ? rgf_sweeps_two(X, n_true, st, sstride, q) : rgf_sweeps_two_w(X, n_true, st, sstride, q);
+  };
+  if (G == 1) return sweep(W, W.status, s);
   // Independent batch groups on side streams: one group's latency-bound pivot
   // inversions overlap the other groups' GEMMs.
   StreamPool& P = pool_for(G);
@@ -342,9 +478,7 @@ cudaError_t rgf_sweeps(const SweepWork& W, const int* n_true, cudaStream_t s) {
     Wg.inv = static_cast<char*>(W.inv) + size_t(g) * inv_b;
     Wg.e_off = W.e_off + e0;
     if ((e = cudaStreamWaitEvent(P.s[g], P.ev[G], 0))) return e;
-    if ((e = use_two_ended(W) ? rgf_sweeps_two(Wg, n_true, W.status + e0, sstride, P.s[g])
-                              : rgf_sweeps_one(Wg, n_true, W.status + e0, sstride, P.s[g])))
-      return e;
+    if ((e = sweep(Wg, W.status + e0, P.s[g]))) return e;
     if ((e = cudaEventRecord(P.ev[g], P.s[g]))) return e;
     if ((e = cudaStreamWaitEvent(s, P.ev[g], 0))) return e;
   }

@@ -89,3 +89,26 @@ def test_two_ended_sweep_layer_counts(gpu, layers, n_e):
     odd / even / minimal layer counts, one and two stream groups, against the
     reference's one-ended RGF."""
     _check(D.scaled(D.CONFIGS[2], num_layers=layers, n_energy=n_e, block_size=64))
+
+
+@pytest.mark.parametrize("w,layers,n_e", [(2, 8, 2), (2, 9, 3), (2, 10, 9), (2, 7, 2), (3, 11, 2), (3, 16, 3)])
+def test_two_ended_banded_sweep(gpu, w, layers, n_e):
+    """Block n-diagonal Dyson batches run the two-ended recursion (chains from both ends,
+    the w middle layers by the one-ended recursion, outward sweeps) when l >= 3w + 2,
+    the one-ended one below; both against the reference's rgf_ndiag."""
+    from dataclasses import replace
+
+    cfg = replace(D.scaled(D.CONFIGS[3], num_layers=layers, n_energy=n_e, block_size=64), bandwidth=w)
+    _check(cfg)
+
+
+@pytest.mark.parametrize("w,layers", [(2, 14), (3, 20)])
+def test_two_ended_banded_host_rows(gpu, w, layers):
+    """Rows streamed by the host path while the outward sweeps run equal the resident bands."""
+    from dataclasses import replace
+
+    cfg = replace(D.scaled(D.CONFIGS[3], num_layers=layers, n_energy=3, block_size=64), bandwidth=w)
+    dev = np.swapaxes(_run_gpu(cfg), -1, -2)
+    got, fails = D.solve_host(cfg)
+    assert (fails == -1).all()
+    assert np.array_equal(got, dev)
