@@ -113,4 +113,36 @@ cudaError_t dyson_form_band(double2* G, const double2* H, int l, int w, int bs, 
   return cudaGetLastError();
 }
 
+
+namespace {
+// Dense window <-> band slots: D (batch x [wb x wb], column-major, ld wb) block (r, c) is
+// band slot (a0 + r, c - r) of each batch entry (stride gstride). to_dense: band -> D.
+__global__ void band_window_kernel(double2* __restrict__ G, long long gstride, double2* __restrict__ D, int a0, int w,
+                                   int b, int batch, int to_dense) {
+  const long long bb = (long long)b * b, wb = (long long)w * b;
+  const long long per = wb * wb, total = per * batch;
+  const int nslot = 2 * w + 1;
+  for (long long idx = blockIdx.x * (long long)blockDim.x + threadIdx.x; idx < total;
+       idx += (long long)gridDim.x * blockDim.x) {
+    const long long e = idx / per, q = idx - e * per;
+    const long long col = q / wb, row = q - col * wb;  // dense (row, col)
+    const int r = int(row / b), c = int(col / b);
+    const long long i = row - (long long)r * b, j = col - (long long)c * b;
+    double2* g = G + e * gstride + ((long long)(a0 + r) * nslot + (c - r) + w) * bb + j * b + i;
+    if (to_dense)
+      D[idx] = *g;
+    else
+      *g = D[idx];
+  }
+}
+}  // namespace
+
+cudaError_t band_window(double2* G, long long gstride, double2* D, int a0, int w, int b, int batch, bool to_dense,
+                        cudaStream_t s) {
+  const long long total = (long long)w * b * w * b * batch;
+  ProfScope prof(s, PROF_BAND, 0.0, 32.0 * total);
+  band_window_kernel<<<grid_for(total, 256), 256, 0, s>>>(G, gstride, D, a0, w, b, batch, to_dense ? 1 : 0);
+  return cudaGetLastError();
+}
+
 }  // namespace bbsi_gpu

@@ -602,13 +602,15 @@ int bbsi_cuda_dyson_rgf_z(int l, int w, int bs, int n_energy, const double* H, c
   size_t free_b = 0, total_b = 0;
   CK(cudaMemGetInfo(&free_b, &total_b));
   free_b += arena_held({1, 4, 5});  // this call's own workspace slots are reused or regrown
-  // Default: chunks of ~32 energies once there are >= 48 (measured on B200, config 2:
-  // 1.27 s with one 64-energy chunk, 1.17 s with two of 32, 1.27 s with four of 16):
-  // the G stream (53 GB/s over PCIe) starts when the first chunk's rows are final and
-  // then stays busy while later chunks compute; below ~24 energies per chunk the
-  // compute no longer keeps ahead of the copy. Smaller chunks when HBM is short.
+  // Default: chunks of at most 24 energies once there are >= 48 (measured on B200,
+  // config 2: one 64-energy chunk 1.27 s; chunks of 40 / 32 / 28 / 24 / 22 / 20 / 16:
+  // 1.18 / 1.17 / 1.15 / 1.13 / 1.13 / 1.16 / 1.22 s): the G stream (53 GB/s over
+  // PCIe) starts when the first chunk's rows are final and then stays busy while later
+  // chunks compute; below ~20 energies per chunk the compute falls behind the copy.
+  // Smaller chunks when HBM is short.
   if (chunk <= 0 || chunk > n_energy) {
-    chunk = n_energy >= 48 ? (n_energy + (n_energy + 31) / 32 - 1) / ((n_energy + 31) / 32) : n_energy;
+    const int nc = (n_energy + 23) / 24;
+    chunk = n_energy >= 48 ? (n_energy + nc - 1) / nc : n_energy;
     while (chunk > 1 && (size_t(chunk) * band_b + band_b +
                          sweep_scratch_bytes(l, w, bs, chunk, default_groups(chunk, bs), two_ended_default())) > free_b * 9 / 10)
       chunk = (chunk + 1) / 2;

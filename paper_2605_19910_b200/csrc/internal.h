@@ -29,6 +29,10 @@ cudaError_t dyson_fill_h(double2* H, int l, int w, int b, uint64_t seed, cudaStr
 // for sweeps that read the off-diagonal blocks from H (SweepWork::Hoff).
 cudaError_t dyson_form_diag(double2* G, const double2* H, int l, int w, int bs, int batch, const double2* z,
                             const double2* sigma, cudaStream_t s);
+// Copies the w x w block window of band rows [a0, a0 + w) between the band slots and a
+// dense (w b) x (w b) column-major matrix per batch entry (to_dense: band -> dense).
+cudaError_t band_window(double2* G, long long gstride, double2* D, int a0, int w, int b, int batch, bool to_dense,
+                        cudaStream_t s);
 cudaError_t dyson_form_band(double2* G, const double2* H, int l, int w, int bs, int batch, const double2* z,
                             const double2* sigma, cudaStream_t s);
 
@@ -67,6 +71,7 @@ struct SweepWork {
   // before sweep_carve (the inversion scratch doubles).
   bool two_ended = false;
   int lm_layers = 0;      // layers per batch entry of LM / UM (0: l; a sub-band view keeps the parent's)
+  void* mid = nullptr;    // two-ended, w >= 2: dense (w b)^2 middle window + its inversion scratch (per group)
 };
 
 // Bytes of LM+UM+piv+wz+status for a sweep.

@@ -91,24 +91,39 @@ def test_two_ended_sweep_layer_counts(gpu, layers, n_e):
     _check(D.scaled(D.CONFIGS[2], num_layers=layers, n_energy=n_e, block_size=64))
 
 
-@pytest.mark.parametrize("w,layers,n_e", [(2, 8, 2), (2, 9, 3), (2, 10, 9), (2, 7, 2), (3, 11, 2), (3, 16, 3)])
-def test_two_ended_banded_sweep(gpu, w, layers, n_e):
-    """Block n-diagonal Dyson batches run the two-ended recursion (chains from both ends,
-    the w middle layers by the one-ended recursion, outward sweeps) when l >= 3w + 2,
-    the one-ended one below; both against the reference's rgf_ndiag."""
-    from dataclasses import replace
-
-    cfg = replace(D.scaled(D.CONFIGS[3], num_layers=layers, n_energy=n_e, block_size=64), bandwidth=w)
-    _check(cfg)
+_BANDED_CASES = [(2, 8, 2), (2, 9, 3), (2, 10, 9), (2, 7, 2), (3, 11, 2), (3, 16, 3), (2, 24, 4)]
 
 
-@pytest.mark.parametrize("w,layers", [(2, 14), (3, 20)])
-def test_two_ended_banded_host_rows(gpu, w, layers):
-    """Rows streamed by the host path while the outward sweeps run equal the resident bands."""
-    from dataclasses import replace
+def _in_subprocess(env, code):
+    """Runs `code` in a fresh interpreter (the library reads its switches once per process)."""
+    import os
+    import subprocess
+    import sys
+    from pathlib import Path
 
+    root = Path(__file__).resolve().parent.parent
+    r = subprocess.run([sys.executable, "-c", code], cwd=root, env={**os.environ, **env}, capture_output=True,
+                       text=True, timeout=600)
+    assert r.returncode == 0, r.stdout[-2000:] + r.stderr[-2000:]
+
+
+def test_two_ended_banded_sweep(gpu):
+    """Opt-in banded two-ended recursion (BBSI_TWO_ENDED_BANDED=1: chains from both ends,
+    the w middle layers inverted as one dense (w b)^2 matrix, outward sweeps; one-ended
+    below l = 3w + 2) against the reference's rgf_ndiag, and the host path's streamed rows
+    against the resident bands."""
+    code = f"""
+import numpy as np
+from dataclasses import replace
+import tests.test_gpu_dyson as T
+from paper_2605_19910_b200 import dyson as D
+for w, layers, n_e in {_BANDED_CASES}:
+    T._check(replace(D.scaled(D.CONFIGS[3], num_layers=layers, n_energy=n_e, block_size=64), bandwidth=w))
+for w, layers in ((2, 14), (3, 20)):
     cfg = replace(D.scaled(D.CONFIGS[3], num_layers=layers, n_energy=3, block_size=64), bandwidth=w)
-    dev = np.swapaxes(_run_gpu(cfg), -1, -2)
+    dev = np.swapaxes(T._run_gpu(cfg), -1, -2)
     got, fails = D.solve_host(cfg)
-    assert (fails == -1).all()
-    assert np.array_equal(got, dev)
+    assert (fails == -1).all() and np.array_equal(got, dev)
+print("ok")
+"""
+    _in_subprocess({"BBSI_TWO_ENDED_BANDED": "1"}, code)
