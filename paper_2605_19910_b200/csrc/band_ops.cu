@@ -54,28 +54,33 @@ __global__ void dyson_form_band_kernel(double2* __restrict__ G, const double2* _
 // Diagonal slots of every band (energy e, layer a) from H, the two out-of-range
 // off-diagonal slots of each band zeroed; in-range off-diagonal slots are left for
 // the downward sweep to fill with G.
+// sel0 >= 0: only the diagonal blocks of layers sel0 (and sel1 >= 0) are formed (the
+// sweeps read the others' A from H inside the GEMM that first updates them).
 __global__ void dyson_form_diag_kernel(double2* __restrict__ G, const double2* __restrict__ H, int l, int w, int bs,
-                                       int batch, const double2* __restrict__ z, const double2* __restrict__ sigma) {
+                                       int batch, const double2* __restrict__ z, const double2* __restrict__ sigma,
+                                       int sel0, int sel1) {
   const long long bb = (long long)bs * bs;
   const long long band = (long long)l * (2 * w + 1) * bb;
-  const long long per = (long long)(l + 2 * w) * bb;  // l diagonal blocks + 2w edge slots per energy
+  const int nd = sel0 < 0 ? l : (sel1 < 0 ? 1 : 2);  // diagonal blocks formed per energy
+  const long long per = (long long)(nd + 2 * w) * bb;  // + 2w edge slots per energy
   const long long total = per * batch;
   for (long long idx = blockIdx.x * (long long)blockDim.x + threadIdx.x; idx < total;
        idx += (long long)gridDim.x * blockDim.x) {
     const long long e = idx / per;
     const long long r = idx - e * per;
     const long long blk = r / bb, q = r - blk * bb;
-    if (blk < l) {  // diagonal block of layer a = blk
-      const long long src = (blk * (2 * w + 1) + w) * bb + q;
+    if (blk < nd) {  // diagonal block of layer a
+      const long long a = sel0 < 0 ? blk : (blk == 0 ? sel0 : sel1);
+      const long long src = (a * (2 * w + 1) + w) * bb + q;
       const double2 h = H[src];
       double2 out = make_double2(-h.x, -h.y);
       if ((q % bs) == (q / bs)) {
-        const double2 ze = z[e], sg = sigma[blk];
+        const double2 ze = z[e], sg = sigma[a];
         out = make_double2((ze.x - h.x) - sg.x, (ze.y - h.y) - sg.y);
       }
       G[e * band + src] = out;
     } else {  // edge slots: layer 0 offsets -w..-1, layer l-1 offsets 1..w
-      const int t = int(blk - l);
+      const int t = int(blk - nd);
       const long long slot = t < w ? (long long)t : (long long)(l - 1) * (2 * w + 1) + w + 1 + (t - w);
       G[e * band + slot * bb + q] = make_double2(0.0, 0.0);
     }
@@ -101,7 +106,16 @@ cudaError_t dyson_form_diag(double2* G, const double2* H, int l, int w, int bs, 
                             const double2* sigma, cudaStream_t s) {
   const long long total = (long long)(l + 2 * w) * bs * bs * batch;
   ProfScope prof(s, PROF_BAND, 0.0, 16.0 * (total + (long long)l * bs * bs));
-  dyson_form_diag_kernel<<<grid_for(total, 256), 256, 0, s>>>(G, H, l, w, bs, batch, z, sigma);
+  dyson_form_diag_kernel<<<grid_for(total, 256), 256, 0, s>>>(G, H, l, w, bs, batch, z, sigma, -1, -1);
+  return cudaGetLastError();
+}
+
+cudaError_t dyson_form_diag_ends(double2* G, const double2* H, int l, int w, int bs, int batch, const double2* z,
+                                 const double2* sigma, bool first, cudaStream_t s) {
+  const int a0 = l - 1, a1 = (first && l > 1) ? 0 : -1;
+  const long long total = (long long)((a1 >= 0 ? 2 : 1) + 2 * w) * bs * bs * batch;
+  ProfScope prof(s, PROF_BAND, 0.0, 16.0 * total);
+  dyson_form_diag_kernel<<<grid_for(total, 256), 256, 0, s>>>(G, H, l, w, bs, batch, z, sigma, a0, a1);
   return cudaGetLastError();
 }
 

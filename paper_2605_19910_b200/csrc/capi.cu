@@ -348,6 +348,16 @@ int bbsi_cuda_rgf_batched_dev(int l, int w, int bs, int batch, const double* dA,
   return bad ? fail(BBSI_SINGULAR, "singular Schur pivot in at least one batch entry") : BBSI_OK;
 }
 
+// Dyson diagonal blocks formed inside the first Schur-update GEMM (BBSI_FORM_IN_GEMM=0: a
+// separate pass over every diagonal block first).
+static bool form_in_gemm() {
+  static const bool on = [] {
+    const char* e = getenv("BBSI_FORM_IN_GEMM");
+    return !(e && atoi(e) == 0);
+  }();
+  return on;
+}
+
 int bbsi_cuda_dyson_rgf_dev(int l, int w, int bs, int n_energy, const double* dH, const double* z,
                             const double* sigma, double* dG, int* fail_layers, void* stream) {
   if (int rc = validate_layout(l, w, bs, nullptr)) return rc;
@@ -379,11 +389,17 @@ int bbsi_cuda_dyson_rgf_dev(int l, int w, int bs, int n_energy, const double* dH
   // tridiagonal: the sweeps read A's off-diagonal blocks (-H) from the shared H, so only
   // the diagonal blocks of each energy's band are formed
   if (w == 1) W.Hoff = reinterpret_cast<const double2*>(dH);
+  if (W.Hoff && form_in_gemm()) {
+    W.zdev = dzs;
+    W.sigdev = dzs + n_energy;
+  }
   CK(run_graphed(key, s, [&](cudaStream_t st) -> cudaError_t {
     double2* g = reinterpret_cast<double2*>(dG);
     const double2* h = reinterpret_cast<const double2*>(dH);
-    cudaError_t e = W.Hoff ? dyson_form_diag(g, h, l, w, bs, n_energy, dzs, dzs + n_energy, st)
-                           : dyson_form_band(g, h, l, w, bs, n_energy, dzs, dzs + n_energy, st);
+    cudaError_t e = W.zdev  ? dyson_form_diag_ends(g, h, l, w, bs, n_energy, dzs, dzs + n_energy,
+                                                   sweep_is_two_ended(W), st)
+                    : W.Hoff ? dyson_form_diag(g, h, l, w, bs, n_energy, dzs, dzs + n_energy, st)
+                             : dyson_form_band(g, h, l, w, bs, n_energy, dzs, dzs + n_energy, st);
     return e ? e : rgf_sweeps(W, nt.data(), st);
   }));
   CK(collect_failures(W, fails, s));
@@ -661,10 +677,6 @@ int bbsi_cuda_dyson_rgf_z(int l, int w, int bs, int n_energy, const double* H, c
       const int e0 = c * chunk, ne = std::min(chunk, n_energy - e0), buf = c % nbuf;
       if (c >= nbuf) CK(cudaStreamWaitEvent(sc, freed[buf], 0));
       double2* g = dG + size_t(buf) * chunk * band;
-      if (w == 1)
-        CK(dyson_form_diag(g, dH, l, w, bs, ne, dzs + e0, dzs + n_energy, sc));
-      else
-        CK(dyson_form_band(g, dH, l, w, bs, ne, dzs + e0, dzs + n_energy, sc));
       SweepWork W;
       W.l = l;
       W.w = w;
@@ -675,7 +687,17 @@ int bbsi_cuda_dyson_rgf_z(int l, int w, int bs, int n_energy, const double* H, c
       W.groups = groups;
       W.two_ended = two_ended_default();
       if (w == 1) W.Hoff = dH;
+      if (W.Hoff && form_in_gemm()) {
+        W.zdev = dzs + e0;
+        W.sigdev = dzs + n_energy;
+      }
       sweep_carve(W, scratch);
+      if (W.zdev)
+        CK(dyson_form_diag_ends(g, dH, l, w, bs, ne, dzs + e0, dzs + n_energy, sweep_is_two_ended(W), sc));
+      else if (w == 1)
+        CK(dyson_form_diag(g, dH, l, w, bs, ne, dzs + e0, dzs + n_energy, sc));
+      else
+        CK(dyson_form_band(g, dH, l, w, bs, ne, dzs + e0, dzs + n_energy, sc));
       W.status = dstat + e0;
       W.status_stride = n_energy;
       // finished band rows of the downward sweep -> host, on the copy stream, while the

@@ -33,6 +33,11 @@ cudaError_t dyson_form_diag(double2* G, const double2* H, int l, int w, int bs, 
 // dense (w b) x (w b) column-major matrix per batch entry (to_dense: band -> dense).
 cudaError_t band_window(double2* G, long long gstride, double2* D, int a0, int w, int b, int batch, bool to_dense,
                         cudaStream_t s);
+// Same for the last layer only (and layer 0 when `first`): the sweeps' first pivots.
+// The other diagonal blocks are read from H by the GEMM that first updates them
+// (ZGemmProblem::cz, SweepWork::zdev).
+cudaError_t dyson_form_diag_ends(double2* G, const double2* H, int l, int w, int bs, int batch, const double2* z,
+                                 const double2* sigma, bool first, cudaStream_t s);
 cudaError_t dyson_form_band(double2* G, const double2* H, int l, int w, int bs, int batch, const double2* z,
                             const double2* sigma, cudaStream_t s);
 
@@ -72,6 +77,11 @@ struct SweepWork {
   bool two_ended = false;
   int lm_layers = 0;      // layers per batch entry of LM / UM (0: l; a sub-band view keeps the parent's)
   void* mid = nullptr;    // two-ended, w >= 2: dense (w b)^2 middle window + its inversion scratch (per group)
+  // Optional (with Hoff): per-batch z (device, this (group's) batch entries) and per-layer
+  // sigma (device): the diagonal blocks of A are not in G until the Schur update that first
+  // touches them reads A = z I - H - sigma I from H (only the chains' first layers are formed)
+  const double2* zdev = nullptr;
+  const double2* sigdev = nullptr;
 };
 
 // Bytes of LM+UM+piv+wz+status for a sweep.

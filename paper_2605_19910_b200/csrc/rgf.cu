@@ -178,6 +178,11 @@ cudaError_t rgf_sweeps_one(const SweepWork& W, const int* n_true, int* status, i
     // window M'(j-s, j-t) -= M'(j-s, j) lm[j][t];  um[j] = [M'(j-t, j)]_t X_j
     ZOp upper = hs ? c.hop(j - 1, +1) : c.gop(c.slot(j - 1, +1), -two_w, 0);
     ZGemmProblem p_win = prob(k * b, k * b, b, -sg, 1.0, upper, c.mop(c.lm(j), 0, 1), c.gop(c.slot(j - 1, 0), -two_w, -1));
+    if (hs && W.zdev) {  // A[j-1, j-1] = z I - H - sigma I read from H (first and only update)
+      p_win.C = c.hop(j - 1, 0);
+      p_win.cz = W.zdev;
+      p_win.csig = W.sigdev + (j - 1);
+    }
     ZGemmProblem p_um = prob(k * b, b, b, sg, 0.0, upper, X, c.mop(c.um(j), 1, 0));
     if ((e = launch(W, {p_win, p_um}, s)) != cudaSuccess) return e;
   }
@@ -260,6 +265,20 @@ cudaError_t rgf_sweeps_two(const SweepWork& W, const int* n_true, int* status, i
   };
 
   // ---------------- two inward chains
+  // diagonal blocks still to be formed from H by their first Schur update (W.zdev):
+  // all but the two chain starts
+  std::vector<char> formed(l, W.zdev ? 0 : 1);
+  formed[0] = formed[l - 1] = 1;
+  auto win = [&](int a, const ZOp& A_, const ZOp& B_) {  // M'[a, a] -= A_ B_ (into G)
+    ZGemmProblem p = prob(b, b, b, -sg, 1.0, A_, B_, blk(c.slot(a, 0)));
+    if (!formed[a]) {
+      p.C = c.hop(a, 0);
+      p.cz = W.zdev;
+      p.csig = W.sigdev + a;
+      formed[a] = 1;
+    }
+    return p;
+  };
   const int nup = nR > nL ? nR : nL;
   for (int t = 0; t < nup; ++t) {
     const int jR = t < nR ? l - 1 - t : -1, jL = t < nL ? t : -1;
@@ -269,13 +288,13 @@ cudaError_t rgf_sweeps_two(const SweepWork& W, const int* n_true, int* status, i
     if (jR >= 0) {
       p1[n1++] = prob(b, b, b, sg, 0.0, blk(c.slot(jR, 0)), offd(jR, -1), lmo(jR));
       const ZOp up = offd(jR - 1, +1);
-      p2[n2++] = prob(b, b, b, -sg, 1.0, up, lmo(jR), blk(c.slot(jR - 1, 0)));
+      p2[n2++] = win(jR - 1, up, lmo(jR));
       p2[n2++] = prob(b, b, b, sg, 0.0, up, blk(c.slot(jR, 0)), umo(jR));
     }
     if (jL >= 0) {
       p1[n1++] = prob(b, b, b, sg, 0.0, blk(c.slot(jL, 0)), offd(jL, +1), lmo(jL));
       const ZOp dn = offd(jL + 1, -1);
-      p2[n2++] = prob(b, b, b, -sg, 1.0, dn, lmo(jL), blk(c.slot(jL + 1, 0)));
+      p2[n2++] = win(jL + 1, dn, lmo(jL));
       p2[n2++] = prob(b, b, b, sg, 0.0, dn, blk(c.slot(jL, 0)), umo(jL));
     }
     if ((e = grp(p1, n1)) != cudaSuccess) return e;
@@ -530,6 +549,7 @@ cudaError_t rgf_sweeps(const SweepWork& W, const int* n_true, cudaStream_t s) {
     Wg.UM = W.UM + (long long)e0 * W.l * W.w * bb;
     Wg.inv = static_cast<char*>(W.inv) + size_t(g) * inv_b;
     Wg.e_off = W.e_off + e0;
+    if (W.zdev) Wg.zdev = W.zdev + e0;
     if ((e = cudaStreamWaitEvent(P.s[g], P.ev[G], 0))) return e;
     if ((e = sweep(Wg, W.status + e0, P.s[g], g))) return e;
     if ((e = cudaEventRecord(P.ev[g], P.s[g]))) return e;

@@ -40,6 +40,11 @@ struct ZGemmProblem {
   // < amax_n, masked ones included, into amax[batch] (the first Gauss-Jordan step)
   unsigned long long* amax;
   int amax_n;
+  // optional (C-as-accumulator path): C holds H (a diagonal block shared by the batch,
+  // bstride 0) and the GEMM reads A = z I - H - sigma I from it, entry by entry as
+  // dyson_form_diag does: diagonal (z - h) - sigma, elsewhere -h; z = cz[batch], sigma = *csig
+  const double2* cz;
+  const double2* csig;
   int tiles_m, tiles_n; // filled by the launcher
   int tile_begin;       // first flattened tile index of this problem
 };

@@ -62,7 +62,7 @@ __device__ __forceinline__ void load_tile(const ZGemmProblem& P, int bs, int bat
 // spills; 3: 168 regs, 12 warps per SM, a few epilogue spills).
 // AMAX: the first Gauss-Jordan step's variant (max |C|^2, ZGemmProblem::amax); a
 // separate instantiation so the other launches keep their register allocation.
-template <bool PLAIN, int MINB, bool AMAX = false>
+template <bool PLAIN, int MINB, bool AMAX = false, bool CFORM = false>
 __global__ void __launch_bounds__(128, MINB) zgemm_grouped_kernel(const __grid_constant__ ZGemmGroup g) {
   extern __shared__ __align__(16) double2 smem[];
   double2* As = smem;
@@ -165,6 +165,19 @@ __global__ void __launch_bounds__(128, MINB) zgemm_grouped_kernel(const __grid_c
             const int nl = wn + ni * 8 + lc * 2 + q;
             cv[mi][ni][q] = (rowok[mi] && colok[ni][q]) ? rb[(long long)nl * P.C.ld + srow[mi]] : make_double2(0.0, 0.0);
           }
+      if (CFORM && P.cz) {  // the Dyson diagonal block from H (see ZGemmProblem::cz)
+        const double2 z = P.cz[batch], sgm = *P.csig;
+#pragma unroll
+        for (int mi = 0; mi < 4; ++mi)
+#pragma unroll
+          for (int ni = 0; ni < 4; ++ni)
+#pragma unroll
+            for (int q = 0; q < 2; ++q) {
+              const double2 h = cv[mi][ni][q];
+              const bool dg = m0 + wm + mi * 8 + lr == n0 + wn + ni * 8 + lc * 2 + q;
+              cv[mi][ni][q] = dg ? make_double2((z.x - h.x) - sgm.x, (z.y - h.y) - sgm.y) : make_double2(-h.x, -h.y);
+            }
+      }
     }
 #pragma unroll
     for (int mi = 0; mi < 4; ++mi)
@@ -317,13 +330,15 @@ int gemm_minb() {
   return m;
 }
 
-template <bool PLAIN, int MINB, bool AMAX = false>
+template <bool PLAIN, int MINB, bool AMAX = false, bool CFORM = false>
 cudaError_t gemm_attrs() {
   static cudaError_t e = [] {
-    cudaError_t r = cudaFuncSetAttribute(zgemm_grouped_kernel<PLAIN, MINB, AMAX>, cudaFuncAttributeMaxDynamicSharedMemorySize,
+    cudaError_t r = cudaFuncSetAttribute(zgemm_grouped_kernel<PLAIN, MINB, AMAX, CFORM>,
+                                         cudaFuncAttributeMaxDynamicSharedMemorySize,
                                          SMEM_BYTES);
     if (r == cudaSuccess)
-      r = cudaFuncSetAttribute(zgemm_grouped_kernel<PLAIN, MINB, AMAX>, cudaFuncAttributePreferredSharedMemoryCarveout,
+      r = cudaFuncSetAttribute(zgemm_grouped_kernel<PLAIN, MINB, AMAX, CFORM>,
+                               cudaFuncAttributePreferredSharedMemoryCarveout,
                                cudaSharedmemCarveoutMaxShared);
     return r;
   }();
@@ -354,10 +369,17 @@ cudaError_t zgemm_grouped(ZGemmGroup& g, cudaStream_t stream) {
   }
   ProfScope prof(stream, g.prof_cat ? g.prof_cat : PROF_GEMM, fl, by);
   cudaError_t e;
-  const bool three = gemm_minb() == 3;
-  bool amax = false;
-  for (int p = 0; p < g.nprob; ++p) amax |= g.prob[p].amax != nullptr;
-  if (plain && amax) {
+  const bool three = gemm_minb() == 3;  // (2 CTAs/SM for the GJ updates alone: 130 vs 121 ms)
+  bool amax = false, cform = false;
+  for (int p = 0; p < g.nprob; ++p) {
+    amax |= g.prob[p].amax != nullptr;
+    cform |= g.prob[p].cz != nullptr;
+  }
+  if (cform) {
+    if (plain) return cudaErrorInvalidValue;  // the Dyson form only feeds block-strided sweep GEMMs
+    if ((e = gemm_attrs<false, 3, false, true>())) return e;
+    zgemm_grouped_kernel<false, 3, false, true><<<total, 128, SMEM_BYTES, stream>>>(g);
+  } else if (plain && amax) {
     if ((e = gemm_attrs<true, 3, true>())) return e;
     zgemm_grouped_kernel<true, 3, true><<<total, 128, SMEM_BYTES, stream>>>(g);
   } else if (plain && three) {
