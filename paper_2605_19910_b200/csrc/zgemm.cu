@@ -62,14 +62,10 @@ __device__ __forceinline__ void load_tile(const ZGemmProblem& P, int bs, int bat
 // spills; 3: 168 regs, 12 warps per SM, a few epilogue spills).
 // AMAX: the first Gauss-Jordan step's variant (max |C|^2, ZGemmProblem::amax); a
 // separate instantiation so the other launches keep their register allocation.
-template <bool PLAIN, int MINB, bool AMAX = false, bool CFORM = false>
-__global__ void __launch_bounds__(128, MINB) zgemm_grouped_kernel(const __grid_constant__ ZGemmGroup g) {
-  extern __shared__ __align__(16) double2 smem[];
-  double2* As = smem;
-  double2* Bs = smem + STAGES * A_STAGE;
-
+// One 64 x 64 output tile t of the flattened (problem, batch, tile) index.
+template <bool PLAIN, bool AMAX, bool CFORM>
+__device__ __forceinline__ void zgemm_tile(const ZGemmGroup& g, const int t, double2* As, double2* Bs) {
   // ---- decode the flattened tile index
-  int t = blockIdx.x;
   int pi = 0;
 #pragma unroll 1
   for (int q = 1; q < g.nprob; ++q)
@@ -318,6 +314,15 @@ __global__ void __launch_bounds__(128, MINB) zgemm_grouped_kernel(const __grid_c
           }
     }
   }
+}
+
+// One CTA per tile. (A persistent grid of 3 CTAs/SM walking the tiles with an L2
+// prefetch of the next tile's C measured slower for the Gauss-Jordan updates on B200:
+// 136 vs 121 ms per step.)
+template <bool PLAIN, int MINB, bool AMAX = false, bool CFORM = false>
+__global__ void __launch_bounds__(128, MINB) zgemm_grouped_kernel(const __grid_constant__ ZGemmGroup g) {
+  extern __shared__ __align__(16) double2 smem[];
+  zgemm_tile<PLAIN, AMAX, CFORM>(g, blockIdx.x, smem, smem + STAGES * A_STAGE);
 }
 
 }  // namespace
