@@ -85,11 +85,19 @@ class CudaPhases:
 
     def __init__(self, l: int, b: int, s2: int):
         self.l, self.b, self.s2 = l, b, s2
+        self._G = None  # one band-sized work buffer: phase 1's scratch, then phase 3's result
+
+    def _band(self, A_loc):
+        import torch
+
+        if self._G is None or self._G.shape != A_loc.shape or self._G.device != A_loc.device:
+            self._G = torch.empty_like(A_loc)
+        return self._G
 
     def phase1(self, A_loc, t0: int, t1: int):
         import torch
 
-        G = torch.empty_like(A_loc)
+        G = self._band(A_loc)
         pk = torch.empty((t1 - t0, PACKET_BLOCKS, self.b, self.b), dtype=torch.complex128, device=A_loc.device)
         fail = C.c_int(-1)
         rc = lib().bbsi_cuda_ddrgf_phase1_dev(self.l, self.b, self.s2, t0, t1, _ptr(A_loc), _ptr(G), _ptr(pk),
@@ -109,9 +117,8 @@ class CudaPhases:
         return out
 
     def phase3(self, A_loc, out, t0: int, t1: int):
-        import torch
-
-        G = torch.empty_like(A_loc)
+        G = self._band(A_loc)
+        self._G = None  # handed to the caller
         fail = C.c_int(-1)
         rc = lib().bbsi_cuda_ddrgf_phase3_dev(self.l, self.b, self.s2, t0, t1, _ptr(A_loc), _ptr(G), _ptr(out),
                                               C.byref(fail), _stream())
