@@ -70,13 +70,7 @@ int panel_kind() {
 // other stream group (BBSI_PANEL_PRIORITY=0: lowest).
 // Pair kernel: panel 2's pivot rows get their own prefetch buffer when two NB x (n+2)
 // staging buffers fit next to the static shared memory (n <= 320).
-bool pair_pre2(int n) {
-  static const bool off = [] {
-    const char* e = getenv("BBSI_PAIR_PRE2");
-    return e && atoi(e) == 0;
-  }();
-  return !off && 2 * size_t(kNB) * (n + 2) * sizeof(double2) + 40 * 1024 <= 227 * 1024;
-}
+bool pair_pre2(int n) { return 2 * size_t(kNB) * (n + 2) * sizeof(double2) + 40 * 1024 <= 227 * 1024; }
 
 int panel_priority() {
   static int p = [] {
@@ -678,15 +672,10 @@ __global__ void __launch_bounds__(PT, 1)
 //   Vs2       = M[P2,:] (0 on K1) - Wz1[P2] V1, I on K2    (panel 2's pivot rows)
 //   M <- M (0 on rows P1, P2 and cols K1, K2) - [Wz1 (0 on P2) | Wz2] [V1 (0 on K2); V2]
 // with Wz2 = M2[:,K2] (-I on P2) and V2 = Pinv2 Vs2. Rows <= RPT * PT for both panels.
-// BBSI_PAIR_MAXNREG=r (build-time): cap the pair kernel at r registers per thread so that
-// a 168-register GEMM CTA can share its SM (experiment).
-#ifdef BBSI_PAIR_MAXNREG
-#define BBSI_PAIR_BOUNDS __maxnreg__(BBSI_PAIR_MAXNREG)
-#else
-#define BBSI_PAIR_BOUNDS __launch_bounds__(PT, 1)
-#endif
+// (Capping it at 168 registers -- 12 B of spills -- so that a GEMM CTA of the other
+// stream group can share its SM measured no better on B200: 577-579 vs 575 ms per step.)
 template <int NB, int RPT>
-__global__ void BBSI_PAIR_BOUNDS
+__global__ void __launch_bounds__(PT, 1)
     gj_pair_kernel(const double2* __restrict__ cur0, long long ld, long long bstride, int n, int n_true, int k,
                    int last, GjScratch S, int* __restrict__ status0, BatchIdx bi, int pre2) {
   constexpr int W2 = 2 * NB;
