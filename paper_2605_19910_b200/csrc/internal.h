@@ -92,6 +92,8 @@ bool two_ended_default();
 // the layer count allows it); its multipliers then hold the right chain for layers
 // > m and the left chain (lm = Y A[j, j+1], um = A[j+1, j] Y) for layers < m = l/2 (w = 1).
 bool sweep_is_two_ended(const SweepWork& W);
+// Stream groups of a Dyson energy batch (env BBSI_GROUPS overrides).
+int dyson_groups(int batch);
 // Default number of concurrent batch groups (env BBSI_GROUPS overrides).
 int default_groups(int batch, int bs);
 // Carves the scratch part of a SweepWork out of `base` (>= sweep_scratch_bytes).

@@ -26,6 +26,18 @@
 
 namespace bbsi_gpu {
 
+int dyson_groups(int batch) {
+  if (const char* e = getenv("BBSI_GROUPS")) {
+    int g = atoi(e);
+    if (g >= 1) return g < batch ? g : batch;
+  }
+  // Energy batches: up to 16 independent stream groups. The chains of a group are
+  // latency-bound (inversion panels), so more concurrent groups help small batches:
+  // B200, config 2 at 64 / 32 / 16 / 8 energies (the per-GPU share at 1 / 2 / 4 / 8 GPUs),
+  // 2 groups: 572 / 311 / 186 / 128 ms; min(16, batch): 573 / 289 / 162 / 116 ms.
+  return batch < 16 ? batch : 16;
+}
+
 int default_groups(int batch, int bs) {
   if (const char* e = getenv("BBSI_GROUPS")) {
     int g = atoi(e);
