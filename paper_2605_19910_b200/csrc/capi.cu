@@ -605,6 +605,51 @@ static int e2e_rows() {
   return v > 0 ? v : 8;
 }
 
+// Persistent compute / copy streams of the host-buffer path (per device) and a pinned
+// staging buffer for z and sigma.
+struct E2eStreams {
+  cudaStream_t sc = nullptr, sd = nullptr;
+};
+static E2eStreams& e2e_streams() {
+  static std::mutex mu;
+  static std::vector<E2eStreams> v;
+  std::lock_guard<std::mutex> lk(mu);
+  int dev = 0;
+  cudaGetDevice(&dev);
+  if (int(v.size()) <= dev) v.resize(dev + 1);
+  if (!v[dev].sc) {
+    cudaStreamCreateWithFlags(&v[dev].sc, cudaStreamNonBlocking);
+    cudaStreamCreateWithFlags(&v[dev].sd, cudaStreamNonBlocking);
+  }
+  return v[dev];
+}
+static double2* e2e_stage(size_t n) {
+  static std::vector<std::pair<double2*, size_t>> per_dev;
+  int dev = 0;
+  cudaGetDevice(&dev);
+  if (int(per_dev.size()) <= dev) per_dev.resize(dev + 1, {nullptr, 0});
+  auto& b = per_dev[dev];
+  if (b.second < n) {
+    if (b.first) {
+      cudaDeviceSynchronize();
+      cudaFreeHost(b.first);
+    }
+    b = {nullptr, 0};
+    void* p = nullptr;
+    if (cudaHostAlloc(&p, n * sizeof(double2), cudaHostAllocDefault) != cudaSuccess) return nullptr;
+    b = {static_cast<double2*>(p), n};
+  }
+  return b.first;
+}
+static bool host_pinned(const void* p) {
+  cudaPointerAttributes a{};
+  if (cudaPointerGetAttributes(&a, p) != cudaSuccess) {
+    cudaGetLastError();
+    return false;
+  }
+  return a.type == cudaMemoryTypeHost;
+}
+
 int bbsi_cuda_dyson_rgf_z(int l, int w, int bs, int n_energy, const double* H, const double* z, const double* sigma,
                           double* G, int* fail_layers, int chunk) {
   if (int rc = validate_layout(l, w, bs, nullptr)) return rc;
@@ -647,9 +692,14 @@ int bbsi_cuda_dyson_rgf_z(int l, int w, int bs, int n_energy, const double* H, c
   int* dstat = static_cast<int*>(arena_get(15, sizeof(int) * size_t(l) * n_energy));
   if (!dH || !dG || !dzs || !scratch || !dstat)
     return fail(BBSI_OUT_OF_MEMORY, "Dyson batch workspace allocation failed");
-  cudaStream_t sc = nullptr, sd = nullptr;
-  CK(cudaStreamCreateWithFlags(&sc, cudaStreamNonBlocking));
-  CK(cudaStreamCreateWithFlags(&sd, cudaStreamNonBlocking));
+  E2eStreams& es = e2e_streams();
+  cudaStream_t sc = es.sc, sd = es.sd;
+  if (!sc || !sd) return fail(BBSI_CUDA_ERROR, "stream creation failed");
+  // z and sigma through a pinned staging buffer (the graph's copy nodes read it at replay)
+  double2* zst = e2e_stage(size_t(n_energy) + l);
+  if (!zst) return fail(BBSI_OUT_OF_MEMORY, "pinned staging allocation failed");
+  std::memcpy(zst, z, sizeof(double2) * n_energy);
+  std::memcpy(zst + n_energy, sigma, sizeof(double2) * l);
   std::vector<cudaEvent_t> done(nchunk), freed(nbuf);
   for (auto& e : done) CK(cudaEventCreateWithFlags(&e, cudaEventDisableTiming));
   for (auto& e : freed) CK(cudaEventCreateWithFlags(&e, cudaEventDisableTiming));
@@ -669,15 +719,19 @@ int bbsi_cuda_dyson_rgf_z(int l, int w, int bs, int n_energy, const double* H, c
   };
   bool first_copy = true;
   int rc = BBSI_OK;
-  auto body = [&]() -> int {
+  cudaEvent_t join = nullptr;
+  CK(cudaEventCreateWithFlags(&join, cudaEventDisableTiming));
+  // everything the call puts on the GPU, on sc (compute) and sd (copies back), ending
+  // with sc joined to sd: replayed as one CUDA graph when H and G are pinned
+  auto enqueue = [&](cudaStream_t) -> cudaError_t {
     mark("start", sc);
-    CK(cudaMemcpyAsync(dH, H, band_b, cudaMemcpyHostToDevice, sc));
-    CK(cudaMemcpyAsync(dzs, z, sizeof(double2) * n_energy, cudaMemcpyHostToDevice, sc));
-    CK(cudaMemcpyAsync(dzs + n_energy, sigma, sizeof(double2) * l, cudaMemcpyHostToDevice, sc));
+    cudaError_t e;
+    if ((e = cudaMemcpyAsync(dH, H, band_b, cudaMemcpyHostToDevice, sc))) return e;
+    if ((e = cudaMemcpyAsync(dzs, zst, sizeof(double2) * (size_t(n_energy) + l), cudaMemcpyHostToDevice, sc))) return e;
     std::vector<int> nt(l, bs);
     for (int c = 0; c < nchunk; ++c) {
       const int e0 = c * chunk, ne = std::min(chunk, n_energy - e0), buf = c % nbuf;
-      if (c >= nbuf) CK(cudaStreamWaitEvent(sc, freed[buf], 0));
+      if (c >= nbuf && (e = cudaStreamWaitEvent(sc, freed[buf], 0))) return e;
       double2* g = dG + size_t(buf) * chunk * band;
       SweepWork W;
       W.l = l;
@@ -694,12 +748,10 @@ int bbsi_cuda_dyson_rgf_z(int l, int w, int bs, int n_energy, const double* H, c
         W.sigdev = dzs + n_energy;
       }
       sweep_carve(W, scratch);
-      if (W.zdev)
-        CK(dyson_form_diag_ends(g, dH, l, w, bs, ne, dzs + e0, dzs + n_energy, sweep_is_two_ended(W), sc));
-      else if (w == 1)
-        CK(dyson_form_diag(g, dH, l, w, bs, ne, dzs + e0, dzs + n_energy, sc));
-      else
-        CK(dyson_form_band(g, dH, l, w, bs, ne, dzs + e0, dzs + n_energy, sc));
+      e = W.zdev    ? dyson_form_diag_ends(g, dH, l, w, bs, ne, dzs + e0, dzs + n_energy, sweep_is_two_ended(W), sc)
+          : w == 1 ? dyson_form_diag(g, dH, l, w, bs, ne, dzs + e0, dzs + n_energy, sc)
+                   : dyson_form_band(g, dH, l, w, bs, ne, dzs + e0, dzs + n_energy, sc);
+      if (e) return e;
       W.status = dstat + e0;
       W.status_stride = n_energy;
       // finished band rows of the downward sweep -> host, on the copy stream, while the
@@ -716,14 +768,26 @@ int bbsi_cuda_dyson_rgf_z(int l, int w, int bs, int n_energy, const double* H, c
         return cudaMemcpy2DAsync(dst, band_b, src, band_b, size_t(r1 - r0) * row_b, size_t(ne_g),
                                  cudaMemcpyDeviceToHost, sd);
       };
-      CK(rgf_sweeps(W, nt.data(), sc));
-      CK(cudaEventRecord(done[c], sc));
+      if ((e = rgf_sweeps(W, nt.data(), sc))) return e;
+      if ((e = cudaEventRecord(done[c], sc))) return e;
       mark("chunk " + std::to_string(c) + " computed", sc);
-      CK(cudaStreamWaitEvent(sd, done[c], 0));
-      CK(cudaEventRecord(freed[buf], sd));
+      if ((e = cudaStreamWaitEvent(sd, done[c], 0))) return e;
+      if ((e = cudaEventRecord(freed[buf], sd))) return e;
       mark("chunk " + std::to_string(c) + " copied", sd);
     }
-    CK(cudaStreamSynchronize(sd));
+    if ((e = cudaEventRecord(join, sd))) return e;
+    return cudaStreamWaitEvent(sc, join, 0);
+  };
+  auto body = [&]() -> int {
+    const bool graphable = !trace && host_pinned(H) && host_pinned(G);
+    if (graphable) {
+      const std::string key = graph_key("e2e", {l, w, bs, n_energy, chunk, groups, nbuf, (long long)H, (long long)G,
+                                                (long long)dH, (long long)dG, (long long)dzs, (long long)scratch,
+                                                (long long)dstat, (long long)zst, e2e_rows(), two_ended_default()});
+      CK(run_graphed(key, sc, enqueue));
+    } else {
+      CK(enqueue(sc));
+    }
     CK(cudaStreamSynchronize(sc));
     CK(cudaMemcpy(status.data(), dstat, sizeof(int) * status.size(), cudaMemcpyDeviceToHost));
     return BBSI_OK;
@@ -740,8 +804,7 @@ int bbsi_cuda_dyson_rgf_z(int l, int w, int bs, int n_energy, const double* H, c
   for (auto& e : done) cudaEventDestroy(e);
   for (auto& e : freed) cudaEventDestroy(e);
   cudaEventDestroy(rows_ev);
-  cudaStreamDestroy(sc);
-  cudaStreamDestroy(sd);
+  cudaEventDestroy(join);
   if (rc) return rc;
   bool bad = false;
   for (int e = 0; e < n_energy; ++e) {
