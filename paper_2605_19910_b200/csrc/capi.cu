@@ -5,6 +5,7 @@
 #include <map>
 #include <cstdlib>
 #include <cstring>
+#include <algorithm>
 #include <complex>
 #include <mutex>
 #include <random>
@@ -677,8 +678,9 @@ int bbsi_cuda_dyson_rgf_z(int l, int w, int bs, int n_energy, const double* H, c
       chunk = (chunk + 1) / 2;
   }
   const int nchunk = (n_energy + chunk - 1) / chunk;
-  // two groups per chunk here: with up to 16 (dyson_groups) every group's rows reach the
-  // copy stream in small pieces and the end-to-end time doubled (2.38 vs 1.12 s)
+  // two groups per chunk here: the copy stream, not the sweeps, bounds this path, and
+  // more groups hand it smaller pieces (graph replay, config 2: 2 / 4 / 8 / 16 groups
+  // 1.112 / 1.113 / 1.120 / 1.148 s; eager with 16 groups: 2.38 s)
   const int groups = default_groups(chunk, bs);
   const size_t scr_b = sweep_scratch_bytes(l, w, bs, chunk, groups, two_ended_default());
   int nbuf = nchunk;
