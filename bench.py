@@ -320,7 +320,21 @@ def run_ours(args, rank, world, local_rank):
             t = torch.tensor([dt], device=dev, dtype=torch.float64)
             dist.all_reduce(t, op=dist.ReduceOp.MAX)
             dt = float(t.item())
+        # the PCIe device->host rate of this box (4 GiB pinned copy, best of 3): G's bytes at
+        # that rate are the floor of this path
+        dbuf = torch.empty(1 << 28, dtype=torch.complex128, device=dev)
+        hbuf = torch.empty(1 << 28, dtype=torch.complex128).pin_memory()
+        best = 0.0
+        for _ in range(3):
+            torch.cuda.synchronize()
+            t1 = time.perf_counter()
+            hbuf.copy_(dbuf, non_blocking=True)
+            torch.cuda.synchronize()
+            best = max(best, dbuf.numel() * 16 / (time.perf_counter() - t1) / 1e9)
+        del dbuf, hbuf
+        d2h_b = 16 * band * n_loc
         e2e = {"value": n_all * l / dt, "unit": UNIT, "ms_per_step": round(dt * 1e3, 2),
+               "pcie_d2h_gbs": round(best, 1), "d2h_floor_ms": round(d2h_b / (best * 1e9) * 1e3, 1),
                "h2d_bytes_per_step": int(16 * band + 16 * n_loc + 16 * l) * world,
                "d2h_bytes_per_step": int(16 * band * n_loc + 4 * n_loc) * world,
                "path": "bbsi_cuda_dyson_rgf_z (host H in, every G band out, pinned host memory)"}
