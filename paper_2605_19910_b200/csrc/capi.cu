@@ -664,15 +664,15 @@ int bbsi_cuda_dyson_rgf_z(int l, int w, int bs, int n_energy, const double* H, c
   size_t free_b = 0, total_b = 0;
   CK(cudaMemGetInfo(&free_b, &total_b));
   free_b += arena_held({1, 4, 5});  // this call's own workspace slots are reused or regrown
-  // Default: chunks of at most 24 energies once there are >= 48 (measured on B200,
-  // config 2: one 64-energy chunk 1.27 s; chunks of 40 / 32 / 28 / 24 / 22 / 20 / 16:
-  // 1.18 / 1.17 / 1.15 / 1.13 / 1.13 / 1.16 / 1.22 s): the G stream (53 GB/s over
-  // PCIe) starts when the first chunk's rows are final and then stays busy while later
-  // chunks compute; below ~20 energies per chunk the compute falls behind the copy.
-  // Smaller chunks when HBM is short.
+  // Default: chunks of at most 12 energies once there are >= 24. Measured on B200,
+  // config 2, CUDA-graph replay, e2e time above the box's PCIe copy floor (0.90-0.99 s):
+  // chunks of 8 / 10 / 12 / 16 / 20 / 24 / 32 energies +155 / +130 / +140..177 / +119..155
+  // / +194 / +188 / +200 ms; one chunk of 64 (eager) 1.27 s. The G stream starts when the
+  // first chunk's rows are final and then stays busy while later chunks compute; with
+  // smaller chunks the compute falls behind the copy. Smaller chunks when HBM is short.
   if (chunk <= 0 || chunk > n_energy) {
-    const int nc = (n_energy + 23) / 24;
-    chunk = n_energy >= 48 ? (n_energy + nc - 1) / nc : n_energy;
+    const int nc = (n_energy + 11) / 12;
+    chunk = n_energy >= 24 ? (n_energy + nc - 1) / nc : n_energy;
     while (chunk > 1 && (size_t(chunk) * band_b + band_b +
                          sweep_scratch_bytes(l, w, bs, chunk, default_groups(chunk, bs), two_ended_default())) > free_b * 9 / 10)
       chunk = (chunk + 1) / 2;
