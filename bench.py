@@ -100,31 +100,35 @@ class ClockSampler:
 
 
 # ---------------------------------------------------------------------------- CPU reference
-def cpu_reference(cfg, n_energies: int, threads_per_energy: int, nproc: int):
-    """Times the compiled, unmodified reference rgf_tridiag / rgf_ndiag (oracle/_ref) on
-    n_energies energies of cfg, each with threads_per_energy BLAS threads, run
-    concurrently on host threads. Returns (seconds, energies)."""
+def energy_sample(n_all: int, k: int) -> list:
+    """k energy indices spread over the whole grid (both ends included)."""
+    k = max(1, min(k, n_all))
+    return sorted({int(round(x)) for x in np.linspace(0, n_all - 1, k)})
+
+
+def cpu_inputs(cfg, energies):
+    """Reference-arm inputs: A(E) = z I - H - Sigma in slot memory from the oracle's own
+    restatement of the generator (oracle/dyson_oracle.py), so no repo library is mapped
+    by the reference process. Built before any timed region."""
+    from oracle import dyson_oracle as DO
     from oracle import ref_lib as R
-    from paper_2605_19910_b200 import dyson as D
+
+    h = DO.hamiltonian(cfg.num_layers, cfg.bandwidth, cfg.block_size, cfg.seed)
+    zs = cfg.z()
+    return [R.to_slots(DO.dyson_matrix(h, complex(zs[e]), cfg.sigma_layers)) for e in energies]
+
+
+def cpu_reference(cfg, inputs, threads_per_energy: int):
+    """Times the compiled, unmodified reference rgf_tridiag / rgf_ndiag (oracle/_ref) on
+    the prepared inputs (one host thread each, threads_per_energy BLAS threads each).
+    Returns seconds."""
+    from oracle import ref_lib as R
 
     L = R.lib()
     l, w, b = cfg.num_layers, cfg.bandwidth, cfg.block_size
-    h = D.fill_h_host(cfg)  # slot memory [a, off, col, row]
-    zs = cfg.z()
-    sig = cfg.sigma()
-    idx = np.arange(b)
     fn = L.ref_rgf_tridiag if w == 1 else L.ref_rgf_ndiag
     L.ref_set_threads(C.c_int(threads_per_energy))
-    inputs = []
-    for e in range(n_energies):
-        a = -h
-        z = zs[e % len(zs)]
-        for layer in range(l):
-            d = a[layer, w]
-            hd = h[layer, w][idx, idx]
-            d[idx, idx] = ((z.real - hd.real) - sig[layer].real) + 1j * ((z.imag - hd.imag) - sig[layer].imag)
-        inputs.append(a)
-    outs = [np.empty_like(h) for _ in range(n_energies)]
+    outs = [np.empty_like(a) for a in inputs]
     errs = []
 
     def run(e):
@@ -137,7 +141,7 @@ def cpu_reference(cfg, n_energies: int, threads_per_energy: int, nproc: int):
             errs.append(rc)
 
     t0 = time.perf_counter()
-    ths = [threading.Thread(target=run, args=(e,)) for e in range(n_energies)]
+    ths = [threading.Thread(target=run, args=(e,)) for e in range(len(inputs))]
     for t in ths:
         t.start()
     for t in ths:
@@ -145,51 +149,64 @@ def cpu_reference(cfg, n_energies: int, threads_per_energy: int, nproc: int):
     dt = time.perf_counter() - t0
     if errs:
         raise RuntimeError(f"reference solve failed: {errs}")
-    return dt, n_energies
+    return dt
 
 
 def cpu_baseline_block(cfg, nproc: int):
     """Best of (i) energy-parallel, 1 BLAS thread per energy and (ii) one energy with
-    nproc BLAS threads."""
-    n_par = nproc
-    t_par, e_par = cpu_reference(cfg, n_par, 1, nproc)
-    t_one, e_one = cpu_reference(cfg, 1, nproc, nproc)
-    r_par, r_one = e_par / t_par, e_one / t_one
+    nproc BLAS threads. The energies span the whole grid."""
+    idx = energy_sample(cfg.n_energy, nproc)
+    inputs = cpu_inputs(cfg, idx)
+    t_par = cpu_reference(cfg, inputs, 1)
+    t_one = cpu_reference(cfg, inputs[len(inputs) // 2: len(inputs) // 2 + 1], nproc)
+    r_par, r_one = len(idx) / t_par, 1 / t_one
     if r_par >= r_one:
-        rate, sample, cores = r_par, f"{e_par} energies of {cfg.name}, one per host thread, 1 BLAS thread each", n_par
+        rate, sample, cores = r_par, f"energies {idx} of {cfg.name}, one per host thread, 1 BLAS thread each", \
+            min(nproc, len(idx))
     else:
-        rate, sample, cores = r_one, f"1 energy of {cfg.name}, {nproc} BLAS threads", nproc
+        rate, sample, cores = r_one, f"energy {idx[len(idx) // 2]} of {cfg.name}, {nproc} BLAS threads", nproc
     return {"value": rate * cfg.num_layers, "unit": UNIT, "cores": cores, "kind": "reference",
             "sample": sample, "seconds": {"energy_parallel": round(t_par, 3), "threaded_blas": round(t_one, 3)},
             "energies_per_s": rate}
 
 
+def workload_config(cfg, n_energies: int) -> dict:
+    """The `config` object of both arms (identical keys and values)."""
+    l, w, b = cfg.num_layers, cfg.bandwidth, cfg.block_size
+    gb = 16 * l * (2 * w + 1) * b * b * n_energies / 2**30
+    return {"workload": cfg.name, "num_layers": l, "block_size": b, "bandwidth": w, "energies": n_energies,
+            "eta": cfg.eta, "seed": cfg.seed,
+            "l2": (f"inputs larger than L2 (G band {gb:.1f} GiB)" if gb * 2**30 > 126e6 else
+                   "L2-resident workload (below the 126 MB L2; not flushed)")}
+
+
 # ---------------------------------------------------------------------------- reference arm
 def run_reference(args, rank, world):
-    from paper_2605_19910_b200 import dyson as D
+    from paper_2605_19910_b200.dyson import CONFIGS
 
     if rank != 0:
         return
-    cfg = D.CONFIGS[args.config]
+    cfg = CONFIGS[args.config]
     nproc = os.cpu_count() or 1
+    idx = energy_sample(cfg.n_energy, nproc)
+    inputs = cpu_inputs(cfg, idx)  # outside the timed region
     for _ in range(args.warmup):
-        cpu_reference(cfg, nproc, 1, nproc)
-    times = []
-    for _ in range(args.steps):
-        dt, ne = cpu_reference(cfg, nproc, 1, nproc)
-        times.append(dt)
+        cpu_reference(cfg, inputs, 1)
+    times = [cpu_reference(cfg, inputs, 1) for _ in range(args.steps)]
     tot = sum(times)
-    value = args.steps * nproc * cfg.num_layers / tot
+    value = args.steps * len(idx) * cfg.num_layers / tot
+    sample = (f"energies {idx} of the {cfg.n_energy}-point grid per step, one per host thread, 1 BLAS thread "
+              f"each (compiled reference, oracle/_ref)")
+    maps = Path("/proc/self/maps").read_text() if Path("/proc/self/maps").exists() else ""
     line = {"impl": "reference", "metric": METRIC, "value": value, "unit": UNIT, "n_gpus": args.gpus,
             "steps": args.steps, "warmup": args.warmup, "ms_per_step": 1e3 * tot / args.steps,
             "higher_is_better": True, "scaling": "strong", "vs_baseline": None, "dtype": "c128 (f64)",
-            "data": "synthetic (seeded Dyson generator, csrc/dyson_gen.h)",
-            "config": {"workload": cfg.name, "num_layers": cfg.num_layers, "block_size": cfg.block_size,
-                       "bandwidth": cfg.bandwidth, "energies": cfg.n_energy, "eta": cfg.eta, "seed": cfg.seed,
-                       "solver": "reference rgf_tridiag (oracle/_ref, OpenBLAS 0.3.15)"},
-            "cpu_baseline": {"value": value, "unit": UNIT, "cores": nproc, "kind": "reference",
-                             "sample": f"{nproc} energies of {cfg.name} per step, one per host thread, 1 BLAS "
-                                       f"thread each"},
+            "data": "synthetic (seeded Dyson generator; oracle/dyson_oracle.py restatement)",
+            "config": workload_config(cfg, cfg.n_energy),
+            "solver": "reference rgf_tridiag / rgf_ndiag (oracle/_ref: unmodified headers, OpenBLAS 0.3.15)",
+            "cpu_baseline": {"value": value, "unit": UNIT, "cores": len(idx), "kind": "reference",
+                             "sample": sample},
+            "repo_library_mapped": "libbbsi_cuda" in maps,
             "e2e": {"value": value, "unit": UNIT, "h2d_bytes_per_step": 0, "d2h_bytes_per_step": 0}}
     print(json.dumps(line), flush=True)
 
@@ -352,10 +369,8 @@ def run_ours(args, rank, world, local_rank):
                 "warmup": max(3, args.warmup), "ms_per_step": ms_step, "higher_is_better": True, "scaling": "strong",
                 "vs_baseline": None, "dtype": "c128 (f64)", "data": "synthetic (seeded Dyson generator, "
                 "csrc/dyson_gen.h)",
-                "config": {"workload": cfg.name, "num_layers": l, "block_size": b, "bandwidth": w,
-                           "energies": n_all, "eta": cfg.eta, "seed": cfg.seed, "solver": "rgf (batched sweeps)",
-                           "parallelism": f"energy shards x{world}", "l2": "inputs larger than L2 (G band "
-                           f"{16 * l * (2 * w + 1) * b * b * n_all / 2**30:.1f} GiB)"},
+                "config": workload_config(cfg, n_all), "solver": "rgf (batched two-ended sweeps)",
+                "parallelism": f"energy shards x{world}",
                 "energies_per_s": n_all / (ms_step * 1e-3), "tflops_algorithmic": tflops,
                 "gpu_launches": int(launches), "clocks": clocks.summary(), "roofline": roofline,
                 "e2e": e2e, "cpu_baseline": cpu}

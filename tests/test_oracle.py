@@ -130,3 +130,60 @@ def test_restatement_on_dyson_matrix_matches_reference():
     g2, _ = R.rgf_tridiag(a)
     assert O.max_block_error(g1, g2) <= 1e-12
     assert O.max_block_error(g1, O.oracle_selected_inverse(a)) <= 1e-10
+
+
+# ---- streaming restatement (oracle/stream/rgf_stream.cpp), the full-size config-5 checker
+@pytest.mark.skipif(not R.available(), reason="oracle/_ref not built (needs /root/reference)")
+@pytest.mark.parametrize("ckpt", [0, 1, 4, 7, 21])
+def test_stream_oracle_bitwise_vs_reference(ckpt):
+    """Same BLAS build as oracle/_ref (OpenBLAS 0.3.15): every G block and every A block
+    is bit-identical to the compiled reference rgf_tridiag, for any checkpoint length."""
+    from oracle import stream_lib as S
+
+    S.use_fast(False)
+    S.set_threads(1)
+    l, b, seed, z = 21, 32, 5, complex(0.3, 1e-4)
+    a = DO.dyson_matrix(DO.hamiltonian(l, 1, b, seed), z, 1)
+    ref, _ = R.rgf_tridiag(a)
+    s = S.DysonStream(l, b, seed, z, 1, ckpt=ckpt)
+    for i in range(l):
+        for off in (-1, 0, 1):
+            if 0 <= i + off < l:
+                assert np.array_equal(s.block(i, off), a.block(i, off))
+    n = 0
+    while (r := s.next()) is not None:
+        i, d, u, lo = r
+        assert np.array_equal(d, ref.block(i, 0))
+        if i > 0:
+            assert np.array_equal(u, ref.block(i - 1, 1)) and np.array_equal(lo, ref.block(i, -1))
+        n += 1
+    assert n == l
+
+
+@pytest.mark.skipif(not R.available(), reason="oracle/_ref not built (needs /root/reference)")
+def test_stream_oracle_fast_blas_vs_reference():
+    """The scipy-OpenBLAS build used at full size agrees with the reference to <= 1e-13
+    (different BLAS kernels, same calls) and its perturbed stream moves A by one ulp."""
+    from oracle import stream_lib as S
+
+    S.use_fast(True)
+    try:
+        S.set_threads(1)
+        l, b, seed, z = 17, 48, 4, complex(-1.0, 1e-5)
+        a = DO.dyson_matrix(DO.hamiltonian(l, 1, b, seed), z, 1)
+        ref, _ = R.rgf_tridiag(a)
+        s = S.DysonStream(l, b, seed, z, 1, ckpt=5)
+        worst = 0.0
+        while (r := s.next()) is not None:
+            i, d, u, lo = r
+            worst = max(worst, O.rel_frobenius_error(d, ref.block(i, 0)))
+            if i > 0:
+                worst = max(worst, O.rel_frobenius_error(u, ref.block(i - 1, 1)),
+                            O.rel_frobenius_error(lo, ref.block(i, -1)))
+        assert worst <= 1e-13
+        p = S.DysonStream(l, b, seed, z, 1, pert=0.5, pert_seed=3, ckpt=5)
+        x, y = a.block(3, 0), p.block(3, 0)
+        rel = np.abs(y.view(np.float64) - x.view(np.float64)) / np.abs(x.view(np.float64))
+        assert 0.3 < np.mean(rel > 0) < 0.7 and rel.max() <= 2.0**-52
+    finally:
+        S.use_fast(False)
