@@ -112,12 +112,16 @@ int bbsi_cuda_dyson_rgf_z(int l, int w, int bs, int n_energy, const double* H, c
 /* Resident stabilised DDRGF of one band (w = 1): dA, dG device [l][3][bs][bs],
  * interior groups of s2 layers (single-level plan). */
 int bbsi_cuda_ddrgf_dev(int l, int bs, int s2, const double* dA, double* dG, int* fail_layer, void* stream);
-/* Domain-sharded DDRGF (one process per GPU). Tasks = interleave_permutation(l,1,s2)
+/* Domain-sharded DDRGF, phase by phase (one process per GPU, the caller does the
+ * collectives; paper_2605_19910_b200/distributed.py). Tasks = interleave_permutation(l,1,s2)
  * groups (partition.hpp:39-75), T = bbsi_cuda_ddrgf_num_tasks(l, s2). A rank owning
  * tasks [t0,t1) holds the band rows of layers [first(t0), sep(t1-1)] (dA/dG local,
- * [rows][3][bs][bs], slot order). Protocol: phase1 -> all-gather of the packets
- * (packet_bytes(t1-t0) per rank, T packets in task order) -> phase2 (identical on
- * every rank) -> phase3. Only the packets (9 bs x bs blocks per task) are exchanged. */
+ * [rows][3][bs][bs], slot order). Protocol:
+ *   phase1 -> all-gather of the packets (packet_bytes(t1-t0) per rank, T packets in
+ *   task order) -> phase2 (identical on every rank) -> phase3 (chains, in place) ->
+ *   halo (2 blocks per rank) all-gathered -> couplings (the previous rank's halo[1] and
+ *   the next rank's halo[0]; NULL at the ends).
+ * Only the packets (9 bs x bs blocks per task) and the halos cross ranks. */
 int bbsi_cuda_ddrgf_num_tasks(int l, int s2);
 long long bbsi_cuda_ddrgf_packet_bytes(int ntask, int bs);
 long long bbsi_cuda_ddrgf_phase2_bytes(int ntask, int bs);
@@ -127,6 +131,43 @@ int bbsi_cuda_ddrgf_phase2_dev(int l, int bs, int s2, const double* dPackets, do
                                void* stream);
 int bbsi_cuda_ddrgf_phase3_dev(int l, int bs, int s2, int t0, int t1, const double* dA, double* dG, const double* dOut,
                                int* fail_layer, void* stream);
+/* dHalo [2][bs][bs] = { G[x0(t0), x0(t0)], G[sep(t1-1), sep(t1-1)] } after phase 3. */
+int bbsi_cuda_ddrgf_halo_dev(int l, int bs, int s2, int t0, int t1, const double* dG, double* dHalo, void* stream);
+/* The inter-chain coupling blocks G[x0_t, sep_{t-1}] and G[sep_t, x0_{t+1}] of the local
+ * tasks; dPrevSepG = previous rank's halo[1] (t0 > 0), dNextX0G = next rank's halo[0]
+ * (t1 < T), NULL otherwise. */
+int bbsi_cuda_ddrgf_couplings_dev(int l, int bs, int s2, int t0, int t1, const double* dA, double* dG,
+                                  const double* dOut, const double* dPrevSepG, const double* dNextX0G, void* stream);
+
+/* ---------------------------------------------------------------- multi-GPU (NCCL inside the library)
+ * The reference's concurrency seam is run_tasks inside ddrgf (ddrgf.hpp:239-262,
+ * 355-386); here domains map onto GPUs and NCCL carries the interface packets.
+ * NCCL is loaded at first use (dlopen libnccl.so.2); without it these return
+ * BBSI_CUDA_ERROR. */
+int bbsi_cuda_nccl_available(void);
+/* ncclGetUniqueId into out128 (128 bytes; rank 0 creates it, the caller broadcasts it). */
+int bbsi_cuda_nccl_unique_id(void* out128);
+/* ncclCommInitRank on the current device; *comm is an opaque ncclComm_t. */
+int bbsi_cuda_nccl_comm_init(const void* id128, int nranks, int rank, void** comm);
+void bbsi_cuda_nccl_comm_destroy(void* comm);
+/* The task range [t0,t1) and band rows [L0,L1) a rank owns (balanced contiguous ranges). */
+int bbsi_cuda_ddrgf_rank_layers(int l, int s2, int nranks, int rank, int* t0, int* t1, int* L0, int* L1);
+/* One rank of the domain-sharded DDRGF (one process per GPU): dA_loc / dG_loc are its
+ * band rows [L0, L1); phase 1, the NCCL all-gather of the packets, phase 2, phase 3, the
+ * halo all-gather and the couplings all run inside. Every rank returns the same
+ * status (a singular pivot anywhere is reported on all ranks). */
+int bbsi_cuda_ddrgf_rank_dev(void* comm, int l, int bs, int s2, const double* dA_loc, double* dG_loc,
+                             int* fail_layer, void* stream);
+/* bbsi::ddrgf (ddrgf.hpp:420-428) over ngpu GPUs of this process (devices: NULL = 0..ngpu-1):
+ * ncclCommInitAll, one host thread per GPU, domains sharded as above. Same arguments and
+ * results as bbsi_cuda_ddrgf_z. */
+int bbsi_cuda_ddrgf_multi_z(int l, int w, int bs, const int* sizes, const double* A, const int* s2_levels,
+                            int n_levels, int n_threads, int terminal_threads, int ngpu, const int* devices, double* G,
+                            long long* counters, int* fail_layer);
+/* bbsi_cuda_dyson_rgf_z with the energies sharded contiguously over ngpu GPUs (no collective). */
+int bbsi_cuda_dyson_rgf_multi_z(int l, int w, int bs, int n_energy, const double* H, const double* z,
+                                const double* sigma, double* G, int* fail_layers, int chunk, int ngpu,
+                                const int* devices);
 
 /* Dyson DDRGF for one energy z (host complex) from the shared device H. */
 int bbsi_cuda_dyson_ddrgf_dev(int l, int bs, const double* dH, const double* z, const double* sigma, int s2,

@@ -6,8 +6,12 @@
 //   #include "bbsi_gpu.hpp"        // this file: bbsi::gpu::rgf_tridiag / rgf_ndiag / ... on the GPU
 // and link libbbsi_cuda.so. Every function keeps the reference signature and
 // semantics (return by value, KernelCounters = the reference's logical counts,
-// invalid_argument_error / singular_matrix_error(layer) on the same conditions)
-// for T = std::complex<double>:
+// invalid_argument_error / singular_matrix_error(layer)) for T = std::complex<double>.
+// singular_matrix_error is raised on the reference's conditions for the RGF solvers
+// (the same pivots, the same layer). ddrgf differs by construction: the stabilised
+// formulation never inverts an isolated domain, so it reports a
+// singular pivot only where a domain WITH its boundary self-energies (or a separator)
+// is singular; the layer is the global layer of that pivot.
 //   rgf_tridiag  rgf.hpp:37-76      rgf_ndiag     rgf.hpp:82-137
 //   rgf_fused    rgf.hpp:143-192    rgf_extended  rgf.hpp:209-270
 //   ddrgf        ddrgf.hpp:420-428
@@ -16,6 +20,7 @@
 #pragma once
 
 #include <complex>
+#include <cstdlib>
 #include <cstring>
 #include <stdexcept>
 #include <string>
@@ -164,14 +169,27 @@ inline std::pair<ExtendedInverse<cd>, KernelCounters> rgf_extended(const BlockBa
   return {std::move(ext), detail::counters(c)};
 }
 
-inline std::pair<BlockBandedMatrix<cd>, KernelCounters> ddrgf(const BlockBandedMatrix<cd>& m, const DomainPlan& plan) {
+// ngpu > 1 shards the domains over GPUs 0..ngpu-1 of this process (NCCL all-gather of
+// the interface packets inside the library); ngpu = 0 reads BBSI_GPUS (default 1).
+inline std::pair<BlockBandedMatrix<cd>, KernelCounters> ddrgf(const BlockBandedMatrix<cd>& m, const DomainPlan& plan,
+                                                               int ngpu = 0) {
+  if (ngpu <= 0) {
+    const char* e = std::getenv("BBSI_GPUS");
+    ngpu = e ? std::atoi(e) : 1;
+    if (ngpu < 1) ngpu = 1;
+  }
   auto s = detail::to_slots(m);
   std::vector<cd> g(s.data.size());
   long long c[3];
   int fl = -1;
-  const int rc = bbsi_cuda_ddrgf_z(s.l, s.w, s.bs, s.sizes.data(), reinterpret_cast<const double*>(s.data.data()),
-                                  plan.s2_levels.data(), plan.n_levels(), plan.n_threads, plan.terminal_threads,
-                                  reinterpret_cast<double*>(g.data()), c, &fl);
+  const int rc =
+      ngpu > 1 ? bbsi_cuda_ddrgf_multi_z(s.l, s.w, s.bs, s.sizes.data(), reinterpret_cast<const double*>(s.data.data()),
+                                         plan.s2_levels.data(), plan.n_levels(), plan.n_threads,
+                                         plan.terminal_threads, ngpu, nullptr, reinterpret_cast<double*>(g.data()), c,
+                                         &fl)
+               : bbsi_cuda_ddrgf_z(s.l, s.w, s.bs, s.sizes.data(), reinterpret_cast<const double*>(s.data.data()),
+                                   plan.s2_levels.data(), plan.n_levels(), plan.n_threads, plan.terminal_threads,
+                                   reinterpret_cast<double*>(g.data()), c, &fl);
   detail::check(rc, fl);
   s.data.swap(g);
   return {detail::from_slots(m.layout(), s), detail::counters(c)};

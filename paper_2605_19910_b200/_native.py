@@ -40,6 +40,16 @@ SIGNATURES = {
     "bbsi_cuda_ddrgf_phase1_dev": (_i, [_i, _i, _i, _i, _i, _vp, _vp, _vp, _vp, _vp]),
     "bbsi_cuda_ddrgf_phase2_dev": (_i, [_i, _i, _i, _vp, _vp, _vp, _vp]),
     "bbsi_cuda_ddrgf_phase3_dev": (_i, [_i, _i, _i, _i, _i, _vp, _vp, _vp, _vp, _vp]),
+    "bbsi_cuda_ddrgf_halo_dev": (_i, [_i, _i, _i, _i, _i, _vp, _vp, _vp]),
+    "bbsi_cuda_ddrgf_couplings_dev": (_i, [_i, _i, _i, _i, _i, _vp, _vp, _vp, _vp, _vp, _vp]),
+    "bbsi_cuda_nccl_available": (_i, []),
+    "bbsi_cuda_nccl_unique_id": (_i, [_vp]),
+    "bbsi_cuda_nccl_comm_init": (_i, [_vp, _i, _i, _vp]),
+    "bbsi_cuda_nccl_comm_destroy": (None, [_vp]),
+    "bbsi_cuda_ddrgf_rank_layers": (_i, [_i, _i, _i, _i, _ip, _ip, _ip, _ip]),
+    "bbsi_cuda_ddrgf_rank_dev": (_i, [_vp, _i, _i, _i, _vp, _vp, _vp, _vp]),
+    "bbsi_cuda_ddrgf_multi_z": (_i, [_i, _i, _i, _vp, _vp, _vp, _i, _i, _i, _i, _vp, _vp, _vp, _vp]),
+    "bbsi_cuda_dyson_rgf_multi_z": (_i, [_i, _i, _i, _i, _vp, _vp, _vp, _vp, _vp, _i, _i, _vp]),
     "bbsi_cuda_launch_count": (_ll, []),
     "bbsi_cuda_profile_enable": (None, [_i]),
     "bbsi_cuda_profile_collect": (_i, [_vp, _i]),

@@ -18,6 +18,7 @@ drop-in contract allows; float inputs are rejected).
 from __future__ import annotations
 
 import ctypes as C
+import os
 from dataclasses import dataclass, field
 
 import numpy as np
@@ -263,15 +264,25 @@ def rgf_extended(m: BlockBandedMatrix):
             KernelCounters(*map(int, cnt)))
 
 
-def ddrgf(m: BlockBandedMatrix, plan: DomainPlan):
-    """ddrgf.hpp:420-428 on the GPU (stabilised DDRGF)."""
+def ddrgf(m: BlockBandedMatrix, plan: DomainPlan, ngpu: int | None = None):
+    """ddrgf.hpp:420-428 on the GPU (stabilised DDRGF). ngpu > 1 shards the
+    domains over GPUs 0..ngpu-1 of this process (bbsi_cuda_ddrgf_multi_z: NCCL all-gather
+    of the interface packets); default: $BBSI_GPUS or 1."""
     plan.validate()
+    if ngpu is None:
+        ngpu = max(1, int(os.environ.get("BBSI_GPUS", "1")))
     lay, sizes, a, g = _args(m)
     s2 = np.array(plan.s2_levels, dtype=np.int32)
     cnt = np.zeros(3, dtype=np.int64)
     fail = C.c_int(-1)
-    rc = lib().bbsi_cuda_ddrgf_z(lay.num_layers, lay.bandwidth, lay.slot_size, _ptr(sizes), _ptr(a), _ptr(s2), len(s2),
-                                 plan.n_threads, plan.terminal_threads, _ptr(g), _ptr(cnt), C.byref(fail))
+    if ngpu > 1:
+        rc = lib().bbsi_cuda_ddrgf_multi_z(lay.num_layers, lay.bandwidth, lay.slot_size, _ptr(sizes), _ptr(a),
+                                           _ptr(s2), len(s2), plan.n_threads, plan.terminal_threads, ngpu, None,
+                                           _ptr(g), _ptr(cnt), C.byref(fail))
+    else:
+        rc = lib().bbsi_cuda_ddrgf_z(lay.num_layers, lay.bandwidth, lay.slot_size, _ptr(sizes), _ptr(a), _ptr(s2),
+                                     len(s2), plan.n_threads, plan.terminal_threads, _ptr(g), _ptr(cnt),
+                                     C.byref(fail))
     _raise(rc, fail.value)
     return BlockBandedMatrix._from_slots(lay, g), KernelCounters(*map(int, cnt))
 

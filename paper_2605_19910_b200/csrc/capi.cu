@@ -6,10 +6,12 @@
 #include <cstdlib>
 #include <cstring>
 #include <algorithm>
+#include <atomic>
 #include <complex>
 #include <mutex>
 #include <random>
 #include <string>
+#include <thread>
 #include <vector>
 
 #include "../../include/bbsi_cuda.h"
@@ -21,7 +23,6 @@ using namespace bbsi_gpu;
 namespace {
 
 thread_local std::string g_err;
-std::mutex g_call_mu;  // the workspace arena is shared: serialise host-buffer calls
 
 int fail(int code, const std::string& msg) {
   g_err = msg;
@@ -129,46 +130,66 @@ bool graphs_enabled() {
 template <class F>
 cudaError_t run_graphed(const std::string& key, cudaStream_t s, F&& enqueue) {
   if (!graphs_enabled() || prof_enabled() || s == nullptr) return enqueue(s);
-  std::lock_guard<std::mutex> lk(g_graph_mu);
-  auto it = g_graphs.find(key);
-  if (it == g_graphs.end()) {
-    g_graphs.emplace(key, GraphEntry{});
+  GraphEntry ent;
+  bool seen = false;
+  {
+    std::lock_guard<std::mutex> lk(g_graph_mu);
+    auto it = g_graphs.find(key);
+    if (it == g_graphs.end()) {
+      g_graphs.emplace(key, GraphEntry{});
+    } else {
+      seen = true;
+      ent = it->second;
+    }
+  }
+  if (!seen) return enqueue(s);  // first call: eager
+  if (ent.exec) {
+    launch_count_add(ent.launches);
+    return cudaGraphLaunch(ent.exec, s);
+  }
+  // second call: capture (keys are per host thread, so no other thread captures this one)
+  const long long c0 = launch_count();
+  auto forget = [&] {
+    std::lock_guard<std::mutex> lk(g_graph_mu);
+    g_graphs.erase(key);
+  };
+  cudaError_t e = cudaStreamBeginCapture(s, cudaStreamCaptureModeThreadLocal);
+  if (e) return e;
+  cudaError_t e2 = enqueue(s);
+  cudaGraph_t g = nullptr;
+  e = cudaStreamEndCapture(s, &g);
+  if (e2 || e) {
+    if (g) cudaGraphDestroy(g);
+    cudaGetLastError();
+    forget();  // fall back to eager launches for this key
     return enqueue(s);
   }
-  if (!it->second.exec) {
-    const long long c0 = launch_count();
-    cudaError_t e = cudaStreamBeginCapture(s, cudaStreamCaptureModeThreadLocal);
-    if (e) return e;
-    cudaError_t e2 = enqueue(s);
-    cudaGraph_t g = nullptr;
-    e = cudaStreamEndCapture(s, &g);
-    if (e2 || e) {
-      if (g) cudaGraphDestroy(g);
-      cudaGetLastError();
-      g_graphs.erase(it);  // fall back to eager launches for this key
-      return enqueue(s);
-    }
-    cudaGraphExec_t x = nullptr;
-    e = cudaGraphInstantiate(&x, g, 0);
-    cudaGraphDestroy(g);
-    if (e) {
-      cudaGetLastError();
-      g_graphs.erase(it);
-      return enqueue(s);
-    }
-    it->second.exec = x;
-    it->second.launches = launch_count() - c0;
-    return cudaGraphLaunch(x, s);
+  cudaGraphExec_t x = nullptr;
+  e = cudaGraphInstantiate(&x, g, 0);
+  cudaGraphDestroy(g);
+  if (e) {
+    cudaGetLastError();
+    forget();
+    return enqueue(s);
   }
-  launch_count_add(it->second.launches);
-  return cudaGraphLaunch(it->second.exec, s);
+  {
+    std::lock_guard<std::mutex> lk(g_graph_mu);
+    g_graphs[key] = GraphEntry{x, launch_count() - c0};
+  }
+  return cudaGraphLaunch(x, s);
 }
 
+// Graph keys name the device and the host thread (workspaces are per thread) plus the
+// shapes and every device pointer the launch sequence touches.
 std::string graph_key(const char* tag, std::initializer_list<long long> v) {
   std::string k(tag);
   int dev = 0;
   cudaGetDevice(&dev);
-  k += ":" + std::to_string(dev);
+  thread_local const unsigned long long tid = [] {
+    static std::atomic<unsigned long long> next{0};
+    return next++;
+  }();
+  k += ":" + std::to_string(dev) + ":t" + std::to_string(tid);
   for (long long x : v) k += ":" + std::to_string(x);
   return k;
 }
@@ -187,14 +208,13 @@ int run_sweeps(SweepWork& W, const std::vector<int>& n_true, std::vector<int>& f
 // Single-matrix drop-in solve of the padded band (shared by tridiag/ndiag/fused).
 int solve_host(const HostBand& h, double2* Gout, int* fail_layer) {
   if (int rc = device_ok()) return rc;
-  std::lock_guard<std::mutex> lk(g_call_mu);
   const int bp = pad64(h.bs);
   std::vector<double2> staging;
   pad_band(h, bp, staging);
   const size_t bytes = staging.size() * sizeof(double2);
   double2* dG = static_cast<double2*>(arena_get(0, bytes));
   if (!dG) return fail(BBSI_OUT_OF_MEMORY, "band allocation failed");
-  cudaStream_t s = 0;
+  cudaStream_t s = thread_stream(0);
   CK(cudaMemcpyAsync(dG, staging.data(), bytes, cudaMemcpyHostToDevice, s));
   SweepWork W;
   W.l = h.l;
@@ -339,7 +359,6 @@ int bbsi_cuda_rgf_batched_dev(int l, int w, int bs, int batch, const double* dA,
   W.G = reinterpret_cast<double2*>(dG);
   W.g_bstride = band;
   std::vector<int> nt(l, bs), fails;
-  std::lock_guard<std::mutex> lk(g_call_mu);
   if (int rc = run_sweeps(W, nt, fails, s)) return rc;
   bool bad = false;
   for (int b = 0; b < batch; ++b) {
@@ -359,6 +378,34 @@ static bool form_in_gemm() {
   return on;
 }
 
+// The two-ended sweep eliminates layers in another order than rgf_tridiag / rgf_ndiag
+// (rgf.hpp:58-64, 100-114), so its pivots are different matrices: an energy whose
+// two-ended sweep hits a negligible pivot is re-solved with the reference's one-ended
+// order. Either that succeeds (its band replaces the failed one) or it reports the layer
+// the reference would (*fail_layer).
+static cudaError_t dyson_retry_one_ended(int l, int w, int bs, const double2* dH, const double2* dz,
+                                         const double2* dsig, double2* dGb, int* fail_layer, cudaStream_t s) {
+  SweepWork W;
+  W.l = l;
+  W.w = w;
+  W.bs = bs;
+  W.batch = 1;
+  W.G = dGb;
+  W.g_bstride = (long long)l * (2 * w + 1) * bs * bs;
+  W.groups = 1;
+  W.two_ended = false;
+  void* scr = arena_get(19, sweep_scratch_bytes(l, w, bs, 1, 1, false));
+  if (!scr) return cudaErrorMemoryAllocation;
+  sweep_carve(W, scr);
+  cudaError_t e = dyson_form_band(dGb, dH, l, w, bs, 1, dz, dsig, s);
+  if (e) return e;
+  std::vector<int> nt(l, bs), fails;
+  if ((e = rgf_sweeps(W, nt.data(), s))) return e;
+  if ((e = collect_failures(W, fails, s))) return e;
+  *fail_layer = fails[0];
+  return cudaSuccess;
+}
+
 int bbsi_cuda_dyson_rgf_dev(int l, int w, int bs, int n_energy, const double* dH, const double* z,
                             const double* sigma, double* dG, int* fail_layers, void* stream) {
   if (int rc = validate_layout(l, w, bs, nullptr)) return rc;
@@ -367,7 +414,6 @@ int bbsi_cuda_dyson_rgf_dev(int l, int w, int bs, int n_energy, const double* dH
   if (n_energy < 1) return fail(BBSI_INVALID_ARGUMENT, "n_energy must be >= 1");
   if (int rc = device_ok()) return rc;
   cudaStream_t s = static_cast<cudaStream_t>(stream);
-  std::lock_guard<std::mutex> lk(g_call_mu);
   double2* dzs = static_cast<double2*>(arena_get(2, sizeof(double2) * (size_t(n_energy) + l)));
   if (!dzs) return fail(BBSI_OUT_OF_MEMORY, "parameter upload allocation failed");
   CK(cudaMemcpyAsync(dzs, z, sizeof(double2) * n_energy, cudaMemcpyHostToDevice, s));
@@ -406,6 +452,9 @@ int bbsi_cuda_dyson_rgf_dev(int l, int w, int bs, int n_energy, const double* dH
   CK(collect_failures(W, fails, s));
   bool bad = false;
   for (int b = 0; b < n_energy; ++b) {
+    if (fails[b] >= 0 && sweep_is_two_ended(W))
+      CK(dyson_retry_one_ended(l, w, bs, reinterpret_cast<const double2*>(dH), dzs + b, dzs + n_energy,
+                               reinterpret_cast<double2*>(dG) + size_t(b) * W.g_bstride, &fails[b], s));
     if (fail_layers) fail_layers[b] = fails[b];
     bad |= fails[b] >= 0;
   }
@@ -513,7 +562,6 @@ int bbsi_cuda_zinv_dev(int n, int n_true, int batch, double* dM, long long ld, l
     return fail(BBSI_INVALID_ARGUMENT, "zinv: requires n % 64 == 0 and 1 <= n_true <= n");
   if (int rc = device_ok()) return rc;
   cudaStream_t s = static_cast<cudaStream_t>(stream);
-  std::lock_guard<std::mutex> lk(g_call_mu);
   size_t scr = zinv_scratch_bytes(n, batch) + sizeof(int) * batch + 256;
   char* base = static_cast<char*>(arena_get(3, scr));
   if (!base) return fail(BBSI_OUT_OF_MEMORY, "zinv scratch allocation failed");
@@ -539,7 +587,6 @@ int bbsi_cuda_bench_kernels(int n, int batch, int samples, double* out) {
   if (n < 64 || n % 64 || batch < 1 || samples < 1 || !out)
     return fail(BBSI_INVALID_ARGUMENT, "bench_kernels: requires n % 64 == 0, batch >= 1, samples >= 1");
   if (int rc = device_ok()) return rc;
-  std::lock_guard<std::mutex> lk(g_call_mu);
   const long long nn = (long long)n * n;
   const size_t scr = zinv_scratch_bytes(n, batch) + sizeof(int) * batch + 256;
   double2* buf = static_cast<double2*>(arena_get(3, scr));
@@ -612,9 +659,7 @@ struct E2eStreams {
   cudaStream_t sc = nullptr, sd = nullptr;
 };
 static E2eStreams& e2e_streams() {
-  static std::mutex mu;
-  static std::vector<E2eStreams> v;
-  std::lock_guard<std::mutex> lk(mu);
+  thread_local std::vector<E2eStreams> v;  // per host thread
   int dev = 0;
   cudaGetDevice(&dev);
   if (int(v.size()) <= dev) v.resize(dev + 1);
@@ -625,7 +670,7 @@ static E2eStreams& e2e_streams() {
   return v[dev];
 }
 static double2* e2e_stage(size_t n) {
-  static std::vector<std::pair<double2*, size_t>> per_dev;
+  thread_local std::vector<std::pair<double2*, size_t>> per_dev;
   int dev = 0;
   cudaGetDevice(&dev);
   if (int(per_dev.size()) <= dev) per_dev.resize(dev + 1, {nullptr, 0});
@@ -658,7 +703,6 @@ int bbsi_cuda_dyson_rgf_z(int l, int w, int bs, int n_energy, const double* H, c
   if (w < 1 && l != 1) return fail(BBSI_INVALID_ARGUMENT, "rgf_ndiag: requires bandwidth >= 1");
   if (n_energy < 1) return fail(BBSI_INVALID_ARGUMENT, "n_energy must be >= 1");
   if (int rc = device_ok()) return rc;
-  std::lock_guard<std::mutex> lk(g_call_mu);
   const long long band = (long long)l * (2 * w + 1) * bs * bs;
   const size_t band_b = size_t(band) * sizeof(double2);
   size_t free_b = 0, total_b = 0;
@@ -816,6 +860,16 @@ int bbsi_cuda_dyson_rgf_z(int l, int w, int bs, int n_energy, const double* H, c
         f = j;
         break;
       }
+    SweepWork Wt;
+    Wt.l = l;
+    Wt.w = w;
+    Wt.two_ended = two_ended_default();
+    if (f >= 0 && sweep_is_two_ended(Wt)) {  // see dyson_retry_one_ended
+      double2* gb = static_cast<double2*>(arena_get(16, band_b));
+      if (!gb) return fail(BBSI_OUT_OF_MEMORY, "retry band allocation failed");
+      CK(dyson_retry_one_ended(l, w, bs, dH, dzs + e, dzs + n_energy, gb, &f, sc));
+      if (f < 0) CK(cudaMemcpy(reinterpret_cast<char*>(G) + size_t(e) * band_b, gb, band_b, cudaMemcpyDeviceToHost));
+    }
     if (fail_layers) fail_layers[e] = f;
     bad |= f >= 0;
   }
@@ -838,7 +892,6 @@ int bbsi_cuda_rgf_extended_z(int l, int w, int bs, const int* sizes, const doubl
   if (int rc = validate_layout(l, w, bs, sizes)) return rc;
   if (w != 1 && l != 1) return fail(BBSI_INVALID_ARGUMENT, "rgf_extended: requires bandwidth 1");
   if (int rc = device_ok()) return rc;
-  std::lock_guard<std::mutex> lk(g_call_mu);
   HostBand h = make_host(l, w, bs, sizes, A);
   const int bp = pad64(h.bs);
   const long long bb = (long long)bp * bp;
@@ -848,7 +901,7 @@ int bbsi_cuda_rgf_extended_z(int l, int w, int bs, const int* sizes, const doubl
   double2* dG = static_cast<double2*>(arena_get(0, bytes));
   double2* halo = static_cast<double2*>(arena_get(11, sizeof(double2) * size_t(4 * l + 4) * bb));
   if (!dG || !halo) return fail(BBSI_OUT_OF_MEMORY, "rgf_extended allocation failed");
-  cudaStream_t s = 0;
+  cudaStream_t s = thread_stream(0);
   CK(cudaMemcpyAsync(dG, staging.data(), bytes, cudaMemcpyHostToDevice, s));
   SweepWork W;
   W.l = l;
@@ -958,11 +1011,6 @@ static int validate_ddrgf(int l, int w, int bs, const int* sizes, const int* s2_
   return BBSI_OK;
 }
 
-static double ddrgf_gamma() {
-  if (const char* e = getenv("BBSI_DDRGF_GAMMA")) return atof(e);
-  return 1.0;
-}
-
 // Runs the stabilised DDRGF on device buffers; fills *fail_layer on a singular pivot.
 static int ddrgf_on_device(const double2* dA, double2* dG, int l, int bp, const std::vector<int>& n_true, int s2,
                            int* fail_layer, cudaStream_t s) {
@@ -970,7 +1018,7 @@ static int ddrgf_on_device(const double2* dA, double2* dG, int l, int bp, const 
   void* scr = arena_get(9, sb);
   if (!scr) return fail(BBSI_OUT_OF_MEMORY, "ddrgf workspace allocation failed");
   int fl = -1;
-  CK(ddrgf_device(dA, dG, l, bp, n_true.data(), s2, ddrgf_gamma(), scr, sb, &fl, s));
+  CK(ddrgf_device(dA, dG, l, bp, n_true.data(), s2, ddrgf_gamma0(), scr, sb, &fl, s));
   CK(cudaStreamSynchronize(s));
   if (fl >= 0) {
     if (fail_layer) *fail_layer = fl;
@@ -984,7 +1032,6 @@ int bbsi_cuda_ddrgf_z(int l, int w, int bs, const int* sizes, const double* A, c
   if (fail_layer) *fail_layer = -1;
   if (int rc = validate_ddrgf(l, w, bs, sizes, s2_levels, n_levels, n_threads, terminal_threads)) return rc;
   if (int rc = device_ok()) return rc;
-  std::lock_guard<std::mutex> lk(g_call_mu);
   HostBand h = make_host(l, w, bs, sizes, A);
   const int bp = pad64(h.bs);
   std::vector<double2> staging;
@@ -993,7 +1040,7 @@ int bbsi_cuda_ddrgf_z(int l, int w, int bs, const int* sizes, const double* A, c
   double2* dA = static_cast<double2*>(arena_get(0, bytes));
   double2* dG = static_cast<double2*>(arena_get(10, bytes));
   if (!dA || !dG) return fail(BBSI_OUT_OF_MEMORY, "band allocation failed");
-  cudaStream_t s = 0;
+  cudaStream_t s = thread_stream(0);
   CK(cudaMemcpyAsync(dA, staging.data(), bytes, cudaMemcpyHostToDevice, s));
   if (int rc = ddrgf_on_device(dA, dG, l, bp, h.sz, s2_levels[0], fail_layer, s)) return rc;
   CK(cudaMemcpyAsync(staging.data(), dG, bytes, cudaMemcpyDeviceToHost, s));
@@ -1009,7 +1056,6 @@ int bbsi_cuda_ddrgf_dev(int l, int bs, int s2, const double* dA, double* dG, int
   if (int rc = validate_ddrgf(l, 1, bs, nullptr, &one, 1, 1, 1)) return rc;
   if (bs % 64) return fail(BBSI_INVALID_ARGUMENT, "resident API requires bs % 64 == 0");
   if (int rc = device_ok()) return rc;
-  std::lock_guard<std::mutex> lk(g_call_mu);
   std::vector<int> nt(l, bs);
   return ddrgf_on_device(reinterpret_cast<const double2*>(dA), reinterpret_cast<double2*>(dG), l, bs, nt, s2,
                          fail_layer, static_cast<cudaStream_t>(stream));
@@ -1023,7 +1069,6 @@ int bbsi_cuda_dyson_ddrgf_dev(int l, int bs, const double* dH, const double* z, 
   if (bs % 64) return fail(BBSI_INVALID_ARGUMENT, "resident API requires bs % 64 == 0");
   if (int rc = device_ok()) return rc;
   cudaStream_t s = static_cast<cudaStream_t>(stream);
-  std::lock_guard<std::mutex> lk(g_call_mu);
   const size_t band_b = sizeof(double2) * size_t(l) * 3 * bs * bs;
   double2* dA = static_cast<double2*>(arena_get(0, band_b));
   double2* dzs = static_cast<double2*>(arena_get(2, sizeof(double2) * (size_t(1) + l)));
@@ -1057,10 +1102,9 @@ int bbsi_cuda_ddrgf_phase1_dev(int l, int bs, int s2, int t0, int t1, const doub
   if (bs % 64) return fail(BBSI_INVALID_ARGUMENT, "resident API requires bs % 64 == 0");
   if (t0 < 0 || t1 > ddrgf_num_tasks(l, s2) || t0 >= t1) return fail(BBSI_INVALID_ARGUMENT, "bad task range");
   if (int rc = device_ok()) return rc;
-  std::lock_guard<std::mutex> lk(g_call_mu);
   int fl = -1;
   cudaError_t e = ddrgf_phase1(reinterpret_cast<const double2*>(dA), reinterpret_cast<double2*>(dG), l, bs, nullptr,
-                               s2, ddrgf_gamma(), t0, t1, reinterpret_cast<double2*>(dPacket), &fl,
+                               s2, ddrgf_gamma0(), t0, t1, reinterpret_cast<double2*>(dPacket), &fl,
                                static_cast<cudaStream_t>(stream));
   if (e == cudaSuccess) e = cudaStreamSynchronize(static_cast<cudaStream_t>(stream));
   return phase_rc(e, fl, fail_layer, "ddrgf phase 1");
@@ -1073,9 +1117,8 @@ int bbsi_cuda_ddrgf_phase2_dev(int l, int bs, int s2, const double* dPackets, do
   if (int rc = validate_ddrgf(l, 1, bs, nullptr, &one, 1, 1, 1)) return rc;
   if (bs % 64) return fail(BBSI_INVALID_ARGUMENT, "resident API requires bs % 64 == 0");
   if (int rc = device_ok()) return rc;
-  std::lock_guard<std::mutex> lk(g_call_mu);
   int fl = -1;
-  cudaError_t e = ddrgf_phase2(reinterpret_cast<const double2*>(dPackets), l, bs, nullptr, s2, ddrgf_gamma(),
+  cudaError_t e = ddrgf_phase2(reinterpret_cast<const double2*>(dPackets), l, bs, nullptr, s2, ddrgf_gamma0(),
                                reinterpret_cast<double2*>(dOut), &fl, static_cast<cudaStream_t>(stream));
   return phase_rc(e, fl, fail_layer, "ddrgf phase 2");
 }
@@ -1088,7 +1131,6 @@ int bbsi_cuda_ddrgf_phase3_dev(int l, int bs, int s2, int t0, int t1, const doub
   if (bs % 64) return fail(BBSI_INVALID_ARGUMENT, "resident API requires bs % 64 == 0");
   if (t0 < 0 || t1 > ddrgf_num_tasks(l, s2) || t0 >= t1) return fail(BBSI_INVALID_ARGUMENT, "bad task range");
   if (int rc = device_ok()) return rc;
-  std::lock_guard<std::mutex> lk(g_call_mu);
   int fl = -1;
   cudaError_t e = ddrgf_phase3(reinterpret_cast<const double2*>(dA), reinterpret_cast<double2*>(dG), l, bs, nullptr, s2,
                                t0, t1, reinterpret_cast<const double2*>(dOut), &fl, static_cast<cudaStream_t>(stream));
@@ -1096,8 +1138,227 @@ int bbsi_cuda_ddrgf_phase3_dev(int l, int bs, int s2, int t0, int t1, const doub
   return phase_rc(e, fl, fail_layer, "ddrgf phase 3");
 }
 
+int bbsi_cuda_ddrgf_halo_dev(int l, int bs, int s2, int t0, int t1, const double* dG, double* dHalo, void* stream) {
+  if (t0 < 0 || s2 < 1 || l < 1 + s2 || t1 > ddrgf_num_tasks(l, s2) || t0 >= t1)
+    return fail(BBSI_INVALID_ARGUMENT, "bad task range");
+  CK(ddrgf_halo(reinterpret_cast<const double2*>(dG), l, bs, s2, t0, t1, reinterpret_cast<double2*>(dHalo),
+                static_cast<cudaStream_t>(stream)));
+  return BBSI_OK;
+}
+
+int bbsi_cuda_ddrgf_couplings_dev(int l, int bs, int s2, int t0, int t1, const double* dA, double* dG,
+                                  const double* dOut, const double* dPrevSepG, const double* dNextX0G, void* stream) {
+  if (t0 < 0 || s2 < 1 || l < 1 + s2 || t1 > ddrgf_num_tasks(l, s2) || t0 >= t1)
+    return fail(BBSI_INVALID_ARGUMENT, "bad task range");
+  if ((t0 > 0 && !dPrevSepG) || (t1 < ddrgf_num_tasks(l, s2) && !dNextX0G))
+    return fail(BBSI_INVALID_ARGUMENT, "ddrgf couplings: a neighbour's halo block is required");
+  CK(ddrgf_couplings(reinterpret_cast<const double2*>(dA), reinterpret_cast<double2*>(dG), l, bs, s2, t0, t1,
+                     reinterpret_cast<const double2*>(dOut), reinterpret_cast<const double2*>(dPrevSepG),
+                     reinterpret_cast<const double2*>(dNextX0G), static_cast<cudaStream_t>(stream)));
+  return BBSI_OK;
+}
+
 void bbsi_ddrgf_reference_counters(long long l, const int* s2_levels, int n_levels, long long* out) {
   ddrgf_reference_counters(l, s2_levels, n_levels, out);
 }
 
 }  // extern "C"
+
+// ------------------------------------------------------------------ multi-GPU (NCCL)
+// One process per GPU (torchrun / MPI style): the caller shares a NCCL unique id and
+// creates one communicator per rank; bbsi_cuda_ddrgf_rank_dev then runs the rank's part
+// of the domain-sharded DDRGF with the packet all-gather and the halo exchange inside
+// the library. One process driving several GPUs: bbsi_cuda_ddrgf_multi_z /
+// bbsi_cuda_dyson_rgf_multi_z (ncclCommInitAll, one host thread per GPU).
+int bbsi_cuda_nccl_available(void) {
+  std::string err;
+  if (nccl_ready(&err)) return 1;
+  fail(BBSI_CUDA_ERROR, err);
+  return 0;
+}
+
+int bbsi_cuda_nccl_unique_id(void* out128) {
+  std::string err;
+  if (nccl_unique_id(out128, &err)) return fail(BBSI_CUDA_ERROR, err);
+  return BBSI_OK;
+}
+
+int bbsi_cuda_nccl_comm_init(const void* id128, int nranks, int rank, void** comm) {
+  if (nranks < 1 || rank < 0 || rank >= nranks || !comm) return fail(BBSI_INVALID_ARGUMENT, "bad NCCL rank / size");
+  if (int rc = device_ok()) return rc;
+  std::string err;
+  if (nccl_comm_init_rank(id128, nranks, rank, comm, &err)) return fail(BBSI_CUDA_ERROR, err);
+  return BBSI_OK;
+}
+
+void bbsi_cuda_nccl_comm_destroy(void* comm) { nccl_comm_destroy(comm); }
+
+int bbsi_cuda_ddrgf_rank_layers(int l, int s2, int nranks, int rank, int* t0, int* t1, int* L0, int* L1) {
+  if (s2 < 1 || l < 1 + s2) return fail(BBSI_INVALID_ARGUMENT, "interleave_permutation: too few layers to split");
+  const int T = ddrgf_num_tasks(l, s2);
+  if (nranks < 1 || nranks > T || rank < 0 || rank >= nranks)
+    return fail(BBSI_INVALID_ARGUMENT, "ddrgf: " + std::to_string(nranks) + " ranks for " + std::to_string(T) +
+                                           " domains");
+  const auto r = ddrgf_rank_ranges(T, nranks)[rank];
+  // tasks t = [t*(s2+1), ...): first(t) = t*(s2+1); sep(t) = min(first + s2, l - 1)
+  auto first = [&](int t) { return t * (s2 + 1); };
+  auto sep = [&](int t) { return std::min(first(t) + s2, l - 1); };
+  if (t0) *t0 = r.first;
+  if (t1) *t1 = r.second;
+  if (L0) *L0 = first(r.first);
+  if (L1) *L1 = sep(r.second - 1) + 1;
+  return BBSI_OK;
+}
+
+int bbsi_cuda_ddrgf_rank_dev(void* comm, int l, int bs, int s2, const double* dA_loc, double* dG_loc, int* fail_layer,
+                             void* stream) {
+  if (fail_layer) *fail_layer = -1;
+  int one = s2;
+  if (int rc = validate_ddrgf(l, 1, bs, nullptr, &one, 1, 1, 1)) return rc;
+  if (bs % 64) return fail(BBSI_INVALID_ARGUMENT, "resident API requires bs % 64 == 0");
+  if (int rc = device_ok()) return rc;
+  std::string err;
+  int nr = 1, rk = 0;
+  if (nccl_comm_shape(comm, &nr, &rk, &err)) return fail(BBSI_CUDA_ERROR, err);
+  int t0 = 0, t1 = 0;
+  if (int rc = bbsi_cuda_ddrgf_rank_layers(l, s2, nr, rk, &t0, &t1, nullptr, nullptr)) return rc;
+  const size_t sb = ddrgf_scratch_bytes(l, bs, s2);
+  void* scr = arena_get(9, sb);
+  if (!scr) return fail(BBSI_OUT_OF_MEMORY, "ddrgf workspace allocation failed");
+  DdrgfExchange x = nccl_ddrgf_exchange(comm, l, bs, s2, &err);
+  int fl = -1;
+  cudaStream_t s = static_cast<cudaStream_t>(stream);
+  cudaError_t e = ddrgf_rank(reinterpret_cast<const double2*>(dA_loc), reinterpret_cast<double2*>(dG_loc), l, bs,
+                             nullptr, s2, t0, t1, ddrgf_gamma0(), x, scr, sb, &fl, s);
+  if (e != cudaSuccess) return err.empty() ? cuda_fail(e, "ddrgf rank") : fail(BBSI_CUDA_ERROR, err);
+  CK(cudaStreamSynchronize(s));
+  if (fl >= 0) {
+    if (fail_layer) *fail_layer = fl;
+    return fail(BBSI_SINGULAR, "singular pivot at layer " + std::to_string(fl));
+  }
+  return BBSI_OK;
+}
+
+// Runs f(rank, device) on one host thread per GPU; each thread releases its workspaces
+// before it exits. Returns the first non-zero code (by rank) and its message.
+template <class F>
+static int on_gpus(int ngpu, const int* devices, F&& f) {
+  std::vector<int> rc(ngpu, BBSI_OK);
+  std::vector<std::string> msg(ngpu);
+  std::vector<std::thread> th;
+  for (int r = 0; r < ngpu; ++r)
+    th.emplace_back([&, r] {
+      const int dev = devices ? devices[r] : r;
+      if (cudaSetDevice(dev) != cudaSuccess) {
+        cudaGetLastError();
+        rc[r] = BBSI_CUDA_ERROR;
+        msg[r] = "cudaSetDevice(" + std::to_string(dev) + ") failed";
+        return;
+      }
+      rc[r] = f(r, dev);
+      if (rc[r]) msg[r] = g_err;
+      thread_resources_release();
+    });
+  for (auto& t : th) t.join();
+  for (int r = 0; r < ngpu; ++r)
+    if (rc[r]) return fail(rc[r], "rank " + std::to_string(r) + ": " + msg[r]);
+  return BBSI_OK;
+}
+
+static int check_devices(int ngpu, const int* devices) {
+  int n = 0;
+  if (cudaGetDeviceCount(&n) != cudaSuccess) {
+    cudaGetLastError();
+    n = 0;
+  }
+  if (ngpu < 1) return fail(BBSI_INVALID_ARGUMENT, "ngpu must be >= 1");
+  for (int r = 0; r < ngpu; ++r) {
+    const int d = devices ? devices[r] : r;
+    if (d < 0 || d >= n) return fail(BBSI_INVALID_ARGUMENT, "device " + std::to_string(d) + " not visible");
+  }
+  return BBSI_OK;
+}
+
+int bbsi_cuda_ddrgf_multi_z(int l, int w, int bs, const int* sizes, const double* A, const int* s2_levels,
+                            int n_levels, int n_threads, int terminal_threads, int ngpu, const int* devices, double* G,
+                            long long* counters, int* fail_layer) {
+  if (fail_layer) *fail_layer = -1;
+  if (int rc = validate_ddrgf(l, w, bs, sizes, s2_levels, n_levels, n_threads, terminal_threads)) return rc;
+  if (int rc = device_ok()) return rc;
+  if (int rc = check_devices(ngpu, devices)) return rc;
+  const int s2 = s2_levels[0];
+  if (ngpu > ddrgf_num_tasks(l, s2))
+    return fail(BBSI_INVALID_ARGUMENT, "ddrgf: more GPUs than domains in the plan");
+  HostBand h = make_host(l, w, bs, sizes, A);
+  const int bp = pad64(h.bs);
+  std::vector<double2> staging;
+  pad_band(h, bp, staging);
+  const long long row = 3LL * bp * bp;  // complex entries per band row
+  std::vector<void*> comms(ngpu, nullptr);
+  std::vector<int> devs(ngpu);
+  for (int r = 0; r < ngpu; ++r) devs[r] = devices ? devices[r] : r;
+  std::string err;
+  if (ngpu > 1 && nccl_comm_init_all(ngpu, devs.data(), comms, &err)) return fail(BBSI_CUDA_ERROR, err);
+  std::vector<int> fl(ngpu, -1);
+  int rc = on_gpus(ngpu, devs.data(), [&](int r, int) -> int {
+    int t0 = 0, t1 = 0, L0 = 0, L1 = 0;
+    if (int q = bbsi_cuda_ddrgf_rank_layers(l, s2, ngpu, r, &t0, &t1, &L0, &L1)) return q;
+    const size_t bytes = size_t(L1 - L0) * row * sizeof(double2);
+    double2* dA = static_cast<double2*>(arena_get(0, bytes));
+    double2* dG = static_cast<double2*>(arena_get(10, bytes));
+    if (!dA || !dG) return fail(BBSI_OUT_OF_MEMORY, "band allocation failed");
+    cudaStream_t s = thread_stream(0);
+    CK(cudaMemcpyAsync(dA, staging.data() + size_t(L0) * row, bytes, cudaMemcpyHostToDevice, s));
+    const size_t sb = ddrgf_scratch_bytes(l, bp, s2);
+    void* scr = arena_get(9, sb);
+    if (!scr) return fail(BBSI_OUT_OF_MEMORY, "ddrgf workspace allocation failed");
+    std::string xerr;
+    DdrgfExchange x;
+    if (ngpu > 1) {
+      x = nccl_ddrgf_exchange(comms[r], l, bp, s2, &xerr);
+    } else {
+      x.packets = [](double2*, int, int, int f, int* any, cudaStream_t) {
+        *any = f;
+        return cudaSuccess;
+      };
+      x.halo = [](const double2*, double2*, int f, int* any, cudaStream_t) {
+        *any = f;
+        return cudaSuccess;
+      };
+    }
+    cudaError_t e = ddrgf_rank(dA, dG, l, bp, h.sz.data(), s2, t0, t1, ddrgf_gamma0(), x, scr, sb, &fl[r], s);
+    if (e != cudaSuccess) return xerr.empty() ? cuda_fail(e, "ddrgf rank") : fail(BBSI_CUDA_ERROR, xerr);
+    if (fl[r] >= 0) return BBSI_OK;
+    // rows [L0, L1) of G: this rank's chains (written once, disjoint across ranks)
+    CK(cudaMemcpyAsync(staging.data() + size_t(L0) * row, dG, bytes, cudaMemcpyDeviceToHost, s));
+    CK(cudaStreamSynchronize(s));
+    return BBSI_OK;
+  });
+  for (void* c : comms) nccl_comm_destroy(c);
+  if (rc) return rc;
+  for (int r = 0; r < ngpu; ++r)
+    if (fl[r] >= 0) {
+      if (fail_layer) *fail_layer = fl[r];
+      return fail(BBSI_SINGULAR, "singular pivot at layer " + std::to_string(fl[r]));
+    }
+  unpad_band(staging, bp, h, reinterpret_cast<double2*>(G));
+  if (counters) ddrgf_reference_counters(l, s2_levels, n_levels, counters);
+  return BBSI_OK;
+}
+
+int bbsi_cuda_dyson_rgf_multi_z(int l, int w, int bs, int n_energy, const double* H, const double* z,
+                                const double* sigma, double* G, int* fail_layers, int chunk, int ngpu,
+                                const int* devices) {
+  if (int rc = device_ok()) return rc;
+  if (int rc = check_devices(ngpu, devices)) return rc;
+  if (n_energy < ngpu) return fail(BBSI_INVALID_ARGUMENT, "fewer energies than GPUs");
+  const size_t band = size_t(l) * (2 * w + 1) * bs * bs;
+  std::vector<int> devs(ngpu);
+  for (int r = 0; r < ngpu; ++r) devs[r] = devices ? devices[r] : r;
+  // contiguous energy shards, no collective
+  return on_gpus(ngpu, devs.data(), [&](int r, int) -> int {
+    const int e0 = int((long long)r * n_energy / ngpu), e1 = int((long long)(r + 1) * n_energy / ngpu);
+    return bbsi_cuda_dyson_rgf_z(l, w, bs, e1 - e0, H, z + 2 * e0, sigma, G + 2 * size_t(e0) * band,
+                                 fail_layers ? fail_layers + e0 : nullptr, chunk);
+  });
+}

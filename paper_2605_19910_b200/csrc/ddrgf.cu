@@ -26,6 +26,7 @@
 // All chains live in the output band itself (domain i + separator i occupy a
 // contiguous run of slots with a uniform stride), so no extra band buffers exist.
 #include <algorithm>
+#include <cstdlib>
 #include <mutex>
 #include <vector>
 
@@ -161,9 +162,10 @@ cudaError_t zmm(int b, int batch, double2 alpha, ZOp A, ZOp B, double beta, ZOp 
 // per-task interface packet of PK b x b blocks; only packets cross ranks.
 //   packet[t] = { a, b, c, e (fake-lead corners), A[s,s], A[s,l], A[l,s], A[s,s+1], A[x0,x0-1] }
 //   phase-2 output[t] = { Sigma^L on the chain's first block, Sigma^R on its separator,
-//                         Y_t (right-connected G at x0: couplings), G[s,s] }
+//                         Y_t = right-connected G at the chain's first layer x0,
+//                         gL_t = left-connected G at separator t }
 enum { PA, PB, PC, PE, PASS, PASL, PALS, PASN, PAX0, PK };
-enum { OSL, OSR, OY, OGSS, NOUT };
+enum { OSL, OSR, OY, OGL, NOUT };
 
 namespace {
 
@@ -176,9 +178,9 @@ struct Local {
   double2* gslot(int a, int off) const { return G + ((long long)(a - L0) * 3 + off + 1) * bb; }
 };
 
-// RGF sweeps over the chains of tasks [t, t+nt) (same length len), in place in G.
-// two_ended: the chains' G is all that is needed (phase 3), so the two-ended sweep
-// may run; phase 1 reads the right-connected multipliers afterwards and may not.
+// RGF sweeps over the chains of tasks [t, t+nt) (same length len), in place in G. The
+// two-ended sweep is used in both phases: phase 1 reads its multipliers in the
+// two-ended layout (sweep_is_two_ended), phase 3 only needs the chains' G.
 cudaError_t chain_sweeps(const Local& X, const Part& P, int s2, int t, int nt, int len, int b, const int* n_true,
                          SweepWork& W, int* fail_layer, cudaStream_t s, bool two_ended = false) {
   W = SweepWork{};
@@ -222,13 +224,63 @@ cudaError_t for_task_runs(const Part& P, int s2, int t0, int t1, F&& f) {
   return cudaSuccess;
 }
 
+// max |z| over each of nblk b x b blocks at base + off[k] (one CTA per block)
+__global__ void block_maxabs_kernel(const double2* base, const long long* off, long long n2, double* out) {
+  const double2* m = base + off[blockIdx.x];
+  double v = 0.0;
+  for (long long i = threadIdx.x; i < n2; i += blockDim.x) v = fmax(v, hypot(m[i].x, m[i].y));
+  for (int o = 16; o; o >>= 1) v = fmax(v, __shfl_xor_sync(0xffffffffu, v, o));
+  __shared__ double red[32];
+  if ((threadIdx.x & 31) == 0) red[threadIdx.x >> 5] = v;
+  __syncthreads();
+  if (threadIdx.x < 32) {
+    v = threadIdx.x < (blockDim.x >> 5) ? red[threadIdx.x] : 0.0;
+    for (int o = 16; o; o >>= 1) v = fmax(v, __shfl_xor_sync(0xffffffffu, v, o));
+    if (threadIdx.x == 0) out[blockIdx.x] = v;
+  }
+}
+
+// Fake-lead strength per task: gamma0 * max|A[s_t, s_t]| (the separator block, which
+// both phase 1 (locally) and phase 2 (from the packet) can see), so the fake leads
+// scale with the matrix and DDRGF stays scale-invariant like the reference.
+cudaError_t task_gammas(const double2* base, const std::vector<long long>& offs, int b, double gamma0,
+                        std::vector<double>& out, cudaStream_t s) {
+  const int n = int(offs.size());
+  out.assign(n, gamma0);
+  if (n == 0) return cudaSuccess;
+  char* buf = static_cast<char*>(arena_get(18, size_t(n) * (sizeof(long long) + sizeof(double)) + 256));
+  if (!buf) return cudaErrorMemoryAllocation;
+  long long* doff = reinterpret_cast<long long*>(buf);
+  double* dmx = reinterpret_cast<double*>(buf + ((size_t(n) * sizeof(long long) + 255) & ~size_t(255)));
+  cudaError_t e;
+  if ((e = cudaMemcpyAsync(doff, offs.data(), sizeof(long long) * n, cudaMemcpyHostToDevice, s))) return e;
+  {
+    ProfScope prof(s, PROF_BAND, 0.0, 16.0 * b * b * n);
+    block_maxabs_kernel<<<n, 256, 0, s>>>(base, doff, (long long)b * b, dmx);
+    if ((e = cudaGetLastError())) return e;
+  }
+  std::vector<double> mx(n);
+  if ((e = cudaMemcpyAsync(mx.data(), dmx, sizeof(double) * n, cudaMemcpyDeviceToHost, s))) return e;
+  if ((e = cudaStreamSynchronize(s))) return e;
+  for (int k = 0; k < n; ++k) out[k] = gamma0 * (mx[k] > 0.0 ? mx[k] : 1.0);
+  return cudaSuccess;
+}
+
 }  // namespace
+
+double ddrgf_gamma0() {
+  if (const char* e = getenv("BBSI_DDRGF_GAMMA")) {
+    const double v = atof(e);
+    if (v > 0.0) return v;
+  }
+  return 1.0;
+}
 
 size_t ddrgf_packet_bytes(int ntask, int b) { return size_t(ntask) * PK * b * b * sizeof(double2); }
 size_t ddrgf_phase2_out_bytes(int ntask, int b) { return size_t(ntask) * NOUT * b * b * sizeof(double2); }
 
 // Phase 1: fake-lead corners of the local domains + interface A blocks -> packet.
-cudaError_t ddrgf_phase1(const double2* A, double2* G, int l, int b, const int* n_true, int s2, double gamma, int t0,
+cudaError_t ddrgf_phase1(const double2* A, double2* G, int l, int b, const int* n_true, int s2, double gamma0, int t0,
                          int t1, double2* packet, int* fail_layer, cudaStream_t s) {
   *fail_layer = -1;
   const Part P = partition(l, s2);
@@ -238,10 +290,14 @@ cudaError_t ddrgf_phase1(const double2* A, double2* G, int l, int b, const int* 
   const int L1 = P.sep[t1 - 1] + 1;
   const size_t band_b = sizeof(double2) * size_t(L1 - X.L0) * 3 * bb;
   cudaError_t e;
+  std::vector<long long> offs;
+  for (int t = t0; t < t1; ++t) offs.push_back(X.aslot(P.sep[t], 0) - A);
+  std::vector<double> gam;
+  if ((e = task_gammas(A, offs, b, gamma0, gam, s))) return e;
   if ((e = cudaMemcpyAsync(G, A, band_b, cudaMemcpyDeviceToDevice, s))) return e;
-  const double2 ig = make_double2(0.0, gamma);  // -Sigma0 = +i*gamma
   for (int t = t0; t < t1; ++t) {
     if (P.count[t] == 0) continue;
+    const double2 ig = make_double2(0.0, gam[t - t0]);  // -Sigma0 = +i*gamma_t
     if ((e = diag_add(X.gslot(P.first[t], 0), 0, b, 1, ig, s))) return e;
     if ((e = diag_add(X.gslot(P.first[t] + P.count[t] - 1, 0), 0, b, 1, ig, s))) return e;
   }
@@ -377,18 +433,14 @@ cudaError_t ddrgf_phase1(const double2* A, double2* G, int l, int b, const int* 
 // Phase 2 (redundant on every rank): left-/right-connected sweeps over all T
 // separators from the gathered packets. The right-connected recursion does not depend
 // on the left sweep, so it runs on a side stream concurrently with it (each step is a
-// chain of b x b inversions, latency-bound at batch 1); the separator G[s,s] =
-// (A[s,s] - Sigma^R - Sigma^L_sep)^{-1}, the only quantity that needs both, is then one
-// inversion launch over all T separators.
+// chain of b x b inversions, latency-bound at batch 1).
 namespace {
 struct SideStream {
   cudaStream_t s = nullptr;
   cudaEvent_t fork = nullptr, join = nullptr;
 };
 SideStream& side_stream() {
-  static std::mutex mu;
-  static std::vector<SideStream> per_dev;
-  std::lock_guard<std::mutex> lk(mu);
+  thread_local std::vector<SideStream> per_dev;  // per host thread: concurrent callers do not share it
   int dev = 0;
   cudaGetDevice(&dev);
   if (int(per_dev.size()) <= dev) per_dev.resize(dev + 1);
@@ -402,7 +454,7 @@ SideStream& side_stream() {
 }
 }  // namespace
 
-cudaError_t ddrgf_phase2(const double2* packets, int l, int b, const int* n_true, int s2, double gamma, double2* out,
+cudaError_t ddrgf_phase2(const double2* packets, int l, int b, const int* n_true, int s2, double gamma0, double2* out,
                          int* fail_layer, cudaStream_t s) {
   *fail_layer = -1;
   const Part P = partition(l, s2);
@@ -410,24 +462,23 @@ cudaError_t ddrgf_phase2(const double2* packets, int l, int b, const int* n_true
   const long long bb = (long long)b * b;
   auto pk = [&](int t, int k) { return packets + ((size_t)t * PK + k) * bb; };
   auto o = [&](int t, int k) { return out + ((size_t)t * NOUT + k) * bb; };
-  const double2 ig = make_double2(0.0, gamma);
   const double2 m1 = make_double2(-1.0, 0.0);
   cudaError_t e;
-  // scratch: gL, gLdom, SigmaLsep per task, then 8 temporaries per stream (+1 for gR)
+  std::vector<long long> offs;
+  for (int t = 0; t < T; ++t) offs.push_back(pk(t, PASS) - packets);
+  std::vector<double> gam;
+  if ((e = task_gammas(packets, offs, b, gamma0, gam, s))) return e;
+  // scratch: 8 temporaries per stream
   constexpr int NT = 8;
-  double2* scr = static_cast<double2*>(arena_get(13, (size_t(3) * T + 2 * NT + 1) * bb * sizeof(double2)));
-  const int max_inv = 8 * T + 4;
+  double2* scr = static_cast<double2*>(arena_get(13, size_t(2 * NT) * bb * sizeof(double2)));
+  const int max_inv = 6 * T + 4;
   void* inv_scr = arena_get(7, zinv_scratch_bytes(b, 1) + 256);
-  void* inv_scr2 = arena_get(17, zinv_scratch_bytes(b, T) + 256);  // side stream; then the batched G[s,s]
-  int* st = static_cast<int*>(arena_get(8, sizeof(int) * size_t(max_inv + T)));
+  void* inv_scr2 = arena_get(17, zinv_scratch_bytes(b, 1) + 256);
+  int* st = static_cast<int*>(arena_get(8, sizeof(int) * size_t(max_inv)));
   if (!scr || !inv_scr || !inv_scr2 || !st) return cudaErrorMemoryAllocation;
   SideStream& side = side_stream();
-  auto gL = [&](int t) { return scr + (size_t)t * bb; };
-  auto gLD = [&](int t) { return scr + ((size_t)T + t) * bb; };
-  auto SLs = [&](int t) { return scr + ((size_t)2 * T + t) * bb; };
-  double2* gR = scr + ((size_t)3 * T + 2 * NT) * bb;
   std::vector<int> st_layer;
-  // the block operations of one stream: temporaries Tm(0..NT-1) of that stream
+  st_layer.reserve(max_inv);
   struct Ops {
     cudaStream_t s;
     double2* tm0;
@@ -435,8 +486,8 @@ cudaError_t ddrgf_phase2(const double2* packets, int l, int b, const int* n_true
     long long bb;
     double2* Tm(int i) const { return tm0 + (size_t)i * bb; }
   };
-  const Ops L{s, scr + (size_t)3 * T * bb, inv_scr, bb};
-  const Ops R{side.s, scr + ((size_t)3 * T + NT) * bb, inv_scr2, bb};
+  const Ops L{s, scr, inv_scr, bb};
+  const Ops R{side.s, scr + (size_t)NT * bb, inv_scr2, bb};
   auto inv = [&](const Ops& q, double2* m, int layer) -> cudaError_t {
     if (int(st_layer.size()) >= max_inv) return cudaErrorInvalidValue;
     int* slot = st + st_layer.size();
@@ -457,7 +508,7 @@ cudaError_t ddrgf_phase2(const double2* packets, int l, int b, const int* n_true
     return e2 ? e2 : mm(b, 1, alpha, blk(q.Tm(7), b), blk(z, b), 0.0, blk(d, b), q.s);
   };
   // out = x + i*gamma x (I - i*gamma x)^{-1} x   (removes the fake lead at the block of x)
-  auto remove_fake = [&](const Ops& q, double2* o_, const double2* x, int layer) -> cudaError_t {
+  auto remove_fake = [&](const Ops& q, double2* o_, const double2* x, double gamma, int layer) -> cudaError_t {
     cudaError_t e2;
     if ((e2 = ident(q, q.Tm(2)))) return e2;
     if ((e2 = axpy(q.Tm(2), x, bb, make_double2(0.0, -gamma), q.s))) return e2;
@@ -467,7 +518,7 @@ cudaError_t ddrgf_phase2(const double2* packets, int l, int b, const int* n_true
     return mmz(b, make_double2(0.0, gamma), blk(x, b), blk(q.Tm(3), b), 1.0, blk(o_, b), q.s);
   };
   if ((e = cudaEventRecord(side.fork, s)) || (e = cudaStreamWaitEvent(side.s, side.fork, 0))) return e;
-  // ---- right-connected recursion (side stream): Sigma^R, Y_t, and pre_t = A[s,s] - Sigma^R in OGSS
+  // ---- right-connected recursion (side stream): Sigma^R and Y_t
   for (int t = T - 1; t >= 0; --t) {
     const int sp = P.sep[t], cnt = P.count[t];
     if (t < T - 1) {
@@ -475,13 +526,14 @@ cudaError_t ddrgf_phase2(const double2* packets, int l, int b, const int* n_true
     } else if ((e = cudaMemsetAsync(o(t, OSR), 0, bb * sizeof(double2), R.s))) {
       return e;
     }
-    // pre = A[s,s] - Sigma^R ; gR = pre^{-1}
+    // gR = (A[s,s] - Sigma^R)^{-1}: the right-connected G at the separator
+    double2* gR = R.Tm(0);
     if ((e = copy(R, gR, pk(t, PASS)))) return e;
     if ((e = axpy(gR, o(t, OSR), bb, m1, R.s))) return e;
-    if ((e = copy(R, o(t, OGSS), gR))) return e;
     if ((e = inv(R, gR, sp))) return e;
     if (cnt > 0) {
       const int last = P.first[t] + cnt - 1;
+      const double2 ig = make_double2(0.0, gam[t]);
       double2* Dl = R.Tm(1);
       if ((e = mm3(R, Dl, 1.0, pk(t, PALS), gR, pk(t, PASL)))) return e;
       if ((e = diag_add(Dl, 0, b, 1, ig, R.s))) return e;
@@ -492,20 +544,22 @@ cudaError_t ddrgf_phase2(const double2* packets, int l, int b, const int* n_true
       if ((e = mm(b, 1, 1.0, blk(R.Tm(3), b), blk(pk(t, PC), b), 0.0, blk(R.Tm(4), b), R.s))) return e;
       if ((e = copy(R, R.Tm(5), pk(t, PA)))) return e;
       if ((e = mm(b, 1, 1.0, blk(pk(t, PB), b), blk(R.Tm(4), b), 1.0, blk(R.Tm(5), b), R.s))) return e;
-      if ((e = remove_fake(R, o(t, OY), R.Tm(5), P.first[t]))) return e;
+      if ((e = remove_fake(R, o(t, OY), R.Tm(5), gam[t], P.first[t]))) return e;
     } else if ((e = copy(R, o(t, OY), gR))) {
       return e;
     }
   }
   if ((e = cudaEventRecord(side.join, R.s))) return e;
-  // ---- left sweep (main stream)
+  // ---- left-connected sweep (main stream): Sigma^L and gL_t
   for (int t = 0; t < T; ++t) {
     const int f = P.first[t], cnt = P.count[t], sp = P.sep[t];
+    double2* SL = L.Tm(6);  // Sigma of everything left of separator t, seen from it
     if (cnt > 0) {
       // Sigma^L on the first block (from separator t-1); Df = Sigma^L - Sigma0
+      const double2 ig = make_double2(0.0, gam[t]);
       double2* Df = L.Tm(1);
       if (t > 0) {
-        if ((e = mm3(L, o(t, OSL), 1.0, pk(t, PAX0), gL(t - 1), pk(t - 1, PASN)))) return e;
+        if ((e = mm3(L, o(t, OSL), 1.0, pk(t, PAX0), o(t - 1, OGL), pk(t - 1, PASN)))) return e;
       } else if ((e = cudaMemsetAsync(o(t, OSL), 0, bb * sizeof(double2), s))) {
         return e;
       }
@@ -519,33 +573,20 @@ cudaError_t ddrgf_phase2(const double2* packets, int l, int b, const int* n_true
       if ((e = mm(b, 1, 1.0, blk(L.Tm(3), b), blk(pk(t, PB), b), 0.0, blk(L.Tm(4), b), s))) return e;
       if ((e = copy(L, L.Tm(5), pk(t, PE)))) return e;
       if ((e = mm(b, 1, 1.0, blk(pk(t, PC), b), blk(L.Tm(4), b), 1.0, blk(L.Tm(5), b), s))) return e;
-      if ((e = remove_fake(L, gLD(t), L.Tm(5), f + cnt - 1))) return e;
-      if ((e = mm3(L, SLs(t), 1.0, pk(t, PASL), gLD(t), pk(t, PALS)))) return e;
+      double2* gld = L.Tm(0);
+      if ((e = remove_fake(L, gld, L.Tm(5), gam[t], f + cnt - 1))) return e;
+      if ((e = mm3(L, SL, 1.0, pk(t, PASL), gld, pk(t, PALS)))) return e;
     } else {
       if (t == 0) return cudaErrorInvalidValue;  // task 0 always has interior layers
-      if ((e = mm3(L, SLs(t), 1.0, pk(t, PASL), gL(t - 1), pk(t - 1, PASN)))) return e;
-      if ((e = copy(L, o(t, OSL), SLs(t)))) return e;  // the chain's only block is the separator
+      if ((e = mm3(L, SL, 1.0, pk(t, PASL), o(t - 1, OGL), pk(t - 1, PASN)))) return e;
+      if ((e = copy(L, o(t, OSL), SL))) return e;  // the chain's only block is the separator
     }
-    if ((e = copy(L, gL(t), pk(t, PASS)))) return e;
-    if ((e = axpy(gL(t), SLs(t), bb, m1, s))) return e;
-    if ((e = inv(L, gL(t), sp))) return e;
+    // gL_t = (A[s,s] - Sigma_left)^{-1}
+    if ((e = copy(L, o(t, OGL), pk(t, PASS)))) return e;
+    if ((e = axpy(o(t, OGL), SL, bb, m1, s))) return e;
+    if ((e = inv(L, o(t, OGL), sp))) return e;
   }
-  // ---- join; G[s,s] = (pre - Sigma^L_sep)^{-1} for every separator in one launch
   if ((e = cudaStreamWaitEvent(s, side.join, 0))) return e;
-  bool uniform = true;
-  for (int t = 0; t < T; ++t) {
-    if ((e = axpy(o(t, OGSS), SLs(t), bb, m1, s))) return e;
-    uniform = uniform && (!n_true || n_true[P.sep[t]] == n_true[P.sep[0]]);
-  }
-  if (uniform) {
-    int* slot = st + st_layer.size();
-    for (int t = 0; t < T; ++t) st_layer.push_back(P.sep[t]);
-    if ((e = zinv_batched(o(0, OGSS), b, NOUT * bb, b, n_true ? n_true[P.sep[0]] : b, T, inv_scr2, slot, s)))
-      return e;
-  } else {
-    for (int t = 0; t < T; ++t)
-      if ((e = inv(L, o(t, OGSS), P.sep[t]))) return e;
-  }
   std::vector<int> sh(st_layer.size());
   if ((e = cudaMemcpyAsync(sh.data(), st, sh.size() * sizeof(int), cudaMemcpyDeviceToHost, s))) return e;
   if ((e = cudaStreamSynchronize(s))) return e;
@@ -557,7 +598,7 @@ cudaError_t ddrgf_phase2(const double2* packets, int l, int b, const int* n_true
   return cudaSuccess;
 }
 
-// Phase 3: re-solve the local chains with the exact boundary self-energies; couplings.
+// Phase 3: re-solve the local chains with the exact boundary self-energies (in place).
 cudaError_t ddrgf_phase3(const double2* A, double2* G, int l, int b, const int* n_true, int s2, int t0, int t1,
                          const double2* out, int* fail_layer, cudaStream_t s) {
   *fail_layer = -1;
@@ -575,47 +616,135 @@ cudaError_t ddrgf_phase3(const double2* A, double2* G, int l, int b, const int* 
     if (t > 0 && (e = axpy(X.gslot(x0, 0), o(t, OSL), bb, m1, s))) return e;
     if (t < T - 1 && (e = axpy(X.gslot(P.sep[t], 0), o(t, OSR), bb, m1, s))) return e;
   }
-  e = for_task_runs(P, s2, t0, t1, [&](int t, int nt, int len) -> cudaError_t {
+  return for_task_runs(P, s2, t0, t1, [&](int t, int nt, int len) -> cudaError_t {
     SweepWork W;
     return chain_sweeps(X, P, s2, t, nt, len + 1, b, n_true, W, fail_layer, s, true);
   });
-  if (e || *fail_layer >= 0) return e;
-  // couplings: G[x0_t, x0_t - 1] = -Y_t A[x0,-1] G_ss(t-1);  G[s_t, s_t + 1] = -G_ss(t) A[s,+1] Y_{t+1}
+}
+
+// The couplings between chains, each made consistent with the chain whose row of A*G
+// it closes: G[x0_t, s_{t-1}] (column s_{t-1}: row s_{t-1} of chain t-1, solved with
+// Sigma^R = A[s,x0] Y_t A[x0,s]) = -Y_t A[x0,s] G[s,s]; G[s_t, x0_{t+1}] (column x0_{t+1}:
+// chain t+1, solved with Sigma^L = A[x0,s] gL_t A[s,x0]) = -gL_t A[s,x0] G[x0,x0]. Both use
+// the neighbour chain's diagonal block from phase 3; at a rank boundary that block comes
+// from the neighbour rank (prev_sep_g = G[s_{t0-1}, s_{t0-1}], next_x0_g = G[x0_{t1},
+// x0_{t1}]; null where there is no neighbour).
+cudaError_t ddrgf_couplings(const double2* A, double2* G, int l, int b, int s2, int t0, int t1, const double2* out,
+                            const double2* prev_sep_g, const double2* next_x0_g, cudaStream_t s) {
+  const Part P = partition(l, s2);
+  const int T = P.T;
+  const long long bb = (long long)b * b;
+  Local X{A, G, P.first[t0], bb};
+  auto o = [&](int t, int k) { return out + ((size_t)t * NOUT + k) * bb; };
+  auto x0_of = [&](int t) { return P.count[t] > 0 ? P.first[t] : P.sep[t]; };
   double2* tmp = static_cast<double2*>(arena_get(14, bb * sizeof(double2)));
   if (!tmp) return cudaErrorMemoryAllocation;
+  cudaError_t e;
   for (int t = t0; t < t1; ++t) {
-    const int x0 = P.count[t] > 0 ? P.first[t] : P.sep[t];
+    const int x0 = x0_of(t);
     if (t > 0) {
+      const double2* gss = t == t0 ? prev_sep_g : X.gslot(P.sep[t - 1], 0);
+      if (!gss) return cudaErrorInvalidValue;
       if ((e = mm(b, 1, 1.0, blk(o(t, OY), b), blk(X.aslot(x0, -1), b), 0.0, blk(tmp, b), s))) return e;
-      if ((e = mm(b, 1, -1.0, blk(tmp, b), blk(o(t - 1, OGSS), b), 0.0, blk(X.gslot(x0, -1), b), s))) return e;
+      if ((e = mm(b, 1, -1.0, blk(tmp, b), blk(gss, b), 0.0, blk(X.gslot(x0, -1), b), s))) return e;
     }
     if (t < T - 1) {
       const int sp = P.sep[t];
-      if ((e = mm(b, 1, 1.0, blk(o(t, OGSS), b), blk(X.aslot(sp, 1), b), 0.0, blk(tmp, b), s))) return e;
-      if ((e = mm(b, 1, -1.0, blk(tmp, b), blk(o(t + 1, OY), b), 0.0, blk(X.gslot(sp, 1), b), s))) return e;
+      const double2* gxx = t == t1 - 1 ? next_x0_g : X.gslot(x0_of(t + 1), 0);
+      if (!gxx) return cudaErrorInvalidValue;
+      if ((e = mm(b, 1, 1.0, blk(o(t, OGL), b), blk(X.aslot(sp, 1), b), 0.0, blk(tmp, b), s))) return e;
+      if ((e = mm(b, 1, -1.0, blk(tmp, b), blk(gxx, b), 0.0, blk(X.gslot(sp, 1), b), s))) return e;
     }
   }
   return cudaSuccess;
 }
 
-cudaError_t ddrgf_device(const double2* A, double2* G, int l, int b, const int* n_true, int s2, double gamma,
-                         void* scratch, size_t scratch_bytes, int* fail_layer, cudaStream_t s) {
+// This rank's two boundary diagonal blocks after phase 3 (the halo its neighbours'
+// couplings need): halo[0] = G[x0_{t0}, x0_{t0}], halo[1] = G[s_{t1-1}, s_{t1-1}].
+cudaError_t ddrgf_halo(const double2* G, int l, int b, int s2, int t0, int t1, double2* halo, cudaStream_t s) {
+  const Part P = partition(l, s2);
+  const long long bb = (long long)b * b;
+  const int L0 = P.first[t0];
+  const int x0 = P.count[t0] > 0 ? P.first[t0] : P.sep[t0];
+  cudaError_t e = cudaMemcpyAsync(halo, G + ((long long)(x0 - L0) * 3 + 1) * bb, bb * sizeof(double2),
+                                  cudaMemcpyDeviceToDevice, s);
+  if (e) return e;
+  return cudaMemcpyAsync(halo + bb, G + ((long long)(P.sep[t1 - 1] - L0) * 3 + 1) * bb, bb * sizeof(double2),
+                         cudaMemcpyDeviceToDevice, s);
+}
+
+std::vector<std::pair<int, int>> ddrgf_rank_ranges(int n_tasks, int nranks) {
+  std::vector<std::pair<int, int>> r;
+  const int base = n_tasks / nranks, extra = n_tasks % nranks;
+  int t = 0;
+  for (int k = 0; k < nranks; ++k) {
+    const int n = base + (k < extra ? 1 : 0);
+    r.emplace_back(t, t + n);
+    t += n;
+  }
+  return r;
+}
+
+// One rank of the domain-sharded DDRGF; `exchange` is the packet all-gather (NCCL across
+// GPUs, identity on one), `halo_exchange` the neighbours' boundary blocks.
+cudaError_t ddrgf_rank(const double2* A_loc, double2* G_loc, int l, int b, const int* n_true, int s2, int t0, int t1,
+                       double gamma0, const DdrgfExchange& x, void* scratch, size_t scratch_bytes, int* fail_layer,
+                       cudaStream_t s) {
+  *fail_layer = -1;
   const Part P = partition(l, s2);
   const int T = P.T;
-  if (scratch_bytes < ddrgf_packet_bytes(T, b) + ddrgf_phase2_out_bytes(T, b)) return cudaErrorMemoryAllocation;
-  double2* packet = static_cast<double2*>(scratch);
-  double2* out = packet + (size_t)T * PK * b * b;
+  const long long bb = (long long)b * b;
+  if (scratch_bytes < ddrgf_packet_bytes(T, b) + ddrgf_phase2_out_bytes(T, b) + 4 * bb * sizeof(double2))
+    return cudaErrorMemoryAllocation;
+  double2* packets = static_cast<double2*>(scratch);          // [T][PK] (own range at t0)
+  double2* out = packets + (size_t)T * PK * bb;                // [T][NOUT]
+  double2* halo = out + (size_t)T * NOUT * bb;                 // [2] own, [2] neighbours' (prev last, next first)
   cudaError_t e;
-  if ((e = ddrgf_phase1(A, G, l, b, n_true, s2, gamma, 0, T, packet, fail_layer, s)) || *fail_layer >= 0) return e;
-  if ((e = ddrgf_phase2(packet, l, b, n_true, s2, gamma, out, fail_layer, s)) || *fail_layer >= 0) return e;
-  return ddrgf_phase3(A, G, l, b, n_true, s2, 0, T, out, fail_layer, s);
+  int fl = -1;
+  e = ddrgf_phase1(A_loc, G_loc, l, b, n_true, s2, gamma0, t0, t1, packets + (size_t)t0 * PK * bb, &fl, s);
+  if (e) return e;
+  int any = fl;
+  if ((e = x.packets(packets, t0, t1, fl, &any, s))) return e;
+  if (any >= 0) {
+    *fail_layer = any;
+    return cudaSuccess;
+  }
+  if ((e = ddrgf_phase2(packets, l, b, n_true, s2, gamma0, out, &fl, s)) || fl >= 0) {
+    *fail_layer = fl;
+    return e;
+  }
+  if ((e = ddrgf_phase3(A_loc, G_loc, l, b, n_true, s2, t0, t1, out, &fl, s))) return e;
+  if ((e = ddrgf_halo(G_loc, l, b, s2, t0, t1, halo, s))) return e;
+  any = fl;
+  if ((e = x.halo(halo, halo + 2 * bb, fl, &any, s))) return e;  // also agrees on phase-3 failures
+  if (any >= 0) {
+    *fail_layer = any;
+    return cudaSuccess;
+  }
+  return ddrgf_couplings(A_loc, G_loc, l, b, s2, t0, t1, out, t0 > 0 ? halo + 2 * bb : nullptr,
+                         t1 < T ? halo + 3 * bb : nullptr, s);
+}
+
+cudaError_t ddrgf_device(const double2* A, double2* G, int l, int b, const int* n_true, int s2, double gamma0,
+                         void* scratch, size_t scratch_bytes, int* fail_layer, cudaStream_t s) {
+  DdrgfExchange local;  // one rank: nothing to exchange
+  local.packets = [](double2*, int, int, int fl, int* any, cudaStream_t) {
+    *any = fl;
+    return cudaSuccess;
+  };
+  local.halo = [](const double2*, double2*, int fl, int* any, cudaStream_t) {
+    *any = fl;
+    return cudaSuccess;
+  };
+  const int T = partition(l, s2).T;
+  return ddrgf_rank(A, G, l, b, n_true, s2, 0, T, gamma0, local, scratch, scratch_bytes, fail_layer, s);
 }
 
 int ddrgf_num_tasks(int l, int s2) { return partition(l, s2).T; }
 
 size_t ddrgf_scratch_bytes(int l, int b, int s2) {
   const int T = partition(l, s2).T;
-  return ddrgf_packet_bytes(T, b) + ddrgf_phase2_out_bytes(T, b) + 4096;
+  return ddrgf_packet_bytes(T, b) + ddrgf_phase2_out_bytes(T, b) + 4 * size_t(b) * b * sizeof(double2) + 4096;
 }
 
 // Logical kernel counts of the reference ddrgf for this plan (walks the same

@@ -7,6 +7,7 @@
 #include <stdint.h>
 
 #include <string>
+#include <utility>
 #include <vector>
 
 #include "zcommon.cuh"
@@ -114,20 +115,49 @@ ZOp zblk(const double2* p, int b, long long bstride = 0);
 cudaError_t zmm(int b, int batch, double2 alpha, ZOp A, ZOp B, double beta, ZOp C, cudaStream_t s);
 
 // Stabilised DDRGF (ddrgf.cu) on one device band A (w = 1, uniform bs) -> G.
-cudaError_t ddrgf_device(const double2* A, double2* G, int l, int b, const int* n_true, int s2, double gamma,
+// gamma0: fake-lead strength relative to max|A[s,s]| of each task (BBSI_DDRGF_GAMMA).
+cudaError_t ddrgf_device(const double2* A, double2* G, int l, int b, const int* n_true, int s2, double gamma0,
                          void* scratch, size_t scratch_bytes, int* fail_layer, cudaStream_t s);
 size_t ddrgf_scratch_bytes(int l, int b, int s2);
+double ddrgf_gamma0();
 // Phases of the same algorithm on a rank-local slice (tasks [t0, t1)); only the
-// per-task interface packets cross ranks (csrc/ddrgf.cu).
+// per-task interface packets (and two halo blocks per rank) cross ranks (csrc/ddrgf.cu).
 int ddrgf_num_tasks(int l, int s2);
 size_t ddrgf_packet_bytes(int ntask, int b);
 size_t ddrgf_phase2_out_bytes(int ntask, int b);
-cudaError_t ddrgf_phase1(const double2* A, double2* G, int l, int b, const int* n_true, int s2, double gamma, int t0,
+cudaError_t ddrgf_phase1(const double2* A, double2* G, int l, int b, const int* n_true, int s2, double gamma0, int t0,
                          int t1, double2* packet, int* fail_layer, cudaStream_t s);
-cudaError_t ddrgf_phase2(const double2* packets, int l, int b, const int* n_true, int s2, double gamma, double2* out,
+cudaError_t ddrgf_phase2(const double2* packets, int l, int b, const int* n_true, int s2, double gamma0, double2* out,
                          int* fail_layer, cudaStream_t s);
 cudaError_t ddrgf_phase3(const double2* A, double2* G, int l, int b, const int* n_true, int s2, int t0, int t1,
                          const double2* out, int* fail_layer, cudaStream_t s);
+cudaError_t ddrgf_halo(const double2* G, int l, int b, int s2, int t0, int t1, double2* halo, cudaStream_t s);
+cudaError_t ddrgf_couplings(const double2* A, double2* G, int l, int b, int s2, int t0, int t1, const double2* out,
+                            const double2* prev_sep_g, const double2* next_x0_g, cudaStream_t s);
+// Balanced contiguous task ranges per rank (distributed.py task_ranges).
+std::vector<std::pair<int, int>> ddrgf_rank_ranges(int n_tasks, int nranks);
+// The two exchanges of a domain-sharded DDRGF (ddrgf_rank):
+//   packets(all, t0, t1, fail, any, s): on entry all[t0..t1) holds this rank's packets;
+//     on return every task's packet (task order) and *any = the first failing layer of
+//     any rank (or -1);
+//   halo(own, nbr, fail, any, s): own = this rank's [2] boundary blocks; nbr[0] = the
+//     previous rank's own[1], nbr[1] = the next rank's own[0]; *any as above.
+struct DdrgfExchange {
+  std::function<cudaError_t(double2*, int, int, int, int*, cudaStream_t)> packets;
+  std::function<cudaError_t(const double2*, double2*, int, int*, cudaStream_t)> halo;
+};
+cudaError_t ddrgf_rank(const double2* A_loc, double2* G_loc, int l, int b, const int* n_true, int s2, int t0, int t1,
+                       double gamma0, const DdrgfExchange& x, void* scratch, size_t scratch_bytes, int* fail_layer,
+                       cudaStream_t s);
+// NCCL (multi.cu, resolved with dlopen at first use).
+bool nccl_ready(std::string* err);
+int nccl_unique_id(void* out, std::string* err);
+int nccl_comm_init_rank(const void* id, int nranks, int rank, void** comm, std::string* err);
+int nccl_comm_init_all(int n, const int* devs, std::vector<void*>& comms, std::string* err);
+void nccl_comm_destroy(void* comm);
+int nccl_comm_shape(void* comm, int* nranks, int* rank, std::string* err);
+DdrgfExchange nccl_ddrgf_exchange(void* comm, int l, int b, int s2, std::string* err);
+
 void ddrgf_reference_counters(long long l, const int* s2_levels, int n_levels, long long out[3]);
 
 // Launch accounting / optional event timing around one kernel launch (prof.cu).
@@ -151,10 +181,20 @@ void prof_enable(bool on);
 int prof_collect(double* out, int ncat);
 double fp64_dmma_peak(double duration_ms, int reps);
 
-// Grow-only device arena per (device, slot) with a mutex; returns nullptr on OOM.
+// cudaFuncAttributeMaxDynamicSharedMemorySize >= bytes for fn on the current device
+// (set once per device and kernel; optionally the max-shared carveout too).
+cudaError_t set_max_dyn_smem(const void* fn, size_t bytes, bool max_carveout = false);
+
+// Grow-only device arena per (host thread, device, slot); returns nullptr on OOM.
 void* arena_get(int slot, size_t bytes);
 // Bytes currently held by the given arena slots on the current device (reusable).
 size_t arena_held(std::initializer_list<int> slots);
+// Frees the calling thread's arenas (every device).
 void arena_release_all();
+// Frees everything the calling thread holds: arenas, side-stream pools, the
+// per-thread streams of the C ABI (worker threads call this before they exit).
+void thread_resources_release();
+// Per-thread streams of the C ABI (non-blocking; created on first use per device).
+cudaStream_t thread_stream(int which);
 
 }  // namespace bbsi_gpu

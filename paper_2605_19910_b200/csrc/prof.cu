@@ -2,6 +2,7 @@
 // kernels (used by bench.py for the roofline of the dominant kernel), plus the
 // FP64 DMMA peak probe that gives the roofline its denominator.
 #include <atomic>
+#include <map>
 #include <mutex>
 #include <vector>
 
@@ -138,6 +139,25 @@ double fp64_dmma_peak(double duration_ms, int reps) {
   cudaEventDestroy(e1);
   cudaFree(d);
   return cudaGetLastError() == cudaSuccess ? best : -1.0;
+}
+
+// Kernel attributes are per device: remembered per (device, kernel) so a process that
+// drives several GPUs sets them on each one (and concurrent callers do not race).
+cudaError_t set_max_dyn_smem(const void* fn, size_t bytes, bool max_carveout) {
+  static std::mutex mu;
+  static std::map<std::pair<int, const void*>, size_t> done;
+  int dev = 0;
+  cudaError_t e = cudaGetDevice(&dev);
+  if (e) return e;
+  std::lock_guard<std::mutex> lk(mu);
+  size_t& have = done[{dev, fn}];
+  if (have >= bytes && have > 0) return cudaSuccess;
+  if ((e = cudaFuncSetAttribute(fn, cudaFuncAttributeMaxDynamicSharedMemorySize, int(bytes)))) return e;
+  if (max_carveout &&
+      (e = cudaFuncSetAttribute(fn, cudaFuncAttributePreferredSharedMemoryCarveout, cudaSharedmemCarveoutMaxShared)))
+    return e;
+  have = bytes;
+  return cudaSuccess;
 }
 
 }  // namespace bbsi_gpu

@@ -503,18 +503,20 @@ cudaError_t rgf_sweeps_two_w(const SweepWork& W, const int* n_true, int* status,
 }
 
 struct StreamPool {
+  int dev = -1;
   std::vector<cudaStream_t> s;
   std::vector<cudaEvent_t> ev;
 };
-std::mutex g_pool_mu;
-std::vector<StreamPool> g_pools;
+// Per host thread (and device): concurrent callers on different threads get their own
+// side streams and events, so their sweeps overlap instead of interleaving on shared ones.
+thread_local std::vector<StreamPool> t_pools;
 
 StreamPool& pool_for(int n) {
-  std::lock_guard<std::mutex> lk(g_pool_mu);
   int dev = 0;
   cudaGetDevice(&dev);
-  if (int(g_pools.size()) <= dev) g_pools.resize(dev + 1);
-  StreamPool& p = g_pools[dev];
+  if (int(t_pools.size()) <= dev) t_pools.resize(dev + 1);
+  StreamPool& p = t_pools[dev];
+  p.dev = dev;
   while (int(p.s.size()) < n) {
     cudaStream_t st;
     cudaStreamCreateWithFlags(&st, cudaStreamNonBlocking);
@@ -587,21 +589,36 @@ cudaError_t collect_failures(const SweepWork& W, std::vector<int>& fail, cudaStr
 }
 
 // ------------------------------------------------------------------ arena
+// Grow-only device workspace, one set of slots per (host thread, device): calls made
+// from different host threads never share scratch, so they may run concurrently (the
+// reference solvers are reentrant).
 namespace {
-std::mutex g_arena_mu;
 struct Buf {
   void* p = nullptr;
   size_t n = 0;
 };
-std::vector<std::vector<Buf>> g_arena;  // [device][slot]
+thread_local std::vector<std::vector<Buf>> t_arena;  // [device][slot]
+thread_local std::vector<std::vector<cudaStream_t>> t_streams;  // [device][which]
 }  // namespace
 
-void* arena_get(int slot, size_t bytes) {
-  std::lock_guard<std::mutex> lk(g_arena_mu);
+cudaStream_t thread_stream(int which) {
   int dev = 0;
   cudaGetDevice(&dev);
-  if (int(g_arena.size()) <= dev) g_arena.resize(dev + 1);
-  auto& v = g_arena[dev];
+  if (int(t_streams.size()) <= dev) t_streams.resize(dev + 1);
+  auto& v = t_streams[dev];
+  while (int(v.size()) <= which) {
+    cudaStream_t st = nullptr;
+    cudaStreamCreateWithFlags(&st, cudaStreamNonBlocking);
+    v.push_back(st);
+  }
+  return v[which];
+}
+
+void* arena_get(int slot, size_t bytes) {
+  int dev = 0;
+  cudaGetDevice(&dev);
+  if (int(t_arena.size()) <= dev) t_arena.resize(dev + 1);
+  auto& v = t_arena[dev];
   if (int(v.size()) <= slot) v.resize(slot + 1);
   Buf& b = v[slot];
   if (b.n >= bytes && b.p) return b.p;
@@ -621,25 +638,47 @@ void* arena_get(int slot, size_t bytes) {
 }
 
 size_t arena_held(std::initializer_list<int> slots) {
-  std::lock_guard<std::mutex> lk(g_arena_mu);
   int dev = 0;
   cudaGetDevice(&dev);
-  if (int(g_arena.size()) <= dev) return 0;
+  if (int(t_arena.size()) <= dev) return 0;
   size_t n = 0;
   for (int sl : slots)
-    if (sl < int(g_arena[dev].size()) && g_arena[dev][sl].p) n += g_arena[dev][sl].n;
+    if (sl < int(t_arena[dev].size()) && t_arena[dev][sl].p) n += t_arena[dev][sl].n;
   return n;
 }
 
 void arena_release_all() {
-  std::lock_guard<std::mutex> lk(g_arena_mu);
   int cur = 0;
   cudaGetDevice(&cur);
-  for (size_t d = 0; d < g_arena.size(); ++d) {
+  for (size_t d = 0; d < t_arena.size(); ++d) {
+    bool any = false;
+    for (auto& b : t_arena[d]) any |= b.p != nullptr;
+    if (!any) continue;
     cudaSetDevice(int(d));
     cudaDeviceSynchronize();
-    for (auto& b : g_arena[d])
+    for (auto& b : t_arena[d])
       if (b.p) cudaFree(b.p), b.p = nullptr, b.n = 0;
+  }
+  cudaSetDevice(cur);
+}
+
+void thread_resources_release() {
+  arena_release_all();
+  int cur = 0;
+  cudaGetDevice(&cur);
+  for (auto& p : t_pools) {
+    if (p.dev < 0) continue;
+    cudaSetDevice(p.dev);
+    for (auto st : p.s) cudaStreamDestroy(st);
+    for (auto e : p.ev) cudaEventDestroy(e);
+    p.s.clear();
+    p.ev.clear();
+  }
+  for (size_t d = 0; d < t_streams.size(); ++d) {
+    if (t_streams[d].empty()) continue;
+    cudaSetDevice(int(d));
+    for (auto st : t_streams[d]) cudaStreamDestroy(st);
+    t_streams[d].clear();
   }
   cudaSetDevice(cur);
 }

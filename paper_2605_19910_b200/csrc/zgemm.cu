@@ -337,17 +337,7 @@ int gemm_minb() {
 
 template <bool PLAIN, int MINB, bool AMAX = false, bool CFORM = false>
 cudaError_t gemm_attrs() {
-  static cudaError_t e = [] {
-    cudaError_t r = cudaFuncSetAttribute(zgemm_grouped_kernel<PLAIN, MINB, AMAX, CFORM>,
-                                         cudaFuncAttributeMaxDynamicSharedMemorySize,
-                                         SMEM_BYTES);
-    if (r == cudaSuccess)
-      r = cudaFuncSetAttribute(zgemm_grouped_kernel<PLAIN, MINB, AMAX, CFORM>,
-                               cudaFuncAttributePreferredSharedMemoryCarveout,
-                               cudaSharedmemCarveoutMaxShared);
-    return r;
-  }();
-  return e;
+  return set_max_dyn_smem((const void*)zgemm_grouped_kernel<PLAIN, MINB, AMAX, CFORM>, SMEM_BYTES, true);
 }
 
 cudaError_t zgemm_grouped(ZGemmGroup& g, cudaStream_t stream) {

@@ -862,23 +862,14 @@ cudaError_t zinv_batched2(double2* M, long long ld, long long bstride, int n, in
   GjScratch S;
   carve(S, scratch, n, nb, batch);
   const size_t smem = size_t(nb) * (n + 1) * sizeof(double2) + 3 * size_t(n) * sizeof(int);
-  static size_t attr = 0;
   cudaError_t e;
-  if (smem > attr) {
-    if ((e = cudaFuncSetAttribute(gj_panel_kernel<kNB>, cudaFuncAttributeMaxDynamicSharedMemorySize, int(smem))))
-      return e;
-    attr = smem;
-  }
+  if ((e = set_max_dyn_smem((const void*)gj_panel_kernel<kNB>, smem))) return e;
   const size_t rows_smem = size_t(nb) * (n + 2) * sizeof(double2);  // Vs staging of the tail
-  static size_t attr_rows = 0;
-  if (rows_smem > attr_rows) {
+  {
     const void* fns[4] = {(const void*)gj_panel_rows_kernel<kNB, 1>, (const void*)gj_panel_rows_kernel<kNB, 2>,
                           (const void*)gj_pair_kernel<kNB, 1>, (const void*)gj_pair_kernel<kNB, 2>};
     for (int i = 0; i < 4; ++i)
-      if ((e = cudaFuncSetAttribute(fns[i], cudaFuncAttributeMaxDynamicSharedMemorySize,
-                                    int((i >= 2 && pair_pre2(n) ? 2 : 1) * rows_smem))))
-        return e;
-    attr_rows = rows_smem;
+      if ((e = set_max_dyn_smem(fns[i], (i >= 2 && pair_pre2(n) ? 2 : 1) * rows_smem))) return e;
   }
   const long long nn = (long long)n * n;
   // panel steps: two panels per step (pair kernel, one rank-2nb GEMM) wherever both

@@ -12,7 +12,12 @@ contiguous task ranges, hence contiguous layer ranges of the band. Protocol
      task, e.g. 8 domains at b = 768: 680 MB over NVLink);
   3. phase 2, identical on every rank: left/right-connected sweeps over the P
      separators -> boundary self-energies, right-connected G, separator G;
-  4. phase 3 on every rank: in-place RGF re-solve of its chains + couplings.
+  4. phase 3 on every rank: in-place RGF re-solve of its chains;
+  5. all-gather of two boundary blocks per rank (the halo), then the couplings between
+     chains, each consistent with the chain whose row of A G it closes.
+
+The same protocol runs inside the library with NCCL (bbsi_cuda_ddrgf_rank_dev,
+:func:`ddrgf_nccl`); this module keeps the phase-by-phase form for the CPU tests.
 
 ``engine`` is the phase implementation; production code always uses
 :class:`CudaPhases` (the C ABI). The CPU tests inject a numpy restatement to run the
@@ -125,6 +130,20 @@ class CudaPhases:
         _raise(rc, fail.value)
         return G
 
+    def halo(self, G, t0: int, t1: int):
+        import torch
+
+        h = torch.empty((2, self.b, self.b), dtype=torch.complex128, device=G.device)
+        _raise(lib().bbsi_cuda_ddrgf_halo_dev(self.l, self.b, self.s2, t0, t1, _ptr(G), _ptr(h), _stream()))
+        return h
+
+    def couplings(self, A_loc, G, out, t0: int, t1: int, prev_sep_g=None, next_x0_g=None):
+        p = _ptr(prev_sep_g) if prev_sep_g is not None else None
+        n = _ptr(next_x0_g) if next_x0_g is not None else None
+        _raise(lib().bbsi_cuda_ddrgf_couplings_dev(self.l, self.b, self.s2, t0, t1, _ptr(A_loc), _ptr(G), _ptr(out),
+                                                   p, n, _stream()))
+        return G
+
 
 def gather_packets(packet, ranges, group=None):
     """All-gather of the per-rank packets into task order (padded to the largest range)."""
@@ -160,4 +179,55 @@ def ddrgf_distributed(A_loc, l: int, b: int, s2: int, group=None, engine=None):
     packet = eng.phase1(A_loc, t0, t1)
     packets = gather_packets(packet, ranges, group) if world > 1 else packet
     out = eng.phase2(packets)
-    return eng.phase3(A_loc, out, t0, t1)
+    G = eng.phase3(A_loc, out, t0, t1)
+    halo = eng.halo(G, t0, t1)
+    prev = nxt = None
+    if world > 1:
+        halos = gather_packets(halo[None], [(r, r + 1) for r in range(world)], group)  # [world][2]
+        prev = halos[rank - 1, 1] if rank > 0 else None
+        nxt = halos[rank + 1, 0] if rank + 1 < world else None
+    return eng.couplings(A_loc, G, out, t0, t1, prev, nxt)
+
+
+class NcclComm:
+    """A NCCL communicator created by the library (one per rank); the unique id travels
+    over torch.distributed (or any side channel) once."""
+
+    def __init__(self, group=None):
+        import torch
+        import torch.distributed as dist
+
+        world = dist.get_world_size(group) if dist.is_initialized() else 1
+        rank = dist.get_rank(group) if dist.is_initialized() else 0
+        uid = (C.c_ubyte * 128)()
+        if rank == 0:
+            _raise(lib().bbsi_cuda_nccl_unique_id(uid))
+        if world > 1:
+            dev = torch.device("cuda", torch.cuda.current_device())
+            t = torch.tensor(list(bytes(uid)), dtype=torch.uint8, device=dev)
+            dist.broadcast(t, 0, group=group)
+            uid = (C.c_ubyte * 128)(*t.cpu().tolist())
+        self.comm = C.c_void_p()
+        _raise(lib().bbsi_cuda_nccl_comm_init(uid, world, rank, C.byref(self.comm)))
+        self.world, self.rank = world, rank
+
+    def close(self):
+        if self.comm:
+            lib().bbsi_cuda_nccl_comm_destroy(self.comm)
+            self.comm = C.c_void_p()
+
+
+def rank_layers(l: int, s2: int, world: int, rank: int) -> tuple[int, int, int, int]:
+    """(t0, t1, L0, L1): the task range and band rows a rank owns (C ABI)."""
+    v = [C.c_int() for _ in range(4)]
+    _raise(lib().bbsi_cuda_ddrgf_rank_layers(l, s2, world, rank, *[C.byref(x) for x in v]))
+    return tuple(x.value for x in v)
+
+
+def ddrgf_nccl(comm: NcclComm, A_loc, G_loc, l: int, b: int, s2: int):
+    """This rank's part of the domain-sharded DDRGF with NCCL inside the library
+    (bbsi_cuda_ddrgf_rank_dev): A_loc / G_loc are the rank's band rows (rank_layers)."""
+    fail = C.c_int(-1)
+    rc = lib().bbsi_cuda_ddrgf_rank_dev(comm.comm, l, b, s2, _ptr(A_loc), _ptr(G_loc), C.byref(fail), _stream())
+    _raise(rc, fail.value)
+    return G_loc

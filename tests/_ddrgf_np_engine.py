@@ -47,7 +47,6 @@ class NumpyPhases:
         L0, _ = layer_range(self.tasks, t0, t1)
         A = lambda a, off: _blk(A_loc, a - L0, off)  # noqa: E731
         pk = np.zeros((t1 - t0, PACKET_BLOCKS, b, b), dtype=np.complex128)
-        s0 = -1j * GAMMA * np.eye(b)
         for t in range(t0, t1):
             tk = self.tasks[t]
             q = t - t0
@@ -59,8 +58,9 @@ class NumpyPhases:
                     if i + 1 < n:
                         M[i * b:(i + 1) * b, (i + 1) * b:(i + 2) * b] = A(tk.first + i, 1)
                         M[(i + 1) * b:(i + 2) * b, i * b:(i + 1) * b] = A(tk.first + i + 1, -1)
-                M[:b, :b] -= s0
-                M[-b:, -b:] -= s0
+                g = GAMMA * (np.abs(A(tk.sep, 0)).max() or 1.0)
+                M[:b, :b] += 1j * g * np.eye(b)
+                M[-b:, -b:] += 1j * g * np.eye(b)
                 Mi = np.linalg.inv(M)
                 corners = (Mi[:b, :b], Mi[:b, -b:], Mi[-b:, :b], Mi[-b:, -b:])
                 for k, m in enumerate(corners):
@@ -77,32 +77,33 @@ class NumpyPhases:
         b, T = self.b, len(self.tasks)
         P = lambda t, k: packets[t, k].numpy().T  # noqa: E731
         I = np.eye(b)
-        ig = 1j * GAMMA * I
+        gam = [GAMMA * (np.abs(P(t, 4)).max() or 1.0) for t in range(T)]  # per-task fake-lead strength
         out = np.zeros((T, PHASE2_BLOCKS, b, b), dtype=np.complex128)
-        gL, SLs, Y = [None] * T, [None] * T, [None] * T
+        gL, Y = [None] * T, [None] * T
         for t, tk in enumerate(self.tasks):
+            g = gam[t]
             if tk.count:
                 SL = P(t, 8) @ gL[t - 1] @ P(t - 1, 7) if t > 0 else np.zeros((b, b), complex)
                 out[t, 0] = _slot(SL)
-                Df = SL + ig
+                Df = SL + 1j * g * I
                 e1 = P(t, 3) + P(t, 2) @ np.linalg.inv(I - Df @ P(t, 0)) @ Df @ P(t, 1)
-                gld = e1 + 1j * GAMMA * e1 @ np.linalg.inv(I - 1j * GAMMA * e1) @ e1
-                SLs[t] = P(t, 5) @ gld @ P(t, 6)
+                gld = e1 + 1j * g * e1 @ np.linalg.inv(I - 1j * g * e1) @ e1
+                Sleft = P(t, 5) @ gld @ P(t, 6)
             else:
-                SLs[t] = P(t, 5) @ gL[t - 1] @ P(t - 1, 7)
-                out[t, 0] = _slot(SLs[t])
-            gL[t] = np.linalg.inv(P(t, 4) - SLs[t])
+                Sleft = P(t, 5) @ gL[t - 1] @ P(t - 1, 7)
+                out[t, 0] = _slot(Sleft)
+            gL[t] = np.linalg.inv(P(t, 4) - Sleft)
+            out[t, 3] = _slot(gL[t])
         for t in range(T - 1, -1, -1):
             tk = self.tasks[t]
+            g = gam[t]
             SR = P(t, 7) @ Y[t + 1] @ P(t + 1, 8) if t < T - 1 else np.zeros((b, b), complex)
             out[t, 1] = _slot(SR)
-            pre = P(t, 4) - SR
-            out[t, 3] = _slot(np.linalg.inv(pre - SLs[t]))
-            gR = np.linalg.inv(pre)
+            gR = np.linalg.inv(P(t, 4) - SR)
             if tk.count:
-                Dl = P(t, 6) @ gR @ P(t, 5) + ig
+                Dl = P(t, 6) @ gR @ P(t, 5) + 1j * g * I
                 a1 = P(t, 0) + P(t, 1) @ np.linalg.inv(I - Dl @ P(t, 3)) @ Dl @ P(t, 2)
-                Y[t] = a1 + 1j * GAMMA * a1 @ np.linalg.inv(I - 1j * GAMMA * a1) @ a1
+                Y[t] = a1 + 1j * g * a1 @ np.linalg.inv(I - 1j * g * a1) @ a1
             else:
                 Y[t] = gR
             out[t, 2] = _slot(Y[t])
@@ -130,9 +131,27 @@ class NumpyPhases:
                 if q + 1 < len(layers):
                     _put(G, x - L0, 1, gu[q])
                     _put(G, x + 1 - L0, -1, gl[q])
-            x0 = layers[0]
+        return G
+
+    def halo(self, G, t0, t1):
+        L0, _ = layer_range(self.tasks, t0, t1)
+        tk0, tk1 = self.tasks[t0], self.tasks[t1 - 1]
+        x0 = tk0.first if tk0.count else tk0.sep
+        return torch.stack([G[x0 - L0, 1].clone(), G[tk1.sep - L0, 1].clone()])
+
+    def couplings(self, A_loc, G, out, t0, t1, prev_sep_g=None, next_x0_g=None):
+        T = len(self.tasks)
+        L0, _ = layer_range(self.tasks, t0, t1)
+        A = lambda a, off: _blk(A_loc, a - L0, off)  # noqa: E731
+        O_ = lambda t, k: out[t, k].numpy().T  # noqa: E731
+        x0_of = lambda t: self.tasks[t].first if self.tasks[t].count else self.tasks[t].sep  # noqa: E731
+        for t in range(t0, t1):
+            x0 = x0_of(t)
             if t > 0:
-                _put(G, x0 - L0, -1, -O_(t, 2) @ A(x0, -1) @ O_(t - 1, 3))
+                gss = prev_sep_g.numpy().T if t == t0 else _blk(G, self.tasks[t - 1].sep - L0, 0)
+                _put(G, x0 - L0, -1, -O_(t, 2) @ A(x0, -1) @ gss)
             if t < T - 1:
-                _put(G, tk.sep - L0, 1, -O_(t, 3) @ A(tk.sep, 1) @ O_(t + 1, 2))
+                sp = self.tasks[t].sep
+                gxx = next_x0_g.numpy().T if t == t1 - 1 else _blk(G, x0_of(t + 1) - L0, 0)
+                _put(G, sp - L0, 1, -O_(t, 3) @ A(sp, 1) @ gxx)
         return G

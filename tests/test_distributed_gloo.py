@@ -95,3 +95,17 @@ def test_two_ranks_gloo(case):
         p.join(timeout=60)
     assert all(p.exitcode == 0 for p in procs)
     assert err <= 1e-10
+
+
+def test_rank_layers_c_abi_matches_protocol():
+    """bbsi_cuda_ddrgf_rank_layers (host-only C ABI, used by the NCCL path inside the
+    library) agrees with the Python protocol's task ranges and band rows."""
+    for l, s2, world in ((4096, 127, 8), (4096, 511, 8), (2048, 255, 4), (30, 5, 3), (17, 7, 2), (23, 4, 5)):
+        tasks = Dd.partition(l, s2)
+        for rank, (t0, t1) in enumerate(Dd.task_ranges(len(tasks), world)):
+            L0, L1 = Dd.layer_range(tasks, t0, t1)
+            assert Dd.rank_layers(l, s2, world, rank) == (t0, t1, L0, L1)
+    from paper_2605_19910_b200 import InvalidArgumentError
+
+    with pytest.raises(InvalidArgumentError):
+        Dd.rank_layers(30, 5, 6, 0)  # 5 domains, 6 ranks
