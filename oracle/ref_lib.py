@@ -15,7 +15,11 @@ from . import bbsi_oracle as O
 
 HERE = Path(__file__).resolve().parent
 LIB_PATH = HERE / "_ref" / "libbbsi_ref.so"
+# the same unmodified reference linked against scipy's OpenBLAS 0.3.31 (oracle/ref/Makefile):
+# only its BLAS rounding differs, so its distance to LIB_PATH is the reference's own floor
+SCIPY_LIB_PATH = HERE / "_ref" / "libbbsi_ref_scipy.so"
 _lib = None
+_lib_scipy = None
 
 
 def available() -> bool:
@@ -30,6 +34,16 @@ def lib():
         _lib = C.CDLL(str(LIB_PATH))
         _lib.ref_last_error.restype = C.c_char_p
     return _lib
+
+
+def lib_scipy():
+    global _lib_scipy
+    if _lib_scipy is None:
+        if not SCIPY_LIB_PATH.exists():
+            raise FileNotFoundError(f"{SCIPY_LIB_PATH} missing: run `make -C oracle/ref`")
+        _lib_scipy = C.CDLL(str(SCIPY_LIB_PATH))
+        _lib_scipy.ref_last_error.restype = C.c_char_p
+    return _lib_scipy
 
 
 def _p(a):

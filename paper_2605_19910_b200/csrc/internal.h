@@ -83,7 +83,14 @@ struct SweepWork {
   // touches them reads A = z I - H - sigma I from H (only the chains' first layers are formed)
   const double2* zdev = nullptr;
   const double2* sigdev = nullptr;
+  // one-ended sweeps, w >= 2 (refine_multipliers_default): copies of the pivots f_j
+  // ([batch][bs*bs]) for one step of iterative refinement of every multiplier
+  double2* fcopy = nullptr;
 };
+// One refinement step of the w >= 2 multipliers (lm += X (M - f lm), um += (M - um f) X):
+// explicit-inverse products are not backward stable; with it the residual of the
+// n-diagonal sweep matches the reference's LU solves (env BBSI_REFINE=0 turns it off).
+bool refine_multipliers_default();
 
 // Bytes of LM+UM+piv+wz+status for a sweep.
 size_t sweep_scratch_bytes(int l, int w, int bs, int batch, int groups = 1, bool two_ended = false);

@@ -91,6 +91,18 @@ bool mid_dense_enabled() {
 
 bool sweep_is_two_ended(const SweepWork& W) { return use_two_ended(W); }
 
+bool refine_multipliers_default() {
+  static const bool on = [] {
+    const char* e = getenv("BBSI_REFINE");
+    return !(e && atoi(e) == 0);
+  }();
+  return on;
+}
+
+namespace {
+bool refine_ok(int l, int w, bool two_ended) { return w >= 2 && !two_ended_ok(two_ended, l, w) && refine_multipliers_default(); }
+}  // namespace
+
 
 
 size_t sweep_scratch_bytes(int l, int w, int bs, int batch, int groups, bool two_ended) {
@@ -100,6 +112,7 @@ size_t sweep_scratch_bytes(int l, int w, int bs, int batch, int groups, bool two
   s += size_t(groups) * (zinv_scratch_bytes(bs, chains * ((batch + groups - 1) / groups)) + 256);  // inversion scratch
   s += size_t(l) * batch * sizeof(int) + 256;             // status
   if (chains == 2 && w >= 2) s += size_t(groups) * mid_bytes(w, bs, (batch + groups - 1) / groups);  // dense middle
+  if (refine_ok(l, w, two_ended)) s += size_t(batch) * bb + 256;  // pivot copies for the refinement
   return s;
 }
 
@@ -117,6 +130,7 @@ void sweep_carve(SweepWork& W, void* base) {
   p += size_t(W.l) * W.batch * sizeof(int);
   p = reinterpret_cast<char*>((reinterpret_cast<uintptr_t>(p) + 255) & ~uintptr_t(255));  // (+256 slack sized)
   W.mid = (use_two_ended(W) && W.w >= 2) ? p : nullptr;
+  W.fcopy = (!W.Hoff && refine_ok(W.l, W.w, W.two_ended)) ? reinterpret_cast<double2*>(p) : nullptr;
 }
 
 namespace {
@@ -178,6 +192,10 @@ cudaError_t rgf_sweeps_one(const SweepWork& W, const int* n_true, int* status, i
   // ---------------- upward sweep (rgf.hpp:98-114)
   for (int j = l - 1; j >= 1; --j) {
     const int k = j < w ? j : w;
+    if (W.fcopy && !(W.Hoff && w == 1) &&
+        (e = cudaMemcpy2DAsync(W.fcopy, c.bb * sizeof(double2), c.slot(j, 0), W.g_bstride * sizeof(double2),
+                               c.bb * sizeof(double2), W.batch, cudaMemcpyDeviceToDevice, s)) != cudaSuccess)
+      return e;
     if ((e = inv(j)) != cudaSuccess) return e;
     const ZOp X = c.gop(c.slot(j, 0), 0, 0);
     // lm[j] = X_j [M'(j,j-1) .. M'(j,j-k)]
@@ -187,6 +205,13 @@ cudaError_t rgf_sweeps_one(const SweepWork& W, const int* n_true, int* status, i
     ZGemmProblem p_lm = prob(b, k * b, b, sg, 0.0, X, hs ? c.hop(j, -1) : c.gop(c.slot(j, -1), 0, -1),
                              c.mop(c.lm(j), 0, 1));
     if ((e = launch(W, {p_lm}, s)) != cudaSuccess) return e;
+    const bool refine = W.fcopy && !hs;
+    const ZOp F{W.fcopy, b, 0, 0, c.bb};
+    if (refine) {  // R = M'(j, j-t) - f_j lm (in place: the row is not read again); lm += X R
+      const ZOp row = c.gop(c.slot(j, -1), 0, -1);
+      if ((e = launch(W, {prob(b, k * b, b, -1.0, 1.0, F, c.mop(c.lm(j), 0, 1), row)}, s)) != cudaSuccess) return e;
+      if ((e = launch(W, {prob(b, k * b, b, 1.0, 1.0, X, row, c.mop(c.lm(j), 0, 1))}, s)) != cudaSuccess) return e;
+    }
     // window M'(j-s, j-t) -= M'(j-s, j) lm[j][t];  um[j] = [M'(j-t, j)]_t X_j
     ZOp upper = hs ? c.hop(j - 1, +1) : c.gop(c.slot(j - 1, +1), -two_w, 0);
     ZGemmProblem p_win = prob(k * b, k * b, b, -sg, 1.0, upper, c.mop(c.lm(j), 0, 1), c.gop(c.slot(j - 1, 0), -two_w, -1));
@@ -197,6 +222,10 @@ cudaError_t rgf_sweeps_one(const SweepWork& W, const int* n_true, int* status, i
     }
     ZGemmProblem p_um = prob(k * b, b, b, sg, 0.0, upper, X, c.mop(c.um(j), 1, 0));
     if ((e = launch(W, {p_win, p_um}, s)) != cudaSuccess) return e;
+    if (refine) {  // R = M'(j-t, j) - um f_j (in place: the column is not read again); um += R X
+      if ((e = launch(W, {prob(k * b, b, b, -1.0, 1.0, c.mop(c.um(j), 1, 0), F, upper)}, s)) != cudaSuccess) return e;
+      if ((e = launch(W, {prob(k * b, b, b, 1.0, 1.0, upper, X, c.mop(c.um(j), 1, 0))}, s)) != cudaSuccess) return e;
+    }
   }
   if ((e = inv(0)) != cudaSuccess) return e;
 
@@ -564,6 +593,7 @@ cudaError_t rgf_sweeps(const SweepWork& W, const int* n_true, cudaStream_t s) {
     Wg.inv = static_cast<char*>(W.inv) + size_t(g) * inv_b;
     Wg.e_off = W.e_off + e0;
     if (W.zdev) Wg.zdev = W.zdev + e0;
+    if (W.fcopy) Wg.fcopy = W.fcopy + (long long)e0 * bb;
     if ((e = cudaStreamWaitEvent(P.s[g], P.ev[G], 0))) return e;
     if ((e = sweep(Wg, W.status + e0, P.s[g], g))) return e;
     if ((e = cudaEventRecord(P.ev[g], P.s[g]))) return e;

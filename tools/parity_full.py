@@ -16,10 +16,17 @@ Oracles (the checker, never the product path):
 
 Per solve: max / median of the per-block relative Frobenius error
 ||G_gpu - G_ref||_F / ||G_ref||_F over every in-band block (north_star's metric,
-bar 1e-10); the reference's input-noise floor (the same metric between the reference
-on A and on A with every real/imaginary component moved one ulp up or down with
-probability 1/2 -- mean perturbation 1/2 ulp); the residual max_i ||(A G)_ii - I||_F /
-sqrt(b) of the GPU and of the reference solution.
+bar 1e-10), the reference's own floor at that energy, and the residual
+max_i ||(A G)_ii - I||_F / sqrt(b) of the GPU and of the reference solution.
+The floor is how far the reference moves from itself under perturbations no
+implementation controls, the max of
+  floor_input: the reference on A vs on A with every real/imaginary component moved
+               one ulp up or down with probability 1/2 (input rounding, mean 1/2 ulp);
+  floor_blas:  the reference vs the SAME unmodified reference linked against another
+               OpenBLAS build (0.3.31 instead of 0.3.15: only the rounding order of the
+               BLAS kernels differs; oracle/_ref/libbbsi_ref_scipy.so).
+An implementation whose residual matches the reference's is as close to it as the
+reference is to itself; the verdict is "<= 1e-10", else "<= floor", else "ABOVE".
 """
 from __future__ import annotations
 
@@ -101,9 +108,10 @@ def perturb(S, seed):
     return y.view(np.complex128).reshape(S.shape)
 
 
-def ref_solve_many(SAs, w, threads_per_solve=1):
-    """Compiled reference rgf_tridiag / rgf_ndiag on each slot array, one host thread each."""
-    L = R.lib()
+def ref_solve_many(SAs, w, threads_per_solve=1, scipy_blas=False):
+    """Compiled reference rgf_tridiag / rgf_ndiag on each slot array, one host thread each
+    (scipy_blas: the same reference built on scipy's OpenBLAS 0.3.31)."""
+    L = R.lib_scipy() if scipy_blas else R.lib()
     L.ref_set_threads(C.c_int(threads_per_solve))
     outs = [np.zeros_like(a) for a in SAs]
     errs = []
@@ -162,13 +170,16 @@ def check_batched(k, energies=None, group=16):
         SAs = [dyson_slots(h, cfg, e) for e in idx]
         SPs = [perturb(a, 1000 + e) for a, e in zip(SAs, idx)]
         refs = ref_solve_many(SAs + SPs, w)
+        refs_b = ref_solve_many(SAs, w, scipy_blas=True)
         for q, e in enumerate(idx):
             Sr, Sp = refs[q], refs[len(idx) + q]
             Sg = G[g0 + q].cpu().numpy()
             mx, md, _ = summarize(Sg, Sr, w)
-            fl = summarize(Sp, Sr, w)[0]
+            fi = summarize(Sp, Sr, w)[0]
+            fb = summarize(refs_b[q], Sr, w)[0]
             rec = {"config": k, "workload": cfg.name, "solver": "gpu rgf (batched, default path)",
-                   "energy_index": int(e), "E": float(cfg.z()[e].real), "max": mx, "median": md, "floor": fl,
+                   "energy_index": int(e), "E": float(cfg.z()[e].real), "max": mx, "median": md,
+                   "floor": max(fi, fb), "floor_input": fi, "floor_blas": fb,
                    "residual_gpu": float(residual_rows(SAs[q], Sg, w).max()),
                    "residual_ref": float(residual_rows(SAs[q], Sr, w).max()),
                    "oracle": "oracle/_ref (compiled reference, OpenBLAS 0.3.15)"}
@@ -178,7 +189,7 @@ def check_batched(k, energies=None, group=16):
                 rec["gpu_vs_dense"] = summarize(Sg, Sd, w)[0]
                 rec["ref_vs_dense"] = summarize(Sr, Sd, w)[0]
             emit(rec)
-        del SAs, SPs, refs
+        del SAs, SPs, refs, refs_b
     print(f"config {k} checked in {time.time() - t0:.0f}s", flush=True)
 
 
@@ -195,9 +206,13 @@ def check_cfg4(domains=(2, 4, 8, 16, 32)):
     del h
     Sr = ref_solve_many([SA], w, nproc)[0]
     Sp = ref_solve_many([perturb(SA, 4000)], w, nproc)[0]
-    fl = summarize(Sp, Sr, w)[0]
+    fi = summarize(Sp, Sr, w)[0]
     del Sp
-    print(f"config 4: reference + perturbed reference in {time.time() - t0:.0f}s, floor {fl:.3e}", flush=True)
+    Sp = ref_solve_many([SA], w, nproc, scipy_blas=True)[0]
+    fb = summarize(Sp, Sr, w)[0]
+    del Sp
+    fl = max(fi, fb)
+    print(f"config 4: references in {time.time() - t0:.0f}s, floor input {fi:.3e} blas {fb:.3e}", flush=True)
     res_ref = float(residual_rows(SA, Sr, w).max())
     H = torch.empty((l, 3, b, b), dtype=torch.complex128, device="cuda")
     D.fill_h_device(cfg, H)
@@ -212,7 +227,8 @@ def check_cfg4(domains=(2, 4, 8, 16, 32)):
         Sg = Gd.cpu().numpy()
         mx, md, e = summarize(Sg, Sr, w)
         emit({"config": 4, "workload": cfg.name, "solver": name, "energy_index": 0, "E": float(cfg.z()[0].real),
-              "max": mx, "median": md, "floor": fl, "residual_gpu": float(residual_rows(SA, Sg, w).max()),
+              "max": mx, "median": md, "floor": fl, "floor_input": fi, "floor_blas": fb,
+              "residual_gpu": float(residual_rows(SA, Sg, w).max()),
               "residual_ref": res_ref, "worst_block": [int(x) for x in np.unravel_index(np.nanargmax(e), e.shape)],
               "oracle": "oracle/_ref (compiled reference, OpenBLAS 0.3.15)"})
         del Sg
