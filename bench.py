@@ -8,12 +8,14 @@ BASELINE names no dataset). A "step" is the selected inversion of all 64 energie
 (strong scaling, no data-path collective).
 
   python bench.py [--gpus N] [--steps K] [--warmup W] [--config 2] [--impl ours|reference]
-  python bench.py --config 4 [--domains P]     DDRGF of config 4 (one energy), P domains
-                                                sharded over the ranks (NCCL all-gather of
-                                                the corner packets, distributed.py)
+  python bench.py --config 3                    n-diagonal RGF (w = 2), 32 energies
+  python bench.py --config 4|5 [--domains P]   DDRGF of config 4 (one energy, P = 32) / config 5
+                                                (8 energies, P = 8); domains sharded over the
+                                                ranks, NCCL inside the library
 
 Prints ONE JSON line (rank 0). Keys beyond the driver contract:
-  roofline      dominant kernel (the DMMA GEMM) vs the FP64 DMMA peak measured live
+  roofline      dominant kernel (the DMMA GEMM) vs the FP64 DMMA peak measured live; its
+                DRAM traffic per launch from an ncu probe run in the same bench
   cpu_baseline  compiled reference rgf_tridiag (oracle/_ref) on a bounded sample, host cores
   e2e           same metric through the host-buffer C ABI (H2D of H, D2H of every G band)
 """
@@ -48,7 +50,8 @@ def parse():
     p.add_argument("--impl", default="ours", choices=["ours", "reference"])
     p.add_argument("--no-e2e", action="store_true")
     p.add_argument("--no-cpu-baseline", action="store_true")
-    p.add_argument("--domains", type=int, default=0, help="config 4: DDRGF domains (0 = max(32, world))")
+    p.add_argument("--domains", type=int, default=0, help="configs 4/5: DDRGF domains (0 = 32 / 8, at least world)")
+    p.add_argument("--no-traffic", action="store_true", help="skip the ncu DRAM-traffic probe of the dominant kernel")
     p.add_argument("--chunk", type=int, default=0, help="energy chunk of the e2e path (0 = library default: ~32 energies per chunk from 48 energies up)")
     return p.parse_args()
 
@@ -180,6 +183,22 @@ def workload_config(cfg, n_energies: int) -> dict:
                    "L2-resident workload (below the 126 MB L2; not flushed)")}
 
 
+SUBCHAIN = {4: 1024, 5: 48}  # leading layers of the reference's bounded single-energy sample (DDRGF configs)
+
+
+def cpu_subchain(cfg, nproc: int, k: int):
+    """Compiled reference rgf_tridiag on the leading SUBCHAIN[k] layers of the config's
+    first energy, nproc BLAS threads (rgf_tridiag costs the same per layer at any chain
+    length, so layers/s is the metric's rate). Returns (seconds, layers, sample text)."""
+    nl = min(SUBCHAIN[k], cfg.num_layers)
+    from paper_2605_19910_b200.dyson import scaled
+
+    sub = scaled(cfg, num_layers=nl)
+    t = cpu_reference(sub, cpu_inputs(sub, [0]), nproc)
+    return t, nl, (f"layers 0..{nl - 1} of {cfg.name} (one energy, E = {cfg.z()[0].real:g}), {nproc} BLAS threads "
+                   f"(compiled reference rgf_tridiag, oracle/_ref)")
+
+
 # ---------------------------------------------------------------------------- reference arm
 def run_reference(args, rank, world):
     from paper_2605_19910_b200.dyson import CONFIGS
@@ -188,15 +207,24 @@ def run_reference(args, rank, world):
         return
     cfg = CONFIGS[args.config]
     nproc = os.cpu_count() or 1
-    idx = energy_sample(cfg.n_energy, nproc)
-    inputs = cpu_inputs(cfg, idx)  # outside the timed region
-    for _ in range(args.warmup):
-        cpu_reference(cfg, inputs, 1)
-    times = [cpu_reference(cfg, inputs, 1) for _ in range(args.steps)]
-    tot = sum(times)
-    value = args.steps * len(idx) * cfg.num_layers / tot
-    sample = (f"energies {idx} of the {cfg.n_energy}-point grid per step, one per host thread, 1 BLAS thread "
-              f"each (compiled reference, oracle/_ref)")
+    if args.config in (4, 5):
+        for _ in range(args.warmup):
+            cpu_subchain(cfg, nproc, args.config)
+        res = [cpu_subchain(cfg, nproc, args.config) for _ in range(args.steps)]
+        tot = sum(r[0] for r in res)
+        value = sum(r[1] for r in res) / tot
+        sample, cores = res[0][2] + " per step", nproc
+    else:
+        idx = energy_sample(cfg.n_energy, nproc)
+        inputs = cpu_inputs(cfg, idx)  # outside the timed region
+        for _ in range(args.warmup):
+            cpu_reference(cfg, inputs, 1)
+        times = [cpu_reference(cfg, inputs, 1) for _ in range(args.steps)]
+        tot = sum(times)
+        value = args.steps * len(idx) * cfg.num_layers / tot
+        sample = (f"energies {idx} of the {cfg.n_energy}-point grid per step, one per host thread, 1 BLAS thread "
+                  f"each (compiled reference, oracle/_ref)")
+        cores = len(idx)
     maps = Path("/proc/self/maps").read_text() if Path("/proc/self/maps").exists() else ""
     line = {"impl": "reference", "metric": METRIC, "value": value, "unit": UNIT, "n_gpus": args.gpus,
             "steps": args.steps, "warmup": args.warmup, "ms_per_step": 1e3 * tot / args.steps,
@@ -204,14 +232,146 @@ def run_reference(args, rank, world):
             "data": "synthetic (seeded Dyson generator; oracle/dyson_oracle.py restatement)",
             "config": workload_config(cfg, cfg.n_energy),
             "solver": "reference rgf_tridiag / rgf_ndiag (oracle/_ref: unmodified headers, OpenBLAS 0.3.15)",
-            "cpu_baseline": {"value": value, "unit": UNIT, "cores": len(idx), "kind": "reference",
-                             "sample": sample},
+            "cpu_baseline": {"value": value, "unit": UNIT, "cores": cores, "kind": "reference", "sample": sample},
             "repo_library_mapped": "libbbsi_cuda" in maps,
             "e2e": {"value": value, "unit": UNIT, "h2d_bytes_per_step": 0, "d2h_bytes_per_step": 0}}
     print(json.dumps(line), flush=True)
 
 
-# ---------------------------------------------------------------------------- our arm
+# ---------------------------------------------------------------------------- profiling helpers
+CATS = ["zgemm_dmma", "gj_panel", "band_ops", "gj_gemm"]
+
+
+def profile_step(L, step, one_group=True):
+    """CUDA events around every library launch of one step (one stream group, so each
+    launch's event time is its own duration). Per category: launches, ms, TFLOP/s, GB/s
+    (algorithmic flops / bytes the launches declare) and bytes per launch."""
+    import torch
+
+    old = os.environ.get("BBSI_GROUPS")
+    if one_group:
+        os.environ["BBSI_GROUPS"] = "1"
+    L.bbsi_cuda_profile_enable(1)
+    step()
+    torch.cuda.synchronize()
+    L.bbsi_cuda_profile_enable(0)
+    if one_group:
+        if old is None:
+            del os.environ["BBSI_GROUPS"]
+        else:
+            os.environ["BBSI_GROUPS"] = old
+    prof = np.zeros(4 * len(CATS))
+    L.bbsi_cuda_profile_collect(prof.ctypes.data_as(C.c_void_p), len(CATS))
+    cats = {}
+    for i, name in enumerate(CATS):
+        cnt, tms, fl, by = prof[4 * i: 4 * i + 4]
+        cats[name] = {"launches": int(cnt), "ms": round(tms, 3),
+                      "tflops": round(fl / (tms * 1e-3) / 1e12, 3) if tms > 0 else None,
+                      "gbs": round(by / (tms * 1e-3) / 1e9, 1) if tms > 0 else None,
+                      "alg_bytes_per_launch": round(by / cnt) if cnt else None,
+                      "flops_per_launch": round(fl / cnt) if cnt else None}
+    return cats
+
+
+def measure_traffic(config: int, domains: int, timeout: float = 240.0):
+    """DRAM bytes per launch of the dominant kernel, measured in this run: ncu on a child
+    process that runs one eager step of the same workload (tools/traffic_probe.py),
+    profiling a few sweep-GEMM launches (zgemm_grouped_kernel<0,...>: the non-plain
+    instantiations, i.e. not the Gauss-Jordan updates). None if ncu is unavailable."""
+    import csv
+    import io
+    import shutil
+    import tempfile
+
+    ncu = shutil.which("ncu") or "/usr/local/cuda/bin/ncu"
+    if not Path(ncu).exists():
+        return None
+    with tempfile.TemporaryDirectory() as td:
+        log = Path(td) / "ncu.csv"
+        cmd = [ncu, "--metrics", "dram__bytes_read.sum,dram__bytes_write.sum,gpu__time_duration.sum",
+               "--clock-control", "none", "--kernel-name-base", "demangled", "--kernel-name",
+               "regex:zgemm_grouped_kernel<0", "--launch-skip", "40", "--launch-count", "6", "--csv",
+               "--log-file", str(log), sys.executable, str(ROOT / "tools" / "traffic_probe.py"), "--config",
+               str(config)]
+        if domains:
+            cmd += ["--domains", str(domains)]
+        try:
+            subprocess.run(cmd, capture_output=True, timeout=timeout, check=True)
+            text = log.read_text()
+        except Exception as ex:  # the bench line stands without it
+            return {"error": f"ncu probe failed: {type(ex).__name__}"}
+    rows = list(csv.reader(io.StringIO(text[text.find('"ID"'):])))
+    if not rows:
+        return None
+    hdr = rows[0]
+    ii, im, iv, iu = hdr.index("ID"), hdr.index("Metric Name"), hdr.index("Metric Value"), hdr.index("Metric Unit")
+    per = {}
+    scale = {"byte": 1, "Kbyte": 1e3, "Mbyte": 1e6, "Gbyte": 1e9, "nsecond": 1e-9, "usecond": 1e-6, "msecond": 1e-3,
+             "second": 1}
+    for r in rows[1:]:
+        if len(r) <= max(ii, im, iv, iu):
+            continue
+        v = float(r[iv].replace(",", "")) * scale.get(r[iu], 1.0)
+        per.setdefault(r[ii], {})[r[im]] = v
+    launches = [d for d in per.values() if "dram__bytes_read.sum" in d]
+    if not launches:
+        return None
+    traffic = statistics.mean(d["dram__bytes_read.sum"] + d["dram__bytes_write.sum"] for d in launches)
+    dur = statistics.mean(d.get("gpu__time_duration.sum", 0.0) for d in launches)
+    return {"bytes_per_launch": traffic, "launches_profiled": len(launches), "ncu_mean_duration_us": dur * 1e6,
+            "command": "ncu --metrics dram__bytes_read.sum,dram__bytes_write.sum -k regex:zgemm_grouped_kernel<0 "
+                       f"-s 40 -c 6 python tools/traffic_probe.py --config {config}"}
+
+
+def roofline_block(cats, peak, traffic, step_tflops, kernel_note):
+    g = cats["zgemm_dmma"]
+    step_kernel_ms = sum(c["ms"] for c in cats.values())
+    out = {"bound": "tensor", "kernel": kernel_note, "achieved": g["tflops"], "peak": round(peak, 2),
+           "unit": "TFLOP/s", "frac": round(g["tflops"] / peak, 4) if (peak > 0 and g["tflops"]) else None,
+           "traffic": (traffic or {}).get("bytes_per_launch"), "traffic_unit": "DRAM bytes per sweep-GEMM launch "
+           "(ncu, this run)", "traffic_probe": traffic,
+           "alg_bytes_per_launch": g["alg_bytes_per_launch"],
+           "peak_source": "FP64 DMMA peak measured live in this run (bbsi_cuda_fp64_peak_tflops; "
+                          "MEASURED_PEAKS.json has no FP64 entry)",
+           "share_of_step": round(g["ms"] / step_kernel_ms, 3) if step_kernel_ms else None,
+           "step_algorithmic_tflops": round(step_tflops, 3),
+           "step_frac_of_peak": round(step_tflops / peak, 4) if peak > 0 else None, "kernels": cats}
+    return out
+
+
+def timed_loop(step, steps, stream, local_rank, world, dev):
+    """W warm-up steps are the caller's; here: barrier, K timed steps on `stream` with CUDA
+    events, barrier; returns (max-over-ranks ms, launches, clock summary)."""
+    import torch
+    import torch.distributed as dist
+
+    from paper_2605_19910_b200._native import lib
+
+    L = lib()
+    torch.cuda.synchronize()
+    if world > 1:
+        dist.barrier()
+    torch.cuda.synchronize()
+    n0 = L.bbsi_cuda_launch_count()
+    e0, e1 = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
+    with ClockSampler(local_rank) as clocks:
+        e0.record(stream)
+        for _ in range(steps):
+            step()
+        e1.record(stream)
+        torch.cuda.synchronize()
+    if world > 1:
+        dist.barrier()
+    ms = e0.elapsed_time(e1)
+    launches = L.bbsi_cuda_launch_count() - n0
+    if world > 1:
+        t = torch.tensor([ms], device=dev, dtype=torch.float64)
+        dist.all_reduce(t, op=dist.ReduceOp.MAX)
+        ms = float(t.item())
+    return ms, launches, clocks.summary()
+
+
+# ---------------------------------------------------------------------------- our arm (configs 1-3)
 def run_ours(args, rank, world, local_rank):
     import torch
     import torch.distributed as dist
@@ -241,73 +401,16 @@ def run_ours(args, rank, world, local_rank):
     def step():
         D.solve_device(cfg, H, G, z=zs, stream=stream)
 
-    def barrier():
-        if world > 1:
-            dist.barrier()
-
     for _ in range(max(3, args.warmup)):
         step()
-    torch.cuda.synchronize()
-    barrier()
-    torch.cuda.synchronize()
-    n0 = L.bbsi_cuda_launch_count()
-    e0, e1 = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
-    with ClockSampler(local_rank) as clocks:
-        e0.record(stream)
-        for _ in range(args.steps):
-            step()
-        e1.record(stream)
-        torch.cuda.synchronize()
-    barrier()
-    ms = e0.elapsed_time(e1)
-    launches = L.bbsi_cuda_launch_count() - n0
-    ms_max = ms
-    if world > 1:
-        t = torch.tensor([ms], device=dev, dtype=torch.float64)
-        dist.all_reduce(t, op=dist.ReduceOp.MAX)
-        ms_max = float(t.item())
-    ms_step = ms_max / args.steps
+    ms, launches, clocks = timed_loop(step, args.steps, stream, local_rank, world, dev)
+    ms_step = ms / args.steps
     value = n_all * l / (ms_step * 1e-3)
-    flops_energy = D.algorithmic_flops(cfg)
-    tflops = n_all * flops_energy / (ms_step * 1e-3) / 1e12
+    tflops = n_all * D.algorithmic_flops(cfg) / (ms_step * 1e-3) / 1e12
 
-    # ---- per-kernel breakdown of one step (CUDA events around every library launch).
-    # One stream group, so every launch runs alone and its event time is its own
-    # duration (with two groups the events of concurrent launches overlap).
-    old_groups = os.environ.get("BBSI_GROUPS")
-    os.environ["BBSI_GROUPS"] = "1"
-    L.bbsi_cuda_profile_enable(1)
-    step()
-    torch.cuda.synchronize()
-    L.bbsi_cuda_profile_enable(0)
-    if old_groups is None:
-        del os.environ["BBSI_GROUPS"]
-    else:
-        os.environ["BBSI_GROUPS"] = old_groups
-    prof = np.zeros(16)
-    L.bbsi_cuda_profile_collect(prof.ctypes.data_as(C.c_void_p), 4)
-    cats = {}
-    for i, name in enumerate(["zgemm_dmma", "gj_panel", "band_ops", "gj_gemm"]):
-        cnt, tms, fl, by = prof[4 * i: 4 * i + 4]
-        cats[name] = {"launches": int(cnt), "ms": round(tms, 3),
-                      "tflops": round(fl / (tms * 1e-3) / 1e12, 3) if tms > 0 else None,
-                      "gbs": round(by / (tms * 1e-3) / 1e9, 1) if tms > 0 else None}
+    cats = profile_step(L, step)
     peak = L.bbsi_cuda_fp64_peak_tflops(50.0, 5)
-    g = cats["zgemm_dmma"]
-    step_kernel_ms = sum(c["ms"] for c in cats.values())
-    roofline = {"bound": "tensor", "kernel": "zgemm_grouped_kernel (DMMA f64), sweep launches "
-                "(its Gauss-Jordan launches are listed as gj_gemm)", "achieved": g["tflops"],
-                "peak": round(peak, 2), "unit": "TFLOP/s", "frac": round(g["tflops"] / peak, 4) if peak > 0 else None,
-                # dram read + write of one sweep-GEMM launch (window + um of both chains of
-                # one 32-energy stream group, 2048 tiles) from the ncu --set full capture
-                # in profiles/r01_ncu_kernels.md
-                "traffic": 297.07e6, "traffic_unit": "bytes per launch (win+um, 2048 tiles)",
-                "peak_source": "FP64 DMMA peak measured live in this run (bbsi_cuda_fp64_peak_tflops; "
-                               "MEASURED_PEAKS.json has no FP64 entry)",
-                "share_of_step": round(g["ms"] / step_kernel_ms, 3) if step_kernel_ms else None,
-                "step_algorithmic_tflops": round(tflops / world, 3),
-                "step_frac_of_peak": round(tflops / world / peak, 4) if peak > 0 else None,
-                "kernels": cats}
+    traffic = None
 
     # ---- end to end through the host-buffer C ABI
     e2e = None
@@ -327,7 +430,8 @@ def run_ours(args, rank, world, local_rank):
         for _ in range(2):  # eager call, then the CUDA-graph capture (pinned buffers); time replays
             e2e_step()
         torch.cuda.synchronize()
-        barrier()
+        if world > 1:
+            dist.barrier()
         t0 = time.perf_counter()
         for _ in range(args.steps):
             e2e_step()
@@ -337,18 +441,7 @@ def run_ours(args, rank, world, local_rank):
             t = torch.tensor([dt], device=dev, dtype=torch.float64)
             dist.all_reduce(t, op=dist.ReduceOp.MAX)
             dt = float(t.item())
-        # the PCIe device->host rate of this box (4 GiB pinned copy, best of 3): G's bytes at
-        # that rate are the floor of this path
-        dbuf = torch.empty(1 << 28, dtype=torch.complex128, device=dev)
-        hbuf = torch.empty(1 << 28, dtype=torch.complex128).pin_memory()
-        best = 0.0
-        for _ in range(3):
-            torch.cuda.synchronize()
-            t1 = time.perf_counter()
-            hbuf.copy_(dbuf, non_blocking=True)
-            torch.cuda.synchronize()
-            best = max(best, dbuf.numel() * 16 / (time.perf_counter() - t1) / 1e9)
-        del dbuf, hbuf
+        best = pcie_d2h_gbs(dev)
         d2h_b = 16 * band * n_loc
         e2e = {"value": n_all * l / dt, "unit": UNIT, "ms_per_step": round(dt * 1e3, 2),
                "pcie_d2h_gbs": round(best, 1), "d2h_floor_ms": round(d2h_b / (best * 1e9) * 1e3, 1),
@@ -363,25 +456,51 @@ def run_ours(args, rank, world, local_rank):
             cpu = cpu_baseline_block(cfg, os.cpu_count() or 1)
         except Exception as ex:  # the GPU number stands without it
             cpu = {"error": str(ex)}
+    if rank == 0 and world == 1 and not args.no_traffic:
+        traffic = measure_traffic(args.config, 0)
 
     if rank == 0:
+        roofline = roofline_block(cats, peak, traffic, tflops / world,
+                                  "zgemm_grouped_kernel (DMMA f64), sweep launches (its Gauss-Jordan launches are "
+                                  "listed as gj_gemm)")
         line = {"metric": METRIC, "value": value, "unit": UNIT, "n_gpus": world, "steps": args.steps,
                 "warmup": max(3, args.warmup), "ms_per_step": ms_step, "higher_is_better": True, "scaling": "strong",
                 "vs_baseline": None, "dtype": "c128 (f64)", "data": "synthetic (seeded Dyson generator, "
                 "csrc/dyson_gen.h)",
-                "config": workload_config(cfg, n_all), "solver": "rgf (batched two-ended sweeps)",
+                "config": workload_config(cfg, n_all), "solver": "rgf (batched sweeps; two-ended for w = 1)",
                 "parallelism": f"energy shards x{world}",
                 "energies_per_s": n_all / (ms_step * 1e-3), "tflops_algorithmic": tflops,
-                "gpu_launches": int(launches), "clocks": clocks.summary(), "roofline": roofline,
+                "gpu_launches": int(launches), "clocks": clocks, "roofline": roofline,
                 "e2e": e2e, "cpu_baseline": cpu}
         print(json.dumps(line), flush=True)
 
 
-# ---------------------------------------------------------------------------- DDRGF arm (config 4)
+def pcie_d2h_gbs(dev):
+    """The box's PCIe device->host rate (4 GiB pinned copy, best of 3)."""
+    import torch
+
+    dbuf = torch.empty(1 << 28, dtype=torch.complex128, device=dev)
+    hbuf = torch.empty(1 << 28, dtype=torch.complex128).pin_memory()
+    best = 0.0
+    for _ in range(3):
+        torch.cuda.synchronize()
+        t1 = time.perf_counter()
+        hbuf.copy_(dbuf, non_blocking=True)
+        torch.cuda.synchronize()
+        best = max(best, dbuf.numel() * 16 / (time.perf_counter() - t1) / 1e9)
+    del dbuf, hbuf
+    return best
+
+
+# ---------------------------------------------------------------------------- DDRGF arm (configs 4, 5)
 def run_ddrgf(args, rank, world, local_rank):
-    """Config 4 (l = 4096, b = 256, E = 0.1, one energy): stabilised DDRGF with P domains,
-    contiguous task ranges per rank; the only collective is the all-gather of the
-    per-task interface packets (paper_2605_19910_b200/distributed.py). Strong scaling."""
+    """Configs 4 and 5: stabilised DDRGF of every energy of the config (4: E = 0.1; 5: the 8
+    energies in [-1, 1]), P domains (4: 32, 5: 8, or --domains) sharded over the ranks as
+    contiguous task ranges. Inside the library (bbsi_cuda_ddrgf_rank_dev): phase 1, the
+    NCCL all-gather of the per-task interface packets, phase 2 (redundant on every
+    rank), phase 3 in place, the NCCL all-gather of two halo blocks per rank, the
+    couplings. A rank holds only its band rows; per energy only A's diagonal changes.
+    Strong scaling (fixed work: all energies x all layers)."""
     import torch
     import torch.distributed as dist
 
@@ -394,62 +513,114 @@ def run_ddrgf(args, rank, world, local_rank):
     torch.cuda.set_device(dev)
     cfg = D.CONFIGS[args.config]
     l, b = cfg.num_layers, cfg.block_size
-    P = args.domains or max(32, world)
+    P = args.domains or max(32 if args.config == 4 else 8, world)
     s2 = -(-l // P) - 1
-    tasks = Dd.partition(l, s2)
-    t0, t1 = Dd.task_ranges(len(tasks), world)[rank]
-    L0, L1 = Dd.layer_range(tasks, t0, t1)
-    H = torch.empty((l, 3, b, b), dtype=torch.complex128, device=dev)
-    D.fill_h_device(cfg, H)
-    A = -H[L0:L1].clone()  # this rank's band rows of A = z I - H - Sigma (slot order)
-    del H
-    z = complex(cfg.z()[0])
-    sig = torch.from_numpy(np.asarray(cfg.sigma()[L0:L1], dtype=np.complex128)).to(dev)
-    dg = A[:, 1].diagonal(dim1=-2, dim2=-1)
-    dg.copy_((dg + z) - sig[:, None])  # (z - H_aa) - sigma_a, the order of csrc/band_ops.cu
+    t0, t1, L0, L1 = Dd.rank_layers(l, s2, world, rank)
     stream = torch.cuda.Stream(device=dev)
     torch.cuda.set_stream(stream)
+    A = torch.empty((L1 - L0, 3, b, b), dtype=torch.complex128, device=dev)
+    D.fill_h_rows_device(cfg, A, L0, L1, stream=stream)
+    hd = A[:, 1].diagonal(dim1=-2, dim2=-1).clone()  # H_aa diagonals (real), kept for every energy
+    A.neg_()  # A = -H off the diagonal
+    sig = torch.from_numpy(cfg.sigma()[L0:L1].copy()).to(dev)
+    G = torch.empty_like(A)
+    zs = cfg.z()
+    comm = Dd.NcclComm()
+    diag = A[:, 1].diagonal(dim1=-2, dim2=-1)
+
+    def solve_energy(z):
+        diag.copy_((complex(z) - hd) - sig[:, None])  # (z - h) - sigma: the generator's order
+        Dd.ddrgf_nccl(comm, A, G, l, b, s2)
 
     def step():
-        return Dd.ddrgf_distributed(A, l, b, s2)
-
-    def barrier():
-        if world > 1:
-            dist.barrier()
+        for z in zs:
+            solve_energy(z)
 
     for _ in range(max(3, args.warmup)):
         step()
-    torch.cuda.synchronize()
-    barrier()
-    n0 = L.bbsi_cuda_launch_count()
-    e0, e1 = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
-    with ClockSampler(local_rank) as clocks:
-        e0.record(stream)
-        for _ in range(args.steps):
-            step()
-        e1.record(stream)
-        torch.cuda.synchronize()
-    barrier()
-    ms = e0.elapsed_time(e1)
-    launches = L.bbsi_cuda_launch_count() - n0
-    if world > 1:
-        t = torch.tensor([ms], device=dev, dtype=torch.float64)
-        dist.all_reduce(t, op=dist.ReduceOp.MAX)
-        ms = float(t.item())
+    ms, launches, clocks = timed_loop(step, args.steps, stream, local_rank, world, dev)
     ms_step = ms / args.steps
-    flops = D.algorithmic_flops(cfg)
+    n_e = len(zs)
+    flops_rgf = n_e * D.algorithmic_flops(cfg)
+    tflops = flops_rgf / (ms_step * 1e-3) / 1e12
+    cats = profile_step(L, lambda: solve_energy(zs[0]), one_group=True)
+    executed = sum((c["flops_per_launch"] or 0) * c["launches"] for c in cats.values())
+    peak = L.bbsi_cuda_fp64_peak_tflops(50.0, 5)
+
+    # ---- end to end: host buffers in and out every step (the drop-in bbsi_cuda_ddrgf_z at
+    # N = 1; at N > 1 each rank's rows through pinned memory around the rank entry)
+    e2e = None
+    if not args.no_e2e:
+        Ah = torch.empty(A.shape, dtype=A.dtype).pin_memory()
+        Gh = torch.empty(A.shape, dtype=A.dtype).pin_memory()
+        e2e_energies = zs if args.config == 4 else zs[:1]
+        Ah.copy_(A)
+        hd_h, sig_h = hd.cpu(), sig.cpu()[:, None]
+        dg = Ah[:, 1].diagonal(dim1=-2, dim2=-1)
+
+        def e2e_step():
+            for z in e2e_energies:
+                dg.copy_((complex(z) - hd_h) - sig_h)  # this energy's A in host memory (the input)
+                if world == 1:
+                    from paper_2605_19910_b200 import bbsi as B
+
+                    B.ddrgf_slots(Ah.numpy(), Gh.numpy(), l, b, [s2])
+                else:
+                    A.copy_(Ah, non_blocking=True)
+                    Dd.ddrgf_nccl(comm, A, G, l, b, s2)
+                    Gh.copy_(G, non_blocking=True)
+                    torch.cuda.synchronize()
+
+        e2e_step()
+        torch.cuda.synchronize()
+        if world > 1:
+            dist.barrier()
+        tt = time.perf_counter()
+        for _ in range(args.steps):
+            e2e_step()
+        torch.cuda.synchronize()
+        dt = (time.perf_counter() - tt) / args.steps
+        if world > 1:
+            t = torch.tensor([dt], device=dev, dtype=torch.float64)
+            dist.all_reduce(t, op=dist.ReduceOp.MAX)
+            dt = float(t.item())
+        band_b = 16 * 3 * b * b * l
+        e2e = {"value": len(e2e_energies) * l / dt, "unit": UNIT, "ms_per_step": round(dt * 1e3, 2),
+               "energies_per_step": len(e2e_energies), "h2d_bytes_per_step": band_b * len(e2e_energies),
+               "d2h_bytes_per_step": band_b * len(e2e_energies),
+               "path": ("bbsi_cuda_ddrgf_z (host A in, host G out, pinned)" if world == 1 else
+                        "per rank: pinned host rows -> bbsi_cuda_ddrgf_rank_dev -> pinned host rows")}
+        del Ah, Gh
+
+    cpu = None
+    if rank == 0 and world == 1 and not args.no_cpu_baseline:
+        try:
+            nproc = os.cpu_count() or 1
+            t, nl, sample = cpu_subchain(cfg, nproc, args.config)
+            cpu = {"value": nl / t, "unit": UNIT, "cores": nproc, "kind": "reference", "sample": sample,
+                   "seconds": round(t, 3)}
+        except Exception as ex:
+            cpu = {"error": str(ex)}
+    traffic = None
+    if rank == 0 and world == 1 and not args.no_traffic:
+        traffic = measure_traffic(args.config, P)
+    comm.close()
     if rank == 0:
-        line = {"metric": METRIC, "value": l / (ms_step * 1e-3), "unit": UNIT, "n_gpus": world,
+        roofline = roofline_block(cats, peak, traffic, tflops / world,
+                                  "zgemm_grouped_kernel (DMMA f64): sweep, corner-chain and interface GEMMs of one "
+                                  "energy")
+        roofline["executed_tflop_per_energy"] = round(executed / 1e12, 3)
+        roofline["rgf_equivalent_tflop_per_energy"] = round(D.algorithmic_flops(cfg) / 1e12, 3)
+        line = {"metric": METRIC, "value": n_e * l / (ms_step * 1e-3), "unit": UNIT, "n_gpus": world,
                 "steps": args.steps, "warmup": max(3, args.warmup), "ms_per_step": ms_step,
                 "higher_is_better": True, "scaling": "strong", "vs_baseline": None, "dtype": "c128 (f64)",
                 "data": "synthetic (seeded Dyson generator, csrc/dyson_gen.h)",
-                "config": {"workload": cfg.name, "num_layers": l, "block_size": b, "bandwidth": 1, "energies": 1,
-                           "eta": cfg.eta, "seed": cfg.seed, "solver": "stabilised ddrgf (DESIGN.md section 5)",
-                           "domains": len(tasks), "s2": s2,
-                           "parallelism": f"ddrgf domains over {world} rank(s), NCCL all-gather of the corner packets",
-                           "l2": "inputs larger than L2 (A band 12 GiB)"},
-                "tflops_rgf_equivalent": flops / (ms_step * 1e-3) / 1e12, "gpu_launches": int(launches),
-                "clocks": clocks.summary(), "roofline": None, "e2e": None, "cpu_baseline": None}
+                "config": workload_config(cfg, n_e),
+                "solver": f"stabilised ddrgf, {len(Dd.partition(l, s2))} domains (s2 = {s2}), NCCL inside the library",
+                "parallelism": f"ddrgf domains over {world} rank(s)",
+                "energies_per_s": n_e / (ms_step * 1e-3), "tflops_rgf_equivalent": tflops,
+                "gpu_launches": int(launches), "clocks": clocks, "roofline": roofline, "e2e": e2e,
+                "cpu_baseline": cpu}
         print(json.dumps(line), flush=True)
 
 
@@ -467,7 +638,7 @@ def main():
 
         torch.cuda.set_device(local_rank)
         dist.init_process_group("nccl", device_id=torch.device("cuda", local_rank))
-    if args.config == 4:
+    if args.config in (4, 5):
         run_ddrgf(args, rank, world, local_rank)
     else:
         run_ours(args, rank, world, local_rank)

@@ -175,6 +175,8 @@ int bbsi_cuda_dyson_ddrgf_dev(int l, int bs, const double* dH, const double* z, 
 
 /* Seeded Dyson Hamiltonian (include/.. csrc/dyson_gen.h spec) written on the device. */
 int bbsi_cuda_dyson_fill_h_dev(int l, int w, int b, uint64_t seed, double* dH, void* stream);
+/* Band rows [a0, a1) of the same H (a rank's share of a domain-sharded band). */
+int bbsi_cuda_dyson_fill_h_rows_dev(int l, int w, int b, uint64_t seed, int a0, int a1, double* dH, void* stream);
 /* Same bytes on the host (for the end-to-end path and the parity tests). */
 void bbsi_dyson_fill_h_host(int l, int w, int b, uint64_t seed, double* H);
 /* random_spd_like<std::complex<double>> (block_banded.hpp:99-133, raw mt19937_64 bits,

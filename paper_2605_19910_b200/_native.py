@@ -27,6 +27,7 @@ SIGNATURES = {
     "bbsi_cuda_dyson_rgf_dev": (_i, [_i, _i, _i, _i, _vp, _vp, _vp, _vp, _vp, _vp]),
     "bbsi_cuda_dyson_fill_h_dev": (_i, [_i, _i, _i, C.c_uint64, _vp, _vp]),
     "bbsi_dyson_fill_h_host": (None, [_i, _i, _i, C.c_uint64, _vp]),
+    "bbsi_cuda_dyson_fill_h_rows_dev": (_i, [_i, _i, _i, C.c_uint64, _i, _i, _vp, _vp]),
     "bbsi_random_spd_like_z": (_i, [_i, _i, _i, _vp, C.c_uint64, _d, _vp]),
     "bbsi_cuda_zgemm_dev": (_i, [_i, _i, _i, _vp, _vp, _ll, _ll, _vp, _ll, _ll, _vp, _vp, _ll, _ll, _i, _vp]),
     "bbsi_cuda_zinv_dev": (_i, [_i, _i, _i, _vp, _ll, _ll, _vp, _vp]),

@@ -287,6 +287,21 @@ def ddrgf(m: BlockBandedMatrix, plan: DomainPlan, ngpu: int | None = None):
     return BlockBandedMatrix._from_slots(lay, g), KernelCounters(*map(int, cnt))
 
 
+def ddrgf_slots(A, G, l: int, bs: int, s2_levels, n_threads: int = 1, terminal_threads: int = 1):
+    """ddrgf on raw slot memory (the C ABI's layout, w = 1): A, G complex128 (l, 3, bs, bs),
+    C-contiguous host buffers (pinned for full PCIe rate). Raises like ddrgf()."""
+    for name, x in (("A", A), ("G", G)):
+        if not (isinstance(x, np.ndarray) and x.dtype == np.complex128 and x.shape == (l, 3, bs, bs)
+                and x.flags.c_contiguous):
+            raise InvalidArgumentError(f"{name}: expected a C-contiguous complex128 array of shape {(l, 3, bs, bs)}")
+    s2 = np.array(list(s2_levels), dtype=np.int32)
+    fail = C.c_int(-1)
+    rc = lib().bbsi_cuda_ddrgf_z(l, 1, bs, None, _ptr(A), _ptr(s2), len(s2), n_threads, terminal_threads, _ptr(G),
+                                 None, C.byref(fail))
+    _raise(rc, fail.value)
+    return G
+
+
 def random_spd_like(layout: BlockLayout, seed: int, dominance: float) -> BlockBandedMatrix:
     """block_banded.hpp:99-133 (raw mt19937_64 stream of block_banded.hpp:70-91), generated
     host-side by the C ABI (bbsi_random_spd_like_z) in the reference's draw order."""

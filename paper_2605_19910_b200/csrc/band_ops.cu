@@ -7,15 +7,16 @@ namespace bbsi_gpu {
 
 namespace {
 
-// H slots [l][2w+1][b*b] (b = slot size, blocks fill the whole slot).
-__global__ void dyson_fill_h_kernel(double2* H, int l, int w, int b, uint64_t seedmix) {
+// H slots [rows][2w+1][b*b] for the global layers a0 .. a0+rows-1 of an l-layer band
+// (b = slot size, blocks fill the whole slot).
+__global__ void dyson_fill_h_kernel(double2* H, int l, int w, int b, uint64_t seedmix, int a0, int rows) {
   const long long bb = (long long)b * b;
-  const long long total = (long long)l * (2 * w + 1) * bb;
+  const long long total = (long long)rows * (2 * w + 1) * bb;
   for (long long idx = blockIdx.x * (long long)blockDim.x + threadIdx.x; idx < total;
        idx += (long long)gridDim.x * blockDim.x) {
     long long slot = idx / bb;
     long long e = idx - slot * bb;
-    int a = int(slot / (2 * w + 1));
+    int a = a0 + int(slot / (2 * w + 1));
     int off = int(slot % (2 * w + 1)) - w;
     int i = int(e % b), j = int(e / b);
     double re = 0.0, im = 0.0;
@@ -96,9 +97,14 @@ int grid_for(long long n, int threads) {
 }  // namespace
 
 cudaError_t dyson_fill_h(double2* H, int l, int w, int b, uint64_t seed, cudaStream_t s) {
-  long long total = (long long)l * (2 * w + 1) * b * b;
+  return dyson_fill_h_rows(H, l, w, b, seed, 0, l, s);
+}
+
+cudaError_t dyson_fill_h_rows(double2* H, int l, int w, int b, uint64_t seed, int a0, int a1, cudaStream_t s) {
+  long long total = (long long)(a1 - a0) * (2 * w + 1) * b * b;
+  if (total <= 0) return cudaSuccess;
   ProfScope prof(s, PROF_BAND, 0.0, 16.0 * total);
-  dyson_fill_h_kernel<<<grid_for(total, 256), 256, 0, s>>>(H, l, w, b, bbsi_mix64(seed));
+  dyson_fill_h_kernel<<<grid_for(total, 256), 256, 0, s>>>(H, l, w, b, bbsi_mix64(seed), a0, a1 - a0);
   return cudaGetLastError();
 }
 

@@ -468,6 +468,14 @@ int bbsi_cuda_dyson_fill_h_dev(int l, int w, int b, uint64_t seed, double* dH, v
   return BBSI_OK;
 }
 
+int bbsi_cuda_dyson_fill_h_rows_dev(int l, int w, int b, uint64_t seed, int a0, int a1, double* dH, void* stream) {
+  if (int rc = validate_layout(l, w, b, nullptr)) return rc;
+  if (a0 < 0 || a1 > l || a0 >= a1) return fail(BBSI_INVALID_ARGUMENT, "bad row range");
+  if (int rc = device_ok()) return rc;
+  CK(dyson_fill_h_rows(reinterpret_cast<double2*>(dH), l, w, b, seed, a0, a1, static_cast<cudaStream_t>(stream)));
+  return BBSI_OK;
+}
+
 void bbsi_dyson_fill_h_host(int l, int w, int b, uint64_t seed, double* H) {
   const uint64_t sm = bbsi_mix64(seed);
   const long long bb = (long long)b * b;
@@ -1034,18 +1042,31 @@ int bbsi_cuda_ddrgf_z(int l, int w, int bs, const int* sizes, const double* A, c
   if (int rc = device_ok()) return rc;
   HostBand h = make_host(l, w, bs, sizes, A);
   const int bp = pad64(h.bs);
+  bool direct = bp == h.bs;  // uniform blocks filling their slots: copy the caller's buffers as they are
+  for (int a = 0; direct && a < l; ++a) direct = h.sz[a] == bs;
   std::vector<double2> staging;
-  pad_band(h, bp, staging);
-  const size_t bytes = staging.size() * sizeof(double2);
+  if (!direct) pad_band(h, bp, staging);
+  const size_t bytes = size_t(l) * 3 * bp * bp * sizeof(double2);
   double2* dA = static_cast<double2*>(arena_get(0, bytes));
   double2* dG = static_cast<double2*>(arena_get(10, bytes));
   if (!dA || !dG) return fail(BBSI_OUT_OF_MEMORY, "band allocation failed");
   cudaStream_t s = thread_stream(0);
-  CK(cudaMemcpyAsync(dA, staging.data(), bytes, cudaMemcpyHostToDevice, s));
+  CK(cudaMemcpyAsync(dA, direct ? static_cast<const void*>(A) : staging.data(), bytes, cudaMemcpyHostToDevice, s));
+  if (direct) {  // out-of-band slots are ignored on input
+    CK(cudaMemsetAsync(dA, 0, size_t(bp) * bp * sizeof(double2), s));
+    CK(cudaMemsetAsync(dA + (size_t(l - 1) * 3 + 2) * bp * bp, 0, size_t(bp) * bp * sizeof(double2), s));
+  }
   if (int rc = ddrgf_on_device(dA, dG, l, bp, h.sz, s2_levels[0], fail_layer, s)) return rc;
-  CK(cudaMemcpyAsync(staging.data(), dG, bytes, cudaMemcpyDeviceToHost, s));
-  CK(cudaStreamSynchronize(s));
-  unpad_band(staging, bp, h, reinterpret_cast<double2*>(G));
+  if (direct) {
+    CK(cudaMemcpyAsync(G, dG, bytes, cudaMemcpyDeviceToHost, s));
+    CK(cudaStreamSynchronize(s));
+    std::memset(G, 0, size_t(bp) * bp * sizeof(double2));  // out-of-band slots zero-filled on output
+    std::memset(G + 2 * (size_t(l - 1) * 3 + 2) * bp * bp, 0, size_t(bp) * bp * sizeof(double2));
+  } else {
+    CK(cudaMemcpyAsync(staging.data(), dG, bytes, cudaMemcpyDeviceToHost, s));
+    CK(cudaStreamSynchronize(s));
+    unpad_band(staging, bp, h, reinterpret_cast<double2*>(G));
+  }
   if (counters) ddrgf_reference_counters(l, s2_levels, n_levels, counters);
   return BBSI_OK;
 }

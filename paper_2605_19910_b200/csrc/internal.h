@@ -16,6 +16,23 @@ namespace bbsi_gpu {
 
 // kernels
 cudaError_t zgemm_grouped(ZGemmGroup& g, cudaStream_t stream);
+// TMA-staged sweep GEMM (zgemm_tma.cu): used by zgemm_grouped when every operand A / B is
+// a view of a registered buffer; *done = false -> not applicable.
+cudaError_t zgemm_tma_try(const ZGemmGroup& g, cudaStream_t stream, bool* done);
+// Registers [base, base + bytes) of bs x bs slots for TMA operands (per host thread,
+// scoped: tma_unregister(n) drops the n most recent registrations; env BBSI_TMA=0 off).
+void tma_register(const void* base, size_t bytes, int bs);
+void tma_unregister(int n);
+struct TmaScope {
+  int n = 0;
+  void add(const void* base, size_t bytes, int bs) {
+    if (base && bytes) {
+      tma_register(base, bytes, bs);
+      ++n;
+    }
+  }
+  ~TmaScope() { tma_unregister(n); }
+};
 // In-place batched inverse (blocked Gauss-Jordan, partial pivoting); scratch of
 // zinv_scratch_bytes(n, batch) bytes; status[b] = -1 or the first negligible pivot.
 cudaError_t zinv_batched(double2* M, long long ld, long long bstride, int n, int n_true, int batch, void* scratch,
@@ -26,6 +43,8 @@ cudaError_t zinv_batched2(double2* M, long long ld, long long bstride, int n, in
                           long long ostride, void* scratch, int* status, long long sostride, cudaStream_t stream);
 size_t zinv_scratch_bytes(int n, int batch);
 cudaError_t dyson_fill_h(double2* H, int l, int w, int b, uint64_t seed, cudaStream_t s);
+// Rows [a0, a1) of the same band into H ([a1-a0][2w+1][b][b], local row 0 = layer a0).
+cudaError_t dyson_fill_h_rows(double2* H, int l, int w, int b, uint64_t seed, int a0, int a1, cudaStream_t s);
 // Diagonal blocks only (A_aa = z I - H_aa - sigma_a I) plus zeroed out-of-range slots,
 // for sweeps that read the off-diagonal blocks from H (SweepWork::Hoff).
 cudaError_t dyson_form_diag(double2* G, const double2* H, int l, int w, int bs, int batch, const double2* z,

@@ -562,6 +562,17 @@ StreamPool& pool_for(int n) {
 }  // namespace
 
 cudaError_t rgf_sweeps(const SweepWork& W, const int* n_true, cudaStream_t s) {
+  // the buffers every sweep GEMM operand lives in, for the TMA-staged GEMM
+  TmaScope tma;
+  {
+    const size_t bb16 = size_t(W.bs) * W.bs * sizeof(double2);
+    const size_t band = size_t(W.l) * (2 * W.w + 1) * bb16;
+    tma.add(W.G, size_t(W.batch - 1) * W.g_bstride * sizeof(double2) + band, W.bs);
+    const size_t lmb = size_t(W.batch) * (W.lm_layers > 0 ? W.lm_layers : W.l) * W.w * bb16;
+    tma.add(W.LM, lmb, W.bs);
+    tma.add(W.UM, lmb, W.bs);
+    if (W.Hoff) tma.add(W.Hoff, band, W.bs);
+  }
   const int G = W.groups < 1 ? 1 : (W.groups > W.batch ? W.batch : W.groups);
   const int sstride = W.status_stride > 0 ? W.status_stride : W.batch;
   // dense middle window of the banded two-ended sweep: one scratch per stream group

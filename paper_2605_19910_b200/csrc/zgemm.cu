@@ -364,6 +364,10 @@ cudaError_t zgemm_grouped(ZGemmGroup& g, cudaStream_t stream) {
   }
   ProfScope prof(stream, g.prof_cat ? g.prof_cat : PROF_GEMM, fl, by);
   cudaError_t e;
+  if (!plain) {
+    bool done = false;
+    if ((e = zgemm_tma_try(g, stream, &done)) || done) return e ? e : cudaGetLastError();
+  }
   const bool three = gemm_minb() == 3;  // (2 CTAs/SM for the GJ updates alone: 130 vs 121 ms)
   bool amax = false, cform = false;
   for (int p = 0; p < g.nprob; ++p) {
