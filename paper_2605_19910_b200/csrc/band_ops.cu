@@ -165,4 +165,34 @@ cudaError_t band_window(double2* G, long long gstride, double2* D, int a0, int w
   return cudaGetLastError();
 }
 
+namespace {
+__global__ void diag_shift_kernel(double2* M, int n, long long stride, int batch) {
+  const int b = blockIdx.y;
+  if (b >= batch) return;
+  double2* m = M + (long long)b * stride;
+  for (int i = blockIdx.x * blockDim.x + threadIdx.x; i < n; i += gridDim.x * blockDim.x) {
+    double2 x = m[(long long)i * n + i];
+    m[(long long)i * n + i] = make_double2(x.x + 1.0, x.y);
+  }
+}
+__global__ void axpy1_kernel(double2* y, const double2* x, long long n) {
+  for (long long i = blockIdx.x * (long long)blockDim.x + threadIdx.x; i < n; i += (long long)gridDim.x * blockDim.x)
+    y[i] = make_double2(y[i].x + x[i].x, y[i].y + x[i].y);
+}
+}  // namespace
+
+// M_b += I for batch matrices n x n (ld n) at M + b*stride
+cudaError_t diag_shift_batched(double2* M, int n, long long stride, int batch, cudaStream_t s) {
+  ProfScope prof(s, PROF_BAND, 0.0, 32.0 * n * batch);
+  diag_shift_kernel<<<dim3((n + 255) / 256, batch), 256, 0, s>>>(M, n, stride, batch);
+  return cudaGetLastError();
+}
+
+// y += x over n complex entries
+cudaError_t axpy_batched(double2* y, const double2* x, long long n, cudaStream_t s) {
+  ProfScope prof(s, PROF_BAND, 2.0 * n, 48.0 * n);
+  axpy1_kernel<<<grid_for(n, 256), 256, 0, s>>>(y, x, n);
+  return cudaGetLastError();
+}
+
 }  // namespace bbsi_gpu

@@ -468,8 +468,8 @@ cudaError_t ddrgf_phase2(const double2* packets, int l, int b, const int* n_true
   for (int t = 0; t < T; ++t) offs.push_back(pk(t, PASS) - packets);
   std::vector<double> gam;
   if ((e = task_gammas(packets, offs, b, gamma0, gam, s))) return e;
-  // scratch: 8 temporaries per stream
-  constexpr int NT = 8;
+  // scratch: 10 temporaries per stream (Tm(8), Tm(9): the inverse refinement)
+  constexpr int NT = 10;
   double2* scr = static_cast<double2*>(arena_get(13, size_t(2 * NT) * bb * sizeof(double2)));
   const int max_inv = 6 * T + 4;
   void* inv_scr = arena_get(7, zinv_scratch_bytes(b, 1) + 256);
@@ -479,6 +479,10 @@ cudaError_t ddrgf_phase2(const double2* packets, int l, int b, const int* n_true
   SideStream& side = side_stream();
   std::vector<int> st_layer;
   st_layer.reserve(max_inv);
+  const bool refine = [] {  // read per call: tools/ddrgf_diag.py compares both
+    const char* ev = getenv("BBSI_DDRGF_REFINE");
+    return !(ev && atoi(ev) == 0);
+  }();
   struct Ops {
     cudaStream_t s;
     double2* tm0;
@@ -488,11 +492,23 @@ cudaError_t ddrgf_phase2(const double2* packets, int l, int b, const int* n_true
   };
   const Ops L{s, scr, inv_scr, bb};
   const Ops R{side.s, scr + (size_t)NT * bb, inv_scr2, bb};
+  // b x b inverse in place, then one Newton-Schulz step X <- X + X (I - M X): the
+  // interface quantities feed every later separator, so their inverses are refined to
+  // working accuracy (env BBSI_DDRGF_REFINE=0: off)
   auto inv = [&](const Ops& q, double2* m, int layer) -> cudaError_t {
     if (int(st_layer.size()) >= max_inv) return cudaErrorInvalidValue;
     int* slot = st + st_layer.size();
     st_layer.push_back(layer);
-    return zinv_batched(m, b, bb, b, n_true ? n_true[layer] : b, 1, q.iscr, slot, q.s);
+    cudaError_t e2;
+    if (refine && (e2 = cudaMemcpyAsync(q.Tm(8), m, bb * sizeof(double2), cudaMemcpyDeviceToDevice, q.s))) return e2;
+    if ((e2 = zinv_batched(m, b, bb, b, n_true ? n_true[layer] : b, 1, q.iscr, slot, q.s))) return e2;
+    if (!refine) return cudaSuccess;
+    // R = I - M X  (into Tm(9));  Tm(8) = X R;  X += Tm(8)
+    if ((e2 = cudaMemsetAsync(q.Tm(9), 0, bb * sizeof(double2), q.s))) return e2;
+    if ((e2 = diag_add(q.Tm(9), 0, b, 1, make_double2(1.0, 0.0), q.s))) return e2;
+    if ((e2 = mm(b, 1, -1.0, blk(q.Tm(8), b), blk(m, b), 1.0, blk(q.Tm(9), b), q.s))) return e2;
+    if ((e2 = mm(b, 1, 1.0, blk(m, b), blk(q.Tm(9), b), 0.0, blk(q.Tm(8), b), q.s))) return e2;
+    return axpy(m, q.Tm(8), bb, make_double2(1.0, 0.0), q.s);
   };
   auto ident = [&](const Ops& q, double2* m) -> cudaError_t {
     cudaError_t e2 = cudaMemsetAsync(m, 0, bb * sizeof(double2), q.s);

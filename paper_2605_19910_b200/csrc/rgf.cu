@@ -100,7 +100,18 @@ bool refine_multipliers_default() {
 }
 
 namespace {
-bool refine_ok(int l, int w, bool two_ended) { return w >= 2 && !two_ended_ok(two_ended, l, w) && refine_multipliers_default(); }
+bool refine_ok(int l, int w, bool two_ended) {
+  (void)l;
+  (void)two_ended;
+  return w >= 2 && refine_multipliers_default();
+}
+// pivot copies of one stream group (complex elements): one-ended f_j [batch]; two-ended
+// f_jR, f_jL [2][batch] plus the dense middle window [batch][(w b)^2]
+long long fcopy_elems(int l, int w, int bs, int batch_g, bool two_ended) {
+  const long long bb = (long long)bs * bs;
+  if (two_ended_ok(two_ended, l, w) && w >= 2) return 2LL * batch_g * bb + (long long)batch_g * w * w * bb;
+  return (long long)batch_g * bb;
+}
 }  // namespace
 
 
@@ -112,7 +123,9 @@ size_t sweep_scratch_bytes(int l, int w, int bs, int batch, int groups, bool two
   s += size_t(groups) * (zinv_scratch_bytes(bs, chains * ((batch + groups - 1) / groups)) + 256);  // inversion scratch
   s += size_t(l) * batch * sizeof(int) + 256;             // status
   if (chains == 2 && w >= 2) s += size_t(groups) * mid_bytes(w, bs, (batch + groups - 1) / groups);  // dense middle
-  if (refine_ok(l, w, two_ended)) s += size_t(batch) * bb + 256;  // pivot copies for the refinement
+  if (refine_ok(l, w, two_ended))  // pivot copies for the refinement, per group
+    s += size_t(groups) * size_t(fcopy_elems(l, w, bs, (batch + groups - 1) / groups, two_ended)) * sizeof(double2) +
+         256;
   return s;
 }
 
@@ -130,6 +143,7 @@ void sweep_carve(SweepWork& W, void* base) {
   p += size_t(W.l) * W.batch * sizeof(int);
   p = reinterpret_cast<char*>((reinterpret_cast<uintptr_t>(p) + 255) & ~uintptr_t(255));  // (+256 slack sized)
   W.mid = (use_two_ended(W) && W.w >= 2) ? p : nullptr;
+  if (W.mid) p += size_t(W.groups) * mid_bytes(W.w, W.bs, gs);
   W.fcopy = (!W.Hoff && refine_ok(W.l, W.w, W.two_ended)) ? reinterpret_cast<double2*>(p) : nullptr;
 }
 
@@ -425,10 +439,23 @@ cudaError_t rgf_sweeps_two_w(const SweepWork& W, const int* n_true, int* status,
     return zinv_batched2(mR, b, W.g_bstride, b, n_true[jR], W.batch, 2, (long long)(c.slot(jL, 0) - mR), W.inv,
                          status + (long long)jR * status_stride, (long long)(jL - jR) * status_stride, s);
   };
+  // refinement of the multipliers (see refine_multipliers_default): pivot copies of
+  // both chains and of the dense middle window
+  const bool refine = W.fcopy != nullptr;
+  double2* FR = W.fcopy;
+  double2* FL = refine ? W.fcopy + (long long)W.batch * c.bb : nullptr;
+  double2* D0 = refine ? W.fcopy + 2LL * W.batch * c.bb : nullptr;
+  const ZOp opFR{FR, b, 0, 0, c.bb}, opFL{FL, b, 0, 0, c.bb};
+  auto save = [&](double2* dst, int j) {
+    return cudaMemcpy2DAsync(dst, c.bb * sizeof(double2), c.slot(j, 0), W.g_bstride * sizeof(double2),
+                             c.bb * sizeof(double2), W.batch, cudaMemcpyDeviceToDevice, s);
+  };
   // ---------------- inward chains
   const int nup = nR > nL ? nR : nL;
   for (int t = 0; t < nup; ++t) {
     const int jR = t < nR ? l - 1 - t : -1, jL = t < nL ? t : -1;
+    if (refine && jR >= 0 && (e = save(FR, jR)) != cudaSuccess) return e;
+    if (refine && jL >= 0 && (e = save(FL, jL)) != cudaSuccess) return e;
     if ((e = inv2(jR, jL)) != cudaSuccess) return e;
     ZGemmProblem p1[2], pR[2], pL[2];
     int n1 = 0;
@@ -447,6 +474,22 @@ cudaError_t rgf_sweeps_two_w(const SweepWork& W, const int* n_true, int* status,
       pL[1] = prob(kb, b, b, 1.0, 0.0, lower, c.gop(c.slot(jL, 0), 0, 0), c.mop(c.um(jL), 1, 0));
     }
     if ((e = grp(p1, n1)) != cudaSuccess) return e;
+    if (refine) {  // R = M'(row) - f lm (in place in the row, not read again); lm += X R
+      ZGemmProblem r1[2], r2[2];
+      int nr = 0;
+      if (jR >= 0) {
+        const ZOp row = c.gop(c.slot(jR, -1), 0, -1);
+        r1[nr] = prob(b, kb, b, -1.0, 1.0, opFR, c.mop(c.lm(jR), 0, 1), row);
+        r2[nr++] = prob(b, kb, b, 1.0, 1.0, c.gop(c.slot(jR, 0), 0, 0), row, c.mop(c.lm(jR), 0, 1));
+      }
+      if (jL >= 0) {
+        const ZOp row = c.gop(c.slot(jL, +1), 0, +1);
+        r1[nr] = prob(b, kb, b, -1.0, 1.0, opFL, c.mop(c.lm(jL), 0, 1), row);
+        r2[nr++] = prob(b, kb, b, 1.0, 1.0, c.gop(c.slot(jL, 0), 0, 0), row, c.mop(c.lm(jL), 0, 1));
+      }
+      if ((e = grp(r1, nr)) != cudaSuccess) return e;
+      if ((e = grp(r2, nr)) != cudaSuccess) return e;
+    }
     // windows: right rows/cols [jR-w, jR-1], left [jL+1, jL+w]; disjoint -> one launch
     if (jR >= 0 && jL >= 0 && jR - w > jL + w) {
       ZGemmProblem p2[4] = {pR[0], pR[1], pL[0], pL[1]};
@@ -454,6 +497,22 @@ cudaError_t rgf_sweeps_two_w(const SweepWork& W, const int* n_true, int* status,
     } else {
       if (jR >= 0 && (e = grp(pR, 2)) != cudaSuccess) return e;
       if (jL >= 0 && (e = grp(pL, 2)) != cudaSuccess) return e;
+    }
+    if (refine) {  // R = M'(column) - um f (in place, not read again); um += R X
+      ZGemmProblem r1[2], r2[2];
+      int nr = 0;
+      if (jR >= 0) {
+        const ZOp col = c.gop(c.slot(jR - 1, +1), -two_w, 0);
+        r1[nr] = prob(kb, b, b, -1.0, 1.0, c.mop(c.um(jR), 1, 0), opFR, col);
+        r2[nr++] = prob(kb, b, b, 1.0, 1.0, col, c.gop(c.slot(jR, 0), 0, 0), c.mop(c.um(jR), 1, 0));
+      }
+      if (jL >= 0) {
+        const ZOp col = c.gop(c.slot(jL + 1, -1), two_w, 0);
+        r1[nr] = prob(kb, b, b, -1.0, 1.0, c.mop(c.um(jL), 1, 0), opFL, col);
+        r2[nr++] = prob(kb, b, b, 1.0, 1.0, col, c.gop(c.slot(jL, 0), 0, 0), c.mop(c.um(jL), 1, 0));
+      }
+      if ((e = grp(r1, nr)) != cudaSuccess) return e;
+      if ((e = grp(r2, nr)) != cudaSuccess) return e;
     }
   }
   // ---------------- the w middle layers: their (w b) x (w b) Schur complement inverted as
@@ -466,8 +525,38 @@ cudaError_t rgf_sweeps_two_w(const SweepWork& W, const int* n_true, int* status,
     double2* D = static_cast<double2*>(W.mid);
     void* zs = static_cast<char*>(W.mid) + mid_dense_bytes(w, b, W.batch);
     if ((e = band_window(W.G, W.g_bstride, D, m, w, b, W.batch, true, s)) != cudaSuccess) return e;
+    if (refine && (e = cudaMemcpyAsync(D0, D, sizeof(double2) * size_t(wb2) * W.batch, cudaMemcpyDeviceToDevice, s)))
+      return e;
     if ((e = zinv_batched(D, kb, wb2, kb, kb, W.batch, zs, status + (long long)m * status_stride, s)) != cudaSuccess)
       return e;
+    if (refine) {  // Newton-Schulz: X += X (I - D0 X); D0 <- I - D0 X in place, then the update
+      ZGemmGroup g{};
+      g.batch = W.batch;
+      g.bs = kb;
+      g.nprob = 1;
+      ZGemmProblem& q = g.prob[0];
+      q.M = q.N = q.K = kb;
+      // D0 <- -D0 X (beta 0), then + I on its diagonal
+      q.alpha = make_double2(-1.0, 0.0);
+      q.beta = make_double2(0.0, 0.0);
+      q.A = ZOp{D0, kb, 0, 0, wb2};
+      q.B = ZOp{D, kb, 0, 0, wb2};
+      q.C = q.D = ZOp{D0 + 0, kb, 0, 0, wb2};
+      // the product may not overwrite its own A operand tile by tile: go through the
+      // multiplier scratch of layer m (free at this point: >= kb*kb per batch entry)
+      double2* T = c.lm(m);
+      const long long tstride = c.lm_bstride();
+      q.C = q.D = ZOp{T, kb, 0, 0, tstride};
+      if ((e = zgemm_grouped(g, s)) != cudaSuccess) return e;
+      if ((e = diag_shift_batched(T, kb, tstride, W.batch, s)) != cudaSuccess) return e;
+      // D0 <- X R, then X += D0
+      q.alpha = make_double2(1.0, 0.0);
+      q.A = ZOp{D, kb, 0, 0, wb2};
+      q.B = ZOp{T, kb, 0, 0, tstride};
+      q.C = q.D = ZOp{D0, kb, 0, 0, wb2};
+      if ((e = zgemm_grouped(g, s)) != cudaSuccess) return e;
+      if ((e = axpy_batched(D, D0, wb2 * W.batch, s)) != cudaSuccess) return e;
+    }
     if ((e = band_window(W.G, W.g_bstride, D, m, w, b, W.batch, false, s)) != cudaSuccess) return e;
     // layers m+1 .. m+w-1 have no pivot of their own here: status -1 (0xff bytes)
     if ((e = cudaMemset2DAsync(status + (long long)(m + 1) * status_stride, sizeof(int) * size_t(status_stride), 0xff,
@@ -604,7 +693,7 @@ cudaError_t rgf_sweeps(const SweepWork& W, const int* n_true, cudaStream_t s) {
     Wg.inv = static_cast<char*>(W.inv) + size_t(g) * inv_b;
     Wg.e_off = W.e_off + e0;
     if (W.zdev) Wg.zdev = W.zdev + e0;
-    if (W.fcopy) Wg.fcopy = W.fcopy + (long long)e0 * bb;
+    if (W.fcopy) Wg.fcopy = W.fcopy + (long long)g * fcopy_elems(W.l, W.w, W.bs, gs, W.two_ended);
     if ((e = cudaStreamWaitEvent(P.s[g], P.ev[G], 0))) return e;
     if ((e = sweep(Wg, W.status + e0, P.s[g], g))) return e;
     if ((e = cudaEventRecord(P.ev[g], P.s[g]))) return e;

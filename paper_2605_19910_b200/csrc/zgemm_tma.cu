@@ -2,11 +2,11 @@
 //
 // Same contract as zgemm_grouped (zgemm.cu, the reference's gemm_into,
 // kernels.hpp:102-117): grouped, batched, block-strided complex-FP64 products
-// D = alpha A B + beta C. Here one producer warp streams the A and B tiles into a
-// ring of shared-memory stages with cp.async.bulk.tensor (TMA) and mbarrier
-// transaction counts, and four consumer warps only issue DMMA (mma.sync m8n8k4
-// f64) and their C / D traffic: no address arithmetic or cp.async issue in the
-// math warps.
+// D = alpha A B + beta C. One elected thread streams the A and B tiles into a ring
+// of shared-memory stages with cp.async.bulk.tensor (TMA) and mbarrier transaction
+// counts (a stage is refilled as soon as all four warps have arrived on its "empty"
+// barrier); the four warps only issue DMMA (mma.sync m8n8k4 f64) and their C / D
+// traffic: no per-thread cp.async address arithmetic or issue.
 //
 // Tensor maps. Operands are views of bs x bs slots of a few device buffers (the band,
 // the multiplier arrays, the shared H); each registered buffer (tma_register) gets one
@@ -92,7 +92,7 @@ __device__ __forceinline__ int pi8(int r) { return ((r & 1) << 2) | (r >> 1); }
 __device__ __forceinline__ int swz(int row, int chunk) { return row * 8 + (chunk ^ (row & 7)); }
 
 template <int STAGES, bool CFORM>
-__global__ void __maxnreg__(200)
+__global__ void __launch_bounds__(128, STAGES == 2 ? 3 : 2)
     zgemm_tma_kernel(const __grid_constant__ ZGemmGroup g, const __grid_constant__ TmaParams tp) {
   extern __shared__ __align__(1024) unsigned char tsm_raw[];
   // 1024-byte alignment of the stages (128-byte swizzle atoms)
@@ -126,30 +126,28 @@ __global__ void __maxnreg__(200)
   }
   __syncthreads();
 
-  if (warp == 4) {  // ---------------- producer: TMA
-    if (lane == 0) {
-      const TmaOp& oa = tp.a[pi];
-      const TmaOp& ob = tp.b[pi];
-      const CUtensorMap* ma = &tp.maps[oa.map];
-      const CUtensorMap* mb = &tp.maps[ob.map];
-      asm volatile("prefetch.tensormap [%0];\n" ::"l"(reinterpret_cast<uint64_t>(ma)) : "memory");
-      asm volatile("prefetch.tensormap [%0];\n" ::"l"(reinterpret_cast<uint64_t>(mb)) : "memory");
-      const long long abase = oa.slot0 + (long long)batch * oa.bst + (long long)(m0 / bs) * oa.rs;
-      const long long bbase = ob.slot0 + (long long)batch * ob.bst + (long long)(n0 / bs) * ob.cs;
-      const int am = (m0 % bs) / 8, bn = n0 % bs;
-      for (int kc = 0; kc < nk; ++kc) {
-        const int s = kc % STAGES;
-        const unsigned ph = (kc / STAGES) & 1;
-        if (kc >= STAGES) mbar_wait(&empty[s], ph ^ 1);
-        mbar_expect_tx(&full[s], TSTAGE_BYTES);
-        const int k0 = kc * TBK;
-        double2* As = stages + s * (TSTAGE_A + TSTAGE_B);
-        double2* Bs = As + TSTAGE_A;
-        tma_load_4d(As, ma, 0, k0 % bs, am, int(abase + (long long)(k0 / bs) * oa.cs), &full[s]);
-        tma_load_4d(Bs, mb, 0, bn, (k0 % bs) / 8, int(bbase + (long long)(k0 / bs) * ob.rs), &full[s]);
-      }
-    }
-    return;
+  // ---------------- TMA issue (one elected thread of warp 0; no separate producer warp,
+  // so the CTA keeps 128 threads and the register budget of 3 CTAs per SM)
+  const TmaOp& oa = tp.a[pi];
+  const TmaOp& ob = tp.b[pi];
+  const CUtensorMap* ma = &tp.maps[oa.map];
+  const CUtensorMap* mb = &tp.maps[ob.map];
+  const long long abase = oa.slot0 + (long long)batch * oa.bst + (long long)(m0 / bs) * oa.rs;
+  const long long bbase = ob.slot0 + (long long)batch * ob.bst + (long long)(n0 / bs) * ob.cs;
+  const int am = (m0 % bs) / 8, bn = n0 % bs;
+  auto issue = [&](int kc) {
+    const int s = kc % STAGES;
+    mbar_expect_tx(&full[s], TSTAGE_BYTES);
+    const int k0 = kc * TBK;
+    double2* As = stages + s * (TSTAGE_A + TSTAGE_B);
+    double2* Bs = As + TSTAGE_A;
+    tma_load_4d(As, ma, 0, k0 % bs, am, int(abase + (long long)(k0 / bs) * oa.cs), &full[s]);
+    tma_load_4d(Bs, mb, 0, bn, (k0 % bs) / 8, int(bbase + (long long)(k0 / bs) * ob.rs), &full[s]);
+  };
+  if (threadIdx.x == 0) {
+    asm volatile("prefetch.tensormap [%0];\n" ::"l"(reinterpret_cast<uint64_t>(ma)) : "memory");
+    asm volatile("prefetch.tensormap [%0];\n" ::"l"(reinterpret_cast<uint64_t>(mb)) : "memory");
+    for (int kc = 0; kc < STAGES && kc < nk; ++kc) issue(kc);
   }
 
   // ---------------- consumers: 4 warps of 32 x 32
@@ -165,7 +163,8 @@ __global__ void __maxnreg__(200)
   if (c_in_acc) {
     const double2* __restrict__ ct = P.C.p + (long long)batch * P.C.bstride + zop_offset(P.C, bs, m0, n0);
     const double sg = P.alpha.x;
-    double2 cv[4][4][2];
+    const double2 z = (CFORM && P.cz) ? P.cz[batch] : make_double2(0.0, 0.0);
+    const double2 sgm = (CFORM && P.cz) ? *P.csig : make_double2(0.0, 0.0);
 #pragma unroll
     for (int mi = 0; mi < 4; ++mi)
 #pragma unroll
@@ -173,29 +172,11 @@ __global__ void __maxnreg__(200)
 #pragma unroll
         for (int q = 0; q < 2; ++q) {
           const int m = wm + mi * 8 + pr, n = wn + ni * 8 + (q ? pc1 : pc0);
-          cv[mi][ni][q] = ct[(long long)n * P.C.ld + m];
-        }
-    if (CFORM && P.cz) {  // the Dyson diagonal block from H (see ZGemmProblem::cz)
-      const double2 z = P.cz[batch], sgm = *P.csig;
-#pragma unroll
-      for (int mi = 0; mi < 4; ++mi)
-#pragma unroll
-        for (int ni = 0; ni < 4; ++ni)
-#pragma unroll
-          for (int q = 0; q < 2; ++q) {
-            const double2 h = cv[mi][ni][q];
-            const bool dg = m0 + wm + mi * 8 + pr == n0 + wn + ni * 8 + (q ? pc1 : pc0);
-            cv[mi][ni][q] = dg ? make_double2((z.x - h.x) - sgm.x, (z.y - h.y) - sgm.y) : make_double2(-h.x, -h.y);
-          }
-    }
-#pragma unroll
-    for (int mi = 0; mi < 4; ++mi)
-#pragma unroll
-      for (int ni = 0; ni < 4; ++ni)
-#pragma unroll
-        for (int q = 0; q < 2; ++q) {
-          cr[mi][ni][q] = sg * cv[mi][ni][q].x;
-          ci[mi][ni][q] = sg * cv[mi][ni][q].y;
+          double2 v = ct[(long long)n * P.C.ld + m];
+          if (CFORM && P.cz)  // the Dyson diagonal block from H (see ZGemmProblem::cz)
+            v = (m0 + m == n0 + n) ? make_double2((z.x - v.x) - sgm.x, (z.y - v.y) - sgm.y) : make_double2(-v.x, -v.y);
+          cr[mi][ni][q] = sg * v.x;
+          ci[mi][ni][q] = sg * v.y;
         }
   } else {
 #pragma unroll
@@ -248,6 +229,10 @@ __global__ void __maxnreg__(200)
     }
     __syncwarp();
     if (lane == 0) mbar_arrive(&empty[s]);
+    if (threadIdx.x == 0 && kc + STAGES < nk) {  // refill this stage once all 4 warps left it
+      mbar_wait(&empty[s], (kc / STAGES) & 1);
+      issue(kc + STAGES);
+    }
   }
 
   // ---- epilogue (full tiles only on this path)
@@ -333,8 +318,8 @@ bool tma_enabled() {  // read per call (tests compare BBSI_TMA=0 / 1 in one proc
 int tma_stages() {
   static const int s = [] {
     const char* e = getenv("BBSI_TMA_STAGES");
-    const int v = e ? atoi(e) : 3;
-    return v == 2 || v == 4 ? v : 3;
+    const int v = e ? atoi(e) : 2;
+    return v == 3 || v == 4 ? v : 2;
   }();
   return s;
 }
@@ -462,7 +447,7 @@ cudaError_t zgemm_tma_try(const ZGemmGroup& g, cudaStream_t stream, bool* done) 
     fn = cform ? (const void*)zgemm_tma_kernel<3, true> : (const void*)zgemm_tma_kernel<3, false>;
   if ((e = set_max_dyn_smem(fn, smem, true))) return e;
   void* args[2] = {const_cast<ZGemmGroup*>(&g), &tp};
-  if ((e = cudaLaunchKernel(fn, dim3(g.total_tiles), dim3(160), args, smem, stream))) return e;
+  if ((e = cudaLaunchKernel(fn, dim3(g.total_tiles), dim3(128), args, smem, stream))) return e;
   *done = true;
   return cudaSuccess;
 }

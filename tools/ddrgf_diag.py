@@ -43,6 +43,7 @@ def main():
     p.add_argument("--block", type=int, default=256)
     p.add_argument("--domains", type=int, nargs="+", default=[2, 8, 32])
     p.add_argument("--gammas", type=float, nargs="+", default=[1.0])
+    p.add_argument("--refine", type=int, nargs="+", default=[1], help="BBSI_DDRGF_REFINE values to compare")
     a = p.parse_args()
     cfg = D.scaled(D.CONFIGS[4], num_layers=a.layers, block_size=a.block)
     l, b = cfg.num_layers, cfg.block_size
@@ -60,8 +61,9 @@ def main():
     for P in a.domains:
         s2 = -(-l // P) - 1
         near = rows_near_interfaces(l, s2)
-        for g in a.gammas:
+        for g, rf in [(g, rf) for g in a.gammas for rf in a.refine]:
             os.environ["BBSI_DDRGF_GAMMA"] = str(g)
+            os.environ["BBSI_DDRGF_REFINE"] = str(rf)
             D.solve_ddrgf_device(cfg, H, Gd, s2)
             torch.cuda.synchronize()
             Sg = Gd.cpu().numpy()
@@ -69,7 +71,7 @@ def main():
             r = PF.residual_rows(SA, Sg, 1)
             er = np.nanmax(e, axis=1)
             wr = int(np.nanargmax(er))
-            print(f"P={P:3d} gamma={g:g}: max {np.nanmax(e):.3e} (interface rows {er[near].max():.3e}, interior "
+            print(f"P={P:3d} gamma={g:g} refine={rf}: max {np.nanmax(e):.3e} (interface rows {er[near].max():.3e}, interior "
                   f"{er[~near].max():.3e}, worst row {wr}) | residual interface {r[near].max():.2e} interior "
                   f"{r[~near].max():.2e} worst row {int(np.argmax(r))}", flush=True)
     os.environ.pop("BBSI_DDRGF_GAMMA", None)
