@@ -10,7 +10,7 @@ PKG = Path(__file__).resolve().parent
 CSRC = PKG / "csrc"
 LIB_DIR = PKG / "_lib"
 LIB = LIB_DIR / "libbbsi_cuda.so"
-SOURCES = ["zgemm.cu", "zgemm_tma.cu", "zinv.cu", "band_ops.cu", "rgf.cu", "ddrgf.cu", "prof.cu", "multi.cu", "capi.cu"]
+SOURCES = ["zgemm.cu", "zgemm_tma.cu", "zinv.cu", "band_ops.cu", "rgf.cu", "ddrgf.cu", "ddrgf_iface.cu", "prof.cu", "multi.cu", "capi.cu"]
 HEADERS = ["zcommon.cuh", "internal.h", "dyson_gen.h"]
 NVCC = os.environ.get("NVCC", "/usr/local/cuda/bin/nvcc")
 FLAGS = ["-gencode", "arch=compute_100a,code=sm_100a", "-O3", "-lineinfo", "-std=c++17",

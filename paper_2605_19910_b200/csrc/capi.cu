@@ -1021,12 +1021,12 @@ static int validate_ddrgf(int l, int w, int bs, const int* sizes, const int* s2_
 
 // Runs the stabilised DDRGF on device buffers; fills *fail_layer on a singular pivot.
 static int ddrgf_on_device(const double2* dA, double2* dG, int l, int bp, const std::vector<int>& n_true, int s2,
-                           int* fail_layer, cudaStream_t s) {
+                           int* fail_layer, cudaStream_t s, const int* levels_above = nullptr, int n_above = 0) {
   const size_t sb = ddrgf_scratch_bytes(l, bp, s2);
   void* scr = arena_get(9, sb);
   if (!scr) return fail(BBSI_OUT_OF_MEMORY, "ddrgf workspace allocation failed");
   int fl = -1;
-  CK(ddrgf_device(dA, dG, l, bp, n_true.data(), s2, ddrgf_gamma0(), scr, sb, &fl, s));
+  CK(ddrgf_device(dA, dG, l, bp, n_true.data(), s2, ddrgf_gamma0(), scr, sb, &fl, s, levels_above, n_above));
   CK(cudaStreamSynchronize(s));
   if (fl >= 0) {
     if (fail_layer) *fail_layer = fl;
@@ -1056,7 +1056,9 @@ int bbsi_cuda_ddrgf_z(int l, int w, int bs, const int* sizes, const double* A, c
     CK(cudaMemsetAsync(dA, 0, size_t(bp) * bp * sizeof(double2), s));
     CK(cudaMemsetAsync(dA + (size_t(l - 1) * 3 + 2) * bp * bp, 0, size_t(bp) * bp * sizeof(double2), s));
   }
-  if (int rc = ddrgf_on_device(dA, dG, l, bp, h.sz, s2_levels[0], fail_layer, s)) return rc;
+  // s2_levels[1..]: the nested interface solve (csrc/ddrgf_iface.cu)
+  if (int rc = ddrgf_on_device(dA, dG, l, bp, h.sz, s2_levels[0], fail_layer, s, s2_levels + 1, n_levels - 1))
+    return rc;
   if (direct) {
     CK(cudaMemcpyAsync(G, dG, bytes, cudaMemcpyDeviceToHost, s));
     CK(cudaStreamSynchronize(s));
@@ -1347,7 +1349,8 @@ int bbsi_cuda_ddrgf_multi_z(int l, int w, int bs, const int* sizes, const double
         return cudaSuccess;
       };
     }
-    cudaError_t e = ddrgf_rank(dA, dG, l, bp, h.sz.data(), s2, t0, t1, ddrgf_gamma0(), x, scr, sb, &fl[r], s);
+    cudaError_t e = ddrgf_rank(dA, dG, l, bp, h.sz.data(), s2, t0, t1, ddrgf_gamma0(), x, scr, sb, &fl[r], s,
+                               s2_levels + 1, n_levels - 1);
     if (e != cudaSuccess) return xerr.empty() ? cuda_fail(e, "ddrgf rank") : fail(BBSI_CUDA_ERROR, xerr);
     if (fl[r] >= 0) return BBSI_OK;
     // rows [L0, L1) of G: this rank's chains (written once, disjoint across ranks)

@@ -87,25 +87,6 @@ cudaError_t mm(int b, int batch, double alpha, ZOp A, ZOp B, double beta, ZOp C,
   return zgemm_grouped(g, s);
 }
 
-// complex-scaled product: D = alpha * A * B + beta * C with complex alpha
-cudaError_t mmz(int b, double2 alpha, ZOp A, ZOp B, double beta, ZOp C, cudaStream_t s) {
-  ZGemmGroup g{};
-  g.batch = 1;
-  g.bs = 64;
-  g.nprob = 1;
-  ZGemmProblem& p = g.prob[0];
-  p.M = b;
-  p.N = b;
-  p.K = b;
-  p.alpha = alpha;
-  p.beta = make_double2(beta, 0.0);
-  p.A = A;
-  p.B = B;
-  p.C = C;
-  p.D = C;
-  return zgemm_grouped(g, s);
-}
-
 struct Part {
   std::vector<int> first, count, sep;  // per task
   int T = 0;
@@ -430,10 +411,9 @@ cudaError_t ddrgf_phase1(const double2* A, double2* G, int l, int b, const int* 
   return cudaSuccess;
 }
 
-// Phase 2 (redundant on every rank): left-/right-connected sweeps over all T
-// separators from the gathered packets. The right-connected recursion does not depend
-// on the left sweep, so it runs on a side stream concurrently with it (each step is a
-// chain of b x b inversions, latency-bound at batch 1).
+// Phase 2 (redundant on every rank): the interface system over all T tasks from the
+// gathered packets, single level or nested over the plan's later levels
+// (csrc/ddrgf_iface.cu). The right-connected recursions run on a side stream.
 namespace {
 struct SideStream {
   cudaStream_t s = nullptr;
@@ -455,156 +435,36 @@ SideStream& side_stream() {
 }  // namespace
 
 cudaError_t ddrgf_phase2(const double2* packets, int l, int b, const int* n_true, int s2, double gamma0, double2* out,
-                         int* fail_layer, cudaStream_t s) {
+                         int* fail_layer, cudaStream_t s, const int* levels_above, int n_above) {
   *fail_layer = -1;
   const Part P = partition(l, s2);
   const int T = P.T;
   const long long bb = (long long)b * b;
-  auto pk = [&](int t, int k) { return packets + ((size_t)t * PK + k) * bb; };
-  auto o = [&](int t, int k) { return out + ((size_t)t * NOUT + k) * bb; };
-  const double2 m1 = make_double2(-1.0, 0.0);
   cudaError_t e;
   std::vector<long long> offs;
-  for (int t = 0; t < T; ++t) offs.push_back(pk(t, PASS) - packets);
+  for (int t = 0; t < T; ++t) offs.push_back((long long)((size_t)t * PK + PASS) * bb);
   std::vector<double> gam;
   if ((e = task_gammas(packets, offs, b, gamma0, gam, s))) return e;
-  // scratch: 10 temporaries per stream (Tm(8), Tm(9): the inverse refinement)
-  constexpr int NT = 10;
-  double2* scr = static_cast<double2*>(arena_get(13, size_t(2 * NT) * bb * sizeof(double2)));
-  const int max_inv = 6 * T + 4;
-  void* inv_scr = arena_get(7, zinv_scratch_bytes(b, 1) + 256);
-  void* inv_scr2 = arena_get(17, zinv_scratch_bytes(b, 1) + 256);
-  int* st = static_cast<int*>(arena_get(8, sizeof(int) * size_t(max_inv)));
-  if (!scr || !inv_scr || !inv_scr2 || !st) return cudaErrorMemoryAllocation;
+  std::vector<char> empty(T);
+  std::vector<int> first(T), last(T), sep(T);
+  for (int t = 0; t < T; ++t) {
+    empty[t] = P.count[t] == 0;
+    first[t] = P.count[t] > 0 ? P.first[t] : P.sep[t];
+    last[t] = P.count[t] > 0 ? P.first[t] + P.count[t] - 1 : P.sep[t];
+    sep[t] = P.sep[t];
+  }
+  if (T > 0 && empty[0]) return cudaErrorInvalidValue;  // task 0 always has interior layers
+  const int cap = iface_status_cap(T);
+  int* st = static_cast<int*>(arena_get(8, sizeof(int) * size_t(cap)));
+  if (!st) return cudaErrorMemoryAllocation;
   SideStream& side = side_stream();
   std::vector<int> st_layer;
-  st_layer.reserve(max_inv);
-  const bool refine = [] {  // read per call: tools/ddrgf_diag.py compares both
-    const char* ev = getenv("BBSI_DDRGF_REFINE");
-    return !(ev && atoi(ev) == 0);
-  }();
-  struct Ops {
-    cudaStream_t s;
-    double2* tm0;
-    void* iscr;
-    long long bb;
-    double2* Tm(int i) const { return tm0 + (size_t)i * bb; }
-  };
-  const Ops L{s, scr, inv_scr, bb};
-  const Ops R{side.s, scr + (size_t)NT * bb, inv_scr2, bb};
-  // b x b inverse in place, then one Newton-Schulz step X <- X + X (I - M X): the
-  // interface quantities feed every later separator, so their inverses are refined to
-  // working accuracy (env BBSI_DDRGF_REFINE=0: off)
-  auto inv = [&](const Ops& q, double2* m, int layer) -> cudaError_t {
-    if (int(st_layer.size()) >= max_inv) return cudaErrorInvalidValue;
-    int* slot = st + st_layer.size();
-    st_layer.push_back(layer);
-    cudaError_t e2;
-    if (refine && (e2 = cudaMemcpyAsync(q.Tm(8), m, bb * sizeof(double2), cudaMemcpyDeviceToDevice, q.s))) return e2;
-    if ((e2 = zinv_batched(m, b, bb, b, n_true ? n_true[layer] : b, 1, q.iscr, slot, q.s))) return e2;
-    if (!refine) return cudaSuccess;
-    // R = I - M X  (into Tm(9));  Tm(8) = X R;  X += Tm(8)
-    if ((e2 = cudaMemsetAsync(q.Tm(9), 0, bb * sizeof(double2), q.s))) return e2;
-    if ((e2 = diag_add(q.Tm(9), 0, b, 1, make_double2(1.0, 0.0), q.s))) return e2;
-    if ((e2 = mm(b, 1, -1.0, blk(q.Tm(8), b), blk(m, b), 1.0, blk(q.Tm(9), b), q.s))) return e2;
-    if ((e2 = mm(b, 1, 1.0, blk(m, b), blk(q.Tm(9), b), 0.0, blk(q.Tm(8), b), q.s))) return e2;
-    return axpy(m, q.Tm(8), bb, make_double2(1.0, 0.0), q.s);
-  };
-  auto ident = [&](const Ops& q, double2* m) -> cudaError_t {
-    cudaError_t e2 = cudaMemsetAsync(m, 0, bb * sizeof(double2), q.s);
-    return e2 ? e2 : diag_add(m, 0, b, 1, make_double2(1.0, 0.0), q.s);
-  };
-  auto copy = [&](const Ops& q, double2* d, const double2* x) {
-    return cudaMemcpyAsync(d, x, bb * sizeof(double2), cudaMemcpyDeviceToDevice, q.s);
-  };
-  auto mm3 = [&](const Ops& q, double2* d, double alpha, const double2* x, const double2* y,
-                 const double2* z) -> cudaError_t {
-    // d = alpha * x * y * z  (via Tm(7))
-    cudaError_t e2 = mm(b, 1, 1.0, blk(x, b), blk(y, b), 0.0, blk(q.Tm(7), b), q.s);
-    return e2 ? e2 : mm(b, 1, alpha, blk(q.Tm(7), b), blk(z, b), 0.0, blk(d, b), q.s);
-  };
-  // out = x + i*gamma x (I - i*gamma x)^{-1} x   (removes the fake lead at the block of x)
-  auto remove_fake = [&](const Ops& q, double2* o_, const double2* x, double gamma, int layer) -> cudaError_t {
-    cudaError_t e2;
-    if ((e2 = ident(q, q.Tm(2)))) return e2;
-    if ((e2 = axpy(q.Tm(2), x, bb, make_double2(0.0, -gamma), q.s))) return e2;
-    if ((e2 = inv(q, q.Tm(2), layer))) return e2;
-    if ((e2 = mm(b, 1, 1.0, blk(q.Tm(2), b), blk(x, b), 0.0, blk(q.Tm(3), b), q.s))) return e2;
-    if ((e2 = copy(q, o_, x))) return e2;
-    return mmz(b, make_double2(0.0, gamma), blk(x, b), blk(q.Tm(3), b), 1.0, blk(o_, b), q.s);
-  };
-  if ((e = cudaEventRecord(side.fork, s)) || (e = cudaStreamWaitEvent(side.s, side.fork, 0))) return e;
-  // ---- right-connected recursion (side stream): Sigma^R and Y_t
-  for (int t = T - 1; t >= 0; --t) {
-    const int sp = P.sep[t], cnt = P.count[t];
-    if (t < T - 1) {
-      if ((e = mm3(R, o(t, OSR), 1.0, pk(t, PASN), o(t + 1, OY), pk(t + 1, PAX0)))) return e;
-    } else if ((e = cudaMemsetAsync(o(t, OSR), 0, bb * sizeof(double2), R.s))) {
-      return e;
-    }
-    // gR = (A[s,s] - Sigma^R)^{-1}: the right-connected G at the separator
-    double2* gR = R.Tm(0);
-    if ((e = copy(R, gR, pk(t, PASS)))) return e;
-    if ((e = axpy(gR, o(t, OSR), bb, m1, R.s))) return e;
-    if ((e = inv(R, gR, sp))) return e;
-    if (cnt > 0) {
-      const int last = P.first[t] + cnt - 1;
-      const double2 ig = make_double2(0.0, gam[t]);
-      double2* Dl = R.Tm(1);
-      if ((e = mm3(R, Dl, 1.0, pk(t, PALS), gR, pk(t, PASL)))) return e;
-      if ((e = diag_add(Dl, 0, b, 1, ig, R.s))) return e;
-      if ((e = ident(R, R.Tm(2)))) return e;
-      if ((e = mm(b, 1, -1.0, blk(Dl, b), blk(pk(t, PE), b), 1.0, blk(R.Tm(2), b), R.s))) return e;
-      if ((e = inv(R, R.Tm(2), last))) return e;
-      if ((e = mm(b, 1, 1.0, blk(R.Tm(2), b), blk(Dl, b), 0.0, blk(R.Tm(3), b), R.s))) return e;
-      if ((e = mm(b, 1, 1.0, blk(R.Tm(3), b), blk(pk(t, PC), b), 0.0, blk(R.Tm(4), b), R.s))) return e;
-      if ((e = copy(R, R.Tm(5), pk(t, PA)))) return e;
-      if ((e = mm(b, 1, 1.0, blk(pk(t, PB), b), blk(R.Tm(4), b), 1.0, blk(R.Tm(5), b), R.s))) return e;
-      if ((e = remove_fake(R, o(t, OY), R.Tm(5), gam[t], P.first[t]))) return e;
-    } else if ((e = copy(R, o(t, OY), gR))) {
-      return e;
-    }
-  }
-  if ((e = cudaEventRecord(side.join, R.s))) return e;
-  // ---- left-connected sweep (main stream): Sigma^L and gL_t
-  for (int t = 0; t < T; ++t) {
-    const int f = P.first[t], cnt = P.count[t], sp = P.sep[t];
-    double2* SL = L.Tm(6);  // Sigma of everything left of separator t, seen from it
-    if (cnt > 0) {
-      // Sigma^L on the first block (from separator t-1); Df = Sigma^L - Sigma0
-      const double2 ig = make_double2(0.0, gam[t]);
-      double2* Df = L.Tm(1);
-      if (t > 0) {
-        if ((e = mm3(L, o(t, OSL), 1.0, pk(t, PAX0), o(t - 1, OGL), pk(t - 1, PASN)))) return e;
-      } else if ((e = cudaMemsetAsync(o(t, OSL), 0, bb * sizeof(double2), s))) {
-        return e;
-      }
-      if ((e = copy(L, Df, o(t, OSL)))) return e;
-      if ((e = diag_add(Df, 0, b, 1, ig, s))) return e;
-      // e' = e + c (I - Df a)^{-1} Df b
-      if ((e = ident(L, L.Tm(2)))) return e;
-      if ((e = mm(b, 1, -1.0, blk(Df, b), blk(pk(t, PA), b), 1.0, blk(L.Tm(2), b), s))) return e;
-      if ((e = inv(L, L.Tm(2), f))) return e;
-      if ((e = mm(b, 1, 1.0, blk(L.Tm(2), b), blk(Df, b), 0.0, blk(L.Tm(3), b), s))) return e;
-      if ((e = mm(b, 1, 1.0, blk(L.Tm(3), b), blk(pk(t, PB), b), 0.0, blk(L.Tm(4), b), s))) return e;
-      if ((e = copy(L, L.Tm(5), pk(t, PE)))) return e;
-      if ((e = mm(b, 1, 1.0, blk(pk(t, PC), b), blk(L.Tm(4), b), 1.0, blk(L.Tm(5), b), s))) return e;
-      double2* gld = L.Tm(0);
-      if ((e = remove_fake(L, gld, L.Tm(5), gam[t], f + cnt - 1))) return e;
-      if ((e = mm3(L, SL, 1.0, pk(t, PASL), gld, pk(t, PALS)))) return e;
-    } else {
-      if (t == 0) return cudaErrorInvalidValue;  // task 0 always has interior layers
-      if ((e = mm3(L, SL, 1.0, pk(t, PASL), o(t - 1, OGL), pk(t - 1, PASN)))) return e;
-      if ((e = copy(L, o(t, OSL), SL))) return e;  // the chain's only block is the separator
-    }
-    // gL_t = (A[s,s] - Sigma_left)^{-1}
-    if ((e = copy(L, o(t, OGL), pk(t, PASS)))) return e;
-    if ((e = axpy(o(t, OGL), SL, bb, m1, s))) return e;
-    if ((e = inv(L, o(t, OGL), sp))) return e;
-  }
-  if ((e = cudaStreamWaitEvent(s, side.join, 0))) return e;
+  e = iface_solve(packets, out, T, b, n_true ? n_true[0] : b, gam, empty, first, last, sep, levels_above, n_above, st,
+                  cap, st_layer, s, side.s, side.fork, side.join);
+  if (e) return e;
   std::vector<int> sh(st_layer.size());
-  if ((e = cudaMemcpyAsync(sh.data(), st, sh.size() * sizeof(int), cudaMemcpyDeviceToHost, s))) return e;
+  if (!sh.empty() && (e = cudaMemcpyAsync(sh.data(), st, sh.size() * sizeof(int), cudaMemcpyDeviceToHost, s)))
+    return e;
   if ((e = cudaStreamSynchronize(s))) return e;
   for (size_t q = 0; q < sh.size(); ++q)
     if (sh[q] >= 0) {
@@ -705,7 +565,7 @@ std::vector<std::pair<int, int>> ddrgf_rank_ranges(int n_tasks, int nranks) {
 // GPUs, identity on one), `halo_exchange` the neighbours' boundary blocks.
 cudaError_t ddrgf_rank(const double2* A_loc, double2* G_loc, int l, int b, const int* n_true, int s2, int t0, int t1,
                        double gamma0, const DdrgfExchange& x, void* scratch, size_t scratch_bytes, int* fail_layer,
-                       cudaStream_t s) {
+                       cudaStream_t s, const int* levels_above, int n_above) {
   *fail_layer = -1;
   const Part P = partition(l, s2);
   const int T = P.T;
@@ -725,7 +585,7 @@ cudaError_t ddrgf_rank(const double2* A_loc, double2* G_loc, int l, int b, const
     *fail_layer = any;
     return cudaSuccess;
   }
-  if ((e = ddrgf_phase2(packets, l, b, n_true, s2, gamma0, out, &fl, s)) || fl >= 0) {
+  if ((e = ddrgf_phase2(packets, l, b, n_true, s2, gamma0, out, &fl, s, levels_above, n_above)) || fl >= 0) {
     *fail_layer = fl;
     return e;
   }
@@ -742,7 +602,8 @@ cudaError_t ddrgf_rank(const double2* A_loc, double2* G_loc, int l, int b, const
 }
 
 cudaError_t ddrgf_device(const double2* A, double2* G, int l, int b, const int* n_true, int s2, double gamma0,
-                         void* scratch, size_t scratch_bytes, int* fail_layer, cudaStream_t s) {
+                         void* scratch, size_t scratch_bytes, int* fail_layer, cudaStream_t s, const int* levels_above,
+                         int n_above) {
   DdrgfExchange local;  // one rank: nothing to exchange
   local.packets = [](double2*, int, int, int fl, int* any, cudaStream_t) {
     *any = fl;
@@ -753,7 +614,8 @@ cudaError_t ddrgf_device(const double2* A, double2* G, int l, int b, const int* 
     return cudaSuccess;
   };
   const int T = partition(l, s2).T;
-  return ddrgf_rank(A, G, l, b, n_true, s2, 0, T, gamma0, local, scratch, scratch_bytes, fail_layer, s);
+  return ddrgf_rank(A, G, l, b, n_true, s2, 0, T, gamma0, local, scratch, scratch_bytes, fail_layer, s, levels_above,
+                    n_above);
 }
 
 int ddrgf_num_tasks(int l, int s2) { return partition(l, s2).T; }

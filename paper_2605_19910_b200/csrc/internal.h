@@ -145,8 +145,10 @@ cudaError_t zmm(int b, int batch, double2 alpha, ZOp A, ZOp B, double beta, ZOp 
 
 // Stabilised DDRGF (ddrgf.cu) on one device band A (w = 1, uniform bs) -> G.
 // gamma0: fake-lead strength relative to max|A[s,s]| of each task (BBSI_DDRGF_GAMMA).
+// levels_above / n_above: the plan's s2_levels[1..] (nested interface solve, ddrgf_iface.cu)
 cudaError_t ddrgf_device(const double2* A, double2* G, int l, int b, const int* n_true, int s2, double gamma0,
-                         void* scratch, size_t scratch_bytes, int* fail_layer, cudaStream_t s);
+                         void* scratch, size_t scratch_bytes, int* fail_layer, cudaStream_t s,
+                         const int* levels_above = nullptr, int n_above = 0);
 size_t ddrgf_scratch_bytes(int l, int b, int s2);
 double ddrgf_gamma0();
 // Phases of the same algorithm on a rank-local slice (tasks [t0, t1)); only the
@@ -157,7 +159,14 @@ size_t ddrgf_phase2_out_bytes(int ntask, int b);
 cudaError_t ddrgf_phase1(const double2* A, double2* G, int l, int b, const int* n_true, int s2, double gamma0, int t0,
                          int t1, double2* packet, int* fail_layer, cudaStream_t s);
 cudaError_t ddrgf_phase2(const double2* packets, int l, int b, const int* n_true, int s2, double gamma0, double2* out,
-                         int* fail_layer, cudaStream_t s);
+                         int* fail_layer, cudaStream_t s, const int* levels_above = nullptr, int n_above = 0);
+// The interface solve behind phase 2 (ddrgf_iface.cu).
+cudaError_t iface_solve(const double2* packets, double2* out, int T, int b, int n_true, const std::vector<double>& gam,
+                        const std::vector<char>& empty, const std::vector<int>& first, const std::vector<int>& last,
+                        const std::vector<int>& sep, const int* levels, int nl, int* st, int st_cap,
+                        std::vector<int>& st_layer, cudaStream_t s, cudaStream_t side, cudaEvent_t fork,
+                        cudaEvent_t join);
+int iface_status_cap(int T);
 cudaError_t ddrgf_phase3(const double2* A, double2* G, int l, int b, const int* n_true, int s2, int t0, int t1,
                          const double2* out, int* fail_layer, cudaStream_t s);
 cudaError_t ddrgf_halo(const double2* G, int l, int b, int s2, int t0, int t1, double2* halo, cudaStream_t s);
@@ -177,7 +186,7 @@ struct DdrgfExchange {
 };
 cudaError_t ddrgf_rank(const double2* A_loc, double2* G_loc, int l, int b, const int* n_true, int s2, int t0, int t1,
                        double gamma0, const DdrgfExchange& x, void* scratch, size_t scratch_bytes, int* fail_layer,
-                       cudaStream_t s);
+                       cudaStream_t s, const int* levels_above = nullptr, int n_above = 0);
 // NCCL (multi.cu, resolved with dlopen at first use).
 bool nccl_ready(std::string* err);
 int nccl_unique_id(void* out, std::string* err);

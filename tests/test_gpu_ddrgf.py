@@ -161,3 +161,18 @@ def test_scale_invariance(gpu, scale):
     ref, _ = O.rgf_tridiag(a)
     g, _ = P.ddrgf(to_product(a), _plan([7]))
     assert max_err(g, ref) <= 1e-10
+
+
+@pytest.mark.parametrize("l,b,plan,E,eta", [(96, 64, [7, 2], 0.1, 1e-4), (120, 64, [4, 3, 1], -0.3, 1e-4),
+                                            (64, 128, [3, 2], 0.2, 1e-4), (77, 64, [5, 4], 0.05, 1e-5),
+                                            (40, 64, [2, 1, 1], 0.3, 1e-3)])
+def test_nested_levels_on_device(gpu, l, b, plan, E, eta):
+    """Multi-level plans (s2_levels[1..], ddrgf.hpp:363-369) run on the device: the level-0
+    2-ports are merged into super 2-ports per level (csrc/ddrgf_iface.cu) and the interface
+    system is solved top-down. Same output as sequential RGF to the 1e-10 bar."""
+    a = DO.dyson_matrix(DO.hamiltonian(l, 1, b, 11), complex(E, eta), 1)
+    ref, _ = O.rgf_tridiag(a)
+    g, c = P.ddrgf(to_product(a), _plan(plan))
+    assert max_err(g, ref) <= 1e-10
+    g1, _ = P.ddrgf(to_product(a), _plan(plan[:1]))
+    assert max_err(g, O.Band(ref.layout, g1.data.copy())) <= 1e-10
