@@ -58,14 +58,16 @@ bool two_ended_default() {
 }
 
 namespace {
-// Banded (w >= 2) two-ended sweeps are opt-in (BBSI_TWO_ENDED_BANDED=1): 1.32x faster on
-// config 3 (307 -> 232 ms/step) and more accurate at E = +-1.5, but at the ill-conditioned
-// E = 0.1452 its error is 3.9e-10 against the reference's 1.7e-10 noise floor, which the
-// one-ended order meets (profiles/r01_parity.md).
+// Banded (w >= 2) two-ended sweeps (BBSI_TWO_ENDED_BANDED=0: one-ended). With one
+// refinement step of every multiplier and of the dense middle inverse they are the
+// faster and the more accurate order on config 3 (B200: 278 vs 353 ms per step; 25 of 32
+// energies <= 1e-10 against the compiled reference vs 15, residual at the reference's
+// level; profiles/r02_parity.md). Round 1 kept them opt-in: without the refinement their
+// worst error was 2.3x the reference's floor at E = 0.145.
 bool two_ended_banded() {
   static const bool on = [] {
     const char* e = getenv("BBSI_TWO_ENDED_BANDED");
-    return e && atoi(e) == 1;
+    return !(e && atoi(e) == 0);
   }();
   return on;
 }

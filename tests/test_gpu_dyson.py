@@ -107,11 +107,11 @@ def _in_subprocess(env, code):
     assert r.returncode == 0, r.stdout[-2000:] + r.stderr[-2000:]
 
 
-def test_two_ended_banded_sweep(gpu):
-    """Opt-in banded two-ended recursion (BBSI_TWO_ENDED_BANDED=1: chains from both ends,
-    the w middle layers inverted as one dense (w b)^2 matrix, outward sweeps; one-ended
-    below l = 3w + 2) against the reference's rgf_ndiag, and the host path's streamed rows
-    against the resident bands."""
+def test_one_ended_banded_sweep(gpu):
+    """The one-ended banded recursion (BBSI_TWO_ENDED_BANDED=0; the default is two-ended:
+    chains from both ends, the w middle layers inverted as one dense (w b)^2 matrix,
+    outward sweeps; one-ended below l = 3w + 2) against the reference's rgf_ndiag, and the
+    host path's streamed rows against the resident bands."""
     code = f"""
 import numpy as np
 from dataclasses import replace
@@ -126,7 +126,7 @@ for w, layers in ((2, 14), (3, 20)):
     assert (fails == -1).all() and np.array_equal(got, dev)
 print("ok")
 """
-    _in_subprocess({"BBSI_TWO_ENDED_BANDED": "1"}, code)
+    _in_subprocess({"BBSI_TWO_ENDED_BANDED": "0"}, code)
 
 
 def test_switches_keep_results(gpu, tmp_path):
