@@ -457,6 +457,8 @@ def run_ours(args, rank, world, local_rank):
         except Exception as ex:  # the GPU number stands without it
             cpu = {"error": str(ex)}
     if rank == 0 and world == 1 and not args.no_traffic:
+        torch.cuda.empty_cache()
+        L.bbsi_cuda_release_workspace()
         traffic = measure_traffic(args.config, 0)
 
     if rank == 0:
@@ -602,9 +604,12 @@ def run_ddrgf(args, rank, world, local_rank):
         except Exception as ex:
             cpu = {"error": str(ex)}
     traffic = None
-    if rank == 0 and world == 1 and not args.no_traffic:
-        traffic = measure_traffic(args.config, P)
     comm.close()
+    if rank == 0 and world == 1 and not args.no_traffic:
+        del A, G, diag  # the probe process needs the device memory (config 5: 154 GB)
+        torch.cuda.empty_cache()
+        L.bbsi_cuda_release_workspace()
+        traffic = measure_traffic(args.config, P)
     if rank == 0:
         roofline = roofline_block(cats, peak, traffic, tflops / world,
                                   "zgemm_grouped_kernel (DMMA f64): sweep, corner-chain and interface GEMMs of one "

@@ -18,6 +18,10 @@ def main():
                 rows.append(r)
     floors5 = {r["energy_index"]: r for r in rows if r.get("kind") == "floor"}
     solves = [r for r in rows if "max" in r]
+    for r in solves:  # config 5: the input-noise floors come from the CPU floor run
+        if r["config"] == 5 and r.get("floor") is None and r["energy_index"] in floors5:
+            r["floor"] = floors5[r["energy_index"]]["floor"]
+            r["verdict"] = "<= 1e-10" if r["max"] <= 1e-10 else ("<= floor" if r["max"] <= r["floor"] else "ABOVE")
     by = collections.defaultdict(list)
     for r in solves:
         by[(r["config"], r["solver"])].append(r)
