@@ -273,10 +273,21 @@ def check_cfg5(energies, domains=8, resid_every=16, floor_file=None):
 
         lib().bbsi_cuda_release_workspace()
         torch.cuda.empty_cache()
-        Gdd = torch.empty((l, 3, b, b), dtype=torch.complex128, device="cuda")
-        D.solve_ddrgf_device(cfg, H, Gdd, s2, energy=e)
-        torch.cuda.synchronize()
+        # A(E) in place of H (58 GB each: H, G and the DDRGF workspace do not fit next to a
+        # separate A): off-diagonal -h, diagonal (z + (-h)) - sigma == (z - h) - sigma exactly
+        A = H.neg_()
         del H
+        dg = A[:, 1].diagonal(dim1=-2, dim2=-1)
+        sig = torch.from_numpy(cfg.sigma()).to(A.device)
+        dg.copy_((z + dg) - sig[:, None])
+        Gdd = torch.empty_like(A)
+        fail = C.c_int(-1)
+        rc = lib().bbsi_cuda_ddrgf_dev(l, b, s2, C.c_void_p(A.data_ptr()), C.c_void_p(Gdd.data_ptr()), C.byref(fail),
+                                       C.c_void_p(torch.cuda.current_stream().cuda_stream))
+        torch.cuda.synchronize()
+        if rc != 0:
+            raise RuntimeError(f"ddrgf failed rc={rc}: {lib().bbsi_cuda_last_error()}")
+        del A, dg
         lib().bbsi_cuda_release_workspace()
         torch.cuda.empty_cache()
         t_gpu = time.time() - t0
