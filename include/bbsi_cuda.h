@@ -112,6 +112,10 @@ int bbsi_cuda_dyson_rgf_z(int l, int w, int bs, int n_energy, const double* H, c
 /* Resident stabilised DDRGF of one band (w = 1): dA, dG device [l][3][bs][bs],
  * interior groups of s2 layers (single-level plan). */
 int bbsi_cuda_ddrgf_dev(int l, int bs, int s2, const double* dA, double* dG, int* fail_layer, void* stream);
+/* Same with a whole DomainPlan: s2_levels[0] partitions the band, s2_levels[1..] the
+ * interface system level by level (ddrgf.hpp:363-369). */
+int bbsi_cuda_ddrgf_plan_dev(int l, int bs, const int* s2_levels, int n_levels, const double* dA, double* dG,
+                             int* fail_layer, void* stream);
 /* Domain-sharded DDRGF, phase by phase (one process per GPU, the caller does the
  * collectives; paper_2605_19910_b200/distributed.py). Tasks = interleave_permutation(l,1,s2)
  * groups (partition.hpp:39-75), T = bbsi_cuda_ddrgf_num_tasks(l, s2). A rank owning

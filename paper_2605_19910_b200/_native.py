@@ -34,6 +34,7 @@ SIGNATURES = {
     "bbsi_cuda_dyson_rgf_z": (_i, [_i, _i, _i, _i, _vp, _vp, _vp, _vp, _vp, _i]),
     "bbsi_cuda_ddrgf_dev": (_i, [_i, _i, _i, _vp, _vp, _vp, _vp]),
     "bbsi_cuda_dyson_ddrgf_dev": (_i, [_i, _i, _vp, _vp, _vp, _i, _vp, _vp, _vp]),
+    "bbsi_cuda_ddrgf_plan_dev": (_i, [_i, _i, _vp, _i, _vp, _vp, _vp, _vp]),
     "bbsi_ddrgf_reference_counters": (None, [_ll, _vp, _i, _vp]),
     "bbsi_cuda_ddrgf_num_tasks": (_i, [_i, _i]),
     "bbsi_cuda_ddrgf_packet_bytes": (_ll, [_i, _i]),

@@ -1084,6 +1084,17 @@ int bbsi_cuda_ddrgf_dev(int l, int bs, int s2, const double* dA, double* dG, int
                          fail_layer, static_cast<cudaStream_t>(stream));
 }
 
+int bbsi_cuda_ddrgf_plan_dev(int l, int bs, const int* s2_levels, int n_levels, const double* dA, double* dG,
+                             int* fail_layer, void* stream) {
+  if (fail_layer) *fail_layer = -1;
+  if (int rc = validate_ddrgf(l, 1, bs, nullptr, s2_levels, n_levels, 1, 1)) return rc;
+  if (bs % 64) return fail(BBSI_INVALID_ARGUMENT, "resident API requires bs % 64 == 0");
+  if (int rc = device_ok()) return rc;
+  std::vector<int> nt(l, bs);
+  return ddrgf_on_device(reinterpret_cast<const double2*>(dA), reinterpret_cast<double2*>(dG), l, bs, nt, s2_levels[0],
+                         fail_layer, static_cast<cudaStream_t>(stream), s2_levels + 1, n_levels - 1);
+}
+
 int bbsi_cuda_dyson_ddrgf_dev(int l, int bs, const double* dH, const double* z, const double* sigma, int s2,
                               double* dG, int* fail_layer, void* stream) {
   if (fail_layer) *fail_layer = -1;

@@ -26,6 +26,7 @@
 // All chains live in the output band itself (domain i + separator i occupy a
 // contiguous run of slots with a uniform stride), so no extra band buffers exist.
 #include <algorithm>
+#include <cstdio>
 #include <cstdlib>
 #include <mutex>
 #include <vector>
@@ -577,7 +578,34 @@ cudaError_t ddrgf_rank(const double2* A_loc, double2* G_loc, int l, int b, const
   double2* halo = out + (size_t)T * NOUT * bb;                 // [2] own, [2] neighbours' (prev last, next first)
   cudaError_t e;
   int fl = -1;
+  // BBSI_DDRGF_TRACE=1: device time of each phase on stderr
+  const bool trace = getenv("BBSI_DDRGF_TRACE") != nullptr;
+  cudaEvent_t ev[6] = {};
+  auto mark = [&](int i) {
+    if (!trace) return;
+    cudaEventCreate(&ev[i]);
+    cudaEventRecord(ev[i], s);
+  };
+  struct Report {
+    bool on;
+    cudaEvent_t* ev;
+    ~Report() {
+      if (!on || !ev[0]) return;
+      const char* names[5] = {"phase 1", "packet exchange", "phase 2", "phase 3", "halo + couplings"};
+      cudaEventSynchronize(ev[5] ? ev[5] : ev[0]);
+      for (int i = 0; i < 5; ++i) {
+        if (!ev[i] || !ev[i + 1]) continue;
+        float ms = 0.f;
+        cudaEventElapsedTime(&ms, ev[i], ev[i + 1]);
+        fprintf(stderr, "[ddrgf] %-17s %9.3f ms\n", names[i], ms);
+      }
+      for (int i = 0; i < 6; ++i)
+        if (ev[i]) cudaEventDestroy(ev[i]);
+    }
+  } report{trace, ev};
+  mark(0);
   e = ddrgf_phase1(A_loc, G_loc, l, b, n_true, s2, gamma0, t0, t1, packets + (size_t)t0 * PK * bb, &fl, s);
+  mark(1);
   if (e) return e;
   int any = fl;
   if ((e = x.packets(packets, t0, t1, fl, &any, s))) return e;
@@ -585,11 +613,14 @@ cudaError_t ddrgf_rank(const double2* A_loc, double2* G_loc, int l, int b, const
     *fail_layer = any;
     return cudaSuccess;
   }
+  mark(2);
   if ((e = ddrgf_phase2(packets, l, b, n_true, s2, gamma0, out, &fl, s, levels_above, n_above)) || fl >= 0) {
     *fail_layer = fl;
     return e;
   }
+  mark(3);
   if ((e = ddrgf_phase3(A_loc, G_loc, l, b, n_true, s2, t0, t1, out, &fl, s))) return e;
+  mark(4);
   if ((e = ddrgf_halo(G_loc, l, b, s2, t0, t1, halo, s))) return e;
   any = fl;
   if ((e = x.halo(halo, halo + 2 * bb, fl, &any, s))) return e;  // also agrees on phase-3 failures
@@ -597,8 +628,10 @@ cudaError_t ddrgf_rank(const double2* A_loc, double2* G_loc, int l, int b, const
     *fail_layer = any;
     return cudaSuccess;
   }
-  return ddrgf_couplings(A_loc, G_loc, l, b, s2, t0, t1, out, t0 > 0 ? halo + 2 * bb : nullptr,
-                         t1 < T ? halo + 3 * bb : nullptr, s);
+  e = ddrgf_couplings(A_loc, G_loc, l, b, s2, t0, t1, out, t0 > 0 ? halo + 2 * bb : nullptr,
+                      t1 < T ? halo + 3 * bb : nullptr, s);
+  mark(5);
+  return e;
 }
 
 cudaError_t ddrgf_device(const double2* A, double2* G, int l, int b, const int* n_true, int s2, double gamma0,

@@ -22,6 +22,7 @@ def main():
     p.add_argument("--layers", type=int, default=0, help="override l (config 5: 512 keeps A + G + scratch in HBM)")
     p.add_argument("--domains", type=int, nargs="+", default=[2, 4, 8])
     p.add_argument("--reps", type=int, default=3)
+    p.add_argument("--plans", nargs="*", default=[], help="DomainPlan s2_levels, e.g. 127 127,5 (A formed once)")
     a = p.parse_args()
     import torch
 
@@ -53,6 +54,31 @@ def main():
     print(json.dumps({"config": cfg.name, "solver": "rgf (1 energy)", "layers": l, "block": b,
                       "ms": round(ms, 2), "inversions_per_s": round(l / (ms * 1e-3), 1)}), flush=True)
     G1 = G[0]
+    if a.plans:
+        import ctypes as C
+
+        import numpy as np
+
+        from paper_2605_19910_b200._native import lib
+
+        A = H.neg()
+        dg = A[:, 1].diagonal(dim1=-2, dim2=-1)
+        sig = torch.from_numpy(cfg.sigma()).to(A.device)
+        dg.copy_((complex(z[0]) + dg) - sig[:, None])
+        for plan in a.plans:
+            lv = np.array([int(x) for x in plan.split(",")], dtype=np.int32)
+            fail = C.c_int(-1)
+
+            def run():
+                rc = lib().bbsi_cuda_ddrgf_plan_dev(l, b, lv.ctypes.data_as(C.c_void_p), len(lv),
+                                                    C.c_void_p(A.data_ptr()), C.c_void_p(G1.data_ptr()),
+                                                    C.byref(fail), C.c_void_p(st.cuda_stream))
+                assert rc == 0, lib().bbsi_cuda_last_error()
+
+            ms = timed(run)
+            print(json.dumps({"config": cfg.name, "solver": f"ddrgf plan {plan} on 1 GPU", "layers": l, "block": b,
+                              "ms": round(ms, 2), "inversions_per_s": round(l / (ms * 1e-3), 1)}), flush=True)
+        return
     for P in a.domains:
         s2 = l // P - 1
         ms = timed(lambda: D.solve_ddrgf_device(cfg, H, G1, s2, stream=st))
