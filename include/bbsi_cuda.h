@@ -89,6 +89,13 @@ int bbsi_cuda_ddrgf_z(int l, int w, int bs, const int* sizes, const double* A, c
  * plan divides evenly). out: int64[3]. */
 void bbsi_ddrgf_reference_counters(long long l, const int* s2_levels, int n_levels, long long* out);
 
+/* Many independent matrices of one layout (the host-buffer batch form of rgf_tridiag /
+ * rgf_ndiag): A, G host [batch][l][2w+1][bs][bs]; solved together on the device in the
+ * reference's elimination order; fail_layers[k] = -1 or matrix k's failing layer (the
+ * other matrices' results are still written); counters as for one call. */
+int bbsi_cuda_rgf_many_z(int l, int w, int bs, const int* sizes, int batch, const double* A, double* G,
+                         long long* counters, int* fail_layers);
+
 /* ---------------------------------------------------------------- resident batched API
  * A batch of independent band matrices (energies or domains) with uniform
  * bs % 64 == 0. dA / dG: device pointers to [batch][l][2w+1][bs][bs];
@@ -102,6 +109,12 @@ int bbsi_cuda_rgf_batched_dev(int l, int w, int bs, int batch, const double* dA,
  * complex[n_energy] (E + i eta), sigma: host complex[l]. */
 int bbsi_cuda_dyson_rgf_dev(int l, int w, int bs, int n_energy, const double* dH, const double* z,
                             const double* sigma, double* dG, int* fail_layers, void* stream);
+
+/* Dyson batch with FULL lead self-energy blocks (energy dependent): A_e = z_e I - H - Sigma_e,
+ * dSigma device [n_energy][2w][bs][bs]: blocks for layers 0..w-1 then l-w..l-1 (Sigma is
+ * zero elsewhere). */
+int bbsi_cuda_dyson_rgf_sigma_dev(int l, int w, int bs, int n_energy, const double* dH, const double* z,
+                                  const double* dSigma, double* dG, int* fail_layers, void* stream);
 
 /* Same solve end to end from HOST buffers (the drop-in form): H host [l][2w+1][bs][bs],
  * G host [n_energy][l][2w+1][bs][bs]. Energies run in chunks of `chunk` (<= 0: n/4);

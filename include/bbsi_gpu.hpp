@@ -195,5 +195,38 @@ inline std::pair<BlockBandedMatrix<cd>, KernelCounters> ddrgf(const BlockBandedM
   return {detail::from_slots(m.layout(), s), detail::counters(c)};
 }
 
+// Many matrices of one layout in one device pass (an energy loop over host-built A(E)):
+// the results of rgf_tridiag / rgf_ndiag for each, in order; throws for the first matrix
+// with a negligible pivot, as calling the single solver on each in turn would.
+inline std::vector<std::pair<BlockBandedMatrix<cd>, KernelCounters>> rgf_many(
+    const std::vector<BlockBandedMatrix<cd>>& ms) {
+  std::vector<std::pair<BlockBandedMatrix<cd>, KernelCounters>> out;
+  if (ms.empty()) return out;
+  std::vector<detail::Slots> in;
+  for (const auto& m : ms) in.push_back(detail::to_slots(m));
+  const auto& s0 = in[0];
+  const size_t n = s0.data.size();
+  std::vector<cd> a(n * ms.size()), g(n * ms.size());
+  for (size_t k = 0; k < ms.size(); ++k) std::memcpy(a.data() + k * n, in[k].data.data(), n * sizeof(cd));
+  long long c[3];
+  std::vector<int> fails(ms.size(), -1);
+  const int rc = bbsi_cuda_rgf_many_z(s0.l, s0.w, s0.bs, s0.sizes.data(), int(ms.size()),
+                                      reinterpret_cast<const double*>(a.data()), reinterpret_cast<double*>(g.data()), c,
+                                      fails.data());
+  int fl = -1;
+  for (int f : fails)
+    if (f >= 0) {
+      fl = f;
+      break;
+    }
+  detail::check(rc, fl);
+  for (size_t k = 0; k < ms.size(); ++k) {
+    auto s = in[k];
+    std::memcpy(s.data.data(), g.data() + k * n, n * sizeof(cd));
+    out.push_back({detail::from_slots(ms[k].layout(), s), detail::counters(c)});
+  }
+  return out;
+}
+
 }  // namespace gpu
 }  // namespace bbsi

@@ -6,8 +6,8 @@ include/bbsi_cuda.h; this package is the host-side mirror of the reference
 """
 from .bbsi import (BlockBandedMatrix, BlockLayout, CudaError, DomainPlan, ExtendedInverse,  # noqa: F401
                    InvalidArgumentError, KernelCounters, SingularMatrixError, ddrgf, make_layout, random_spd_like,
-                   read_bbm, rgf_extended, rgf_fused, rgf_ndiag, rgf_tridiag, write_bbm)
+                   read_bbm, rgf_extended, rgf_fused, rgf_many, rgf_ndiag, rgf_tridiag, write_bbm)
 
 __all__ = ["BlockBandedMatrix", "BlockLayout", "CudaError", "DomainPlan", "ExtendedInverse", "InvalidArgumentError",
            "KernelCounters", "SingularMatrixError", "ddrgf", "make_layout", "random_spd_like", "read_bbm",
-           "rgf_extended", "rgf_fused", "rgf_ndiag", "rgf_tridiag", "write_bbm"]
+           "rgf_extended", "rgf_fused", "rgf_many", "rgf_ndiag", "rgf_tridiag", "write_bbm"]

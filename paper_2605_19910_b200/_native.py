@@ -52,6 +52,8 @@ SIGNATURES = {
     "bbsi_cuda_ddrgf_rank_dev": (_i, [_vp, _i, _i, _i, _vp, _vp, _vp, _vp]),
     "bbsi_cuda_ddrgf_multi_z": (_i, [_i, _i, _i, _vp, _vp, _vp, _i, _i, _i, _i, _vp, _vp, _vp, _vp]),
     "bbsi_cuda_dyson_rgf_multi_z": (_i, [_i, _i, _i, _i, _vp, _vp, _vp, _vp, _vp, _i, _i, _vp]),
+    "bbsi_cuda_rgf_many_z": (_i, [_i, _i, _i, _vp, _i, _vp, _vp, _vp, _vp]),
+    "bbsi_cuda_dyson_rgf_sigma_dev": (_i, [_i, _i, _i, _i, _vp, _vp, _vp, _vp, _vp, _vp]),
     "bbsi_cuda_launch_count": (_ll, []),
     "bbsi_cuda_profile_enable": (None, [_i]),
     "bbsi_cuda_profile_collect": (_i, [_vp, _i]),

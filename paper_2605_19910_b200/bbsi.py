@@ -208,6 +208,32 @@ def rgf_tridiag(m: BlockBandedMatrix, trace: dict | None = None):
     return BlockBandedMatrix._from_slots(lay, g), KernelCounters(*map(int, cnt))
 
 
+def rgf_many(ms: list) -> list:
+    """rgf_tridiag / rgf_ndiag (rgf.hpp:37-137) of many matrices of one layout in one device
+    pass (bbsi_cuda_rgf_many_z). Returns [(G, KernelCounters)]; raises SingularMatrixError
+    for the first matrix (in list order) with a negligible pivot, as calling the single
+    solver on each in turn would."""
+    if not ms:
+        return []
+    lay = ms[0].layout
+    l, w, bs = lay.num_layers, lay.bandwidth, lay.slot_size
+    for m in ms:
+        if (m.layout.num_layers, m.layout.bandwidth, tuple(m.layout.block_sizes)) != (l, w, tuple(lay.block_sizes)):
+            raise InvalidArgumentError("rgf_many: every matrix must have the same layout")
+    sizes = np.array(lay.block_sizes, dtype=np.int32)
+    a = np.ascontiguousarray(np.stack([_args(m)[2] for m in ms]))
+    g = np.zeros_like(a)
+    cnt = np.zeros(3, dtype=np.int64)
+    fails = np.full(len(ms), -1, dtype=np.int32)
+    rc = lib().bbsi_cuda_rgf_many_z(l, w, bs, _ptr(sizes), len(ms), _ptr(a), _ptr(g), _ptr(cnt), _ptr(fails))
+    if rc == 2:
+        k = int(np.argmax(fails >= 0))
+        raise SingularMatrixError(f"singular Schur pivot at layer {int(fails[k])} (matrix {k})", int(fails[k]))
+    _raise(rc)
+    c = KernelCounters(*map(int, cnt))
+    return [(BlockBandedMatrix._from_slots(lay, g[k]), c) for k in range(len(ms))]
+
+
 def rgf_ndiag(m: BlockBandedMatrix, trace: dict | None = None):
     """rgf.hpp:82-137 on the GPU; ``trace`` mirrors StructuralTrace (rgf.hpp:14-16)."""
     lay, sizes, a, g = _args(m)

@@ -188,6 +188,25 @@ cudaError_t diag_shift_batched(double2* M, int n, long long stride, int batch, c
   return cudaGetLastError();
 }
 
+namespace {
+__global__ void axpy_strided_kernel(double2* y, long long ys, const double2* x, long long xs, long long n, double2 a) {
+  const long long g = blockIdx.y;
+  for (long long i = blockIdx.x * (long long)blockDim.x + threadIdx.x; i < n; i += (long long)gridDim.x * blockDim.x) {
+    const double2 v = x[g * xs + i];
+    double2& o = y[g * ys + i];
+    o = make_double2(fma(a.x, v.x, fma(-a.y, v.y, o.x)), fma(a.x, v.y, fma(a.y, v.x, o.y)));
+  }
+}
+}  // namespace
+
+// y_g += a * x_g for nb strided families of n contiguous complex entries
+cudaError_t axpy_strided(double2* y, long long ys, const double2* x, long long xs, long long n, int nb, double2 a,
+                         cudaStream_t s) {
+  ProfScope prof(s, PROF_BAND, 8.0 * n * nb, 48.0 * n * nb);
+  axpy_strided_kernel<<<dim3(grid_for(n, 256) / 4 + 1, nb), 256, 0, s>>>(y, ys, x, xs, n, a);
+  return cudaGetLastError();
+}
+
 // y += x over n complex entries
 cudaError_t axpy_batched(double2* y, const double2* x, long long n, cudaStream_t s) {
   ProfScope prof(s, PROF_BAND, 2.0 * n, 48.0 * n);

@@ -340,6 +340,59 @@ int bbsi_cuda_rgf_fused_z(int l, int w, int bs, const int* sizes, const double* 
   return BBSI_OK;
 }
 
+// Many independent matrices of one layout in one call (an energy loop that built its
+// A(E) on the host): every matrix is padded, the batch is solved by the batched sweeps in
+// the reference's one-ended order (so fail_layers[k] is the layer rgf_tridiag /
+// rgf_ndiag would report for matrix k), and the results come back in one pass.
+int bbsi_cuda_rgf_many_z(int l, int w, int bs, const int* sizes, int batch, const double* A, double* G,
+                         long long* counters, int* fail_layers) {
+  if (int rc = validate_layout(l, w, bs, sizes)) return rc;
+  if (w < 1 && l != 1) return fail(BBSI_INVALID_ARGUMENT, "rgf_ndiag: requires bandwidth >= 1");
+  if (batch < 1) return fail(BBSI_INVALID_ARGUMENT, "batch must be >= 1");
+  if (int rc = device_ok()) return rc;
+  const int bp = pad64(bs);
+  const size_t band_h = size_t(l) * (2 * w + 1) * bs * bs;  // complex per host band
+  const size_t band_d = size_t(l) * (2 * w + 1) * bp * bp;
+  double2* dG = static_cast<double2*>(arena_get(0, band_d * batch * sizeof(double2)));
+  if (!dG) return fail(BBSI_OUT_OF_MEMORY, "band allocation failed");
+  cudaStream_t s = thread_stream(0);
+  std::vector<double2> staging;
+  std::vector<int> sz;
+  for (int k = 0; k < batch; ++k) {
+    HostBand h = make_host(l, w, bs, sizes, A + 2 * band_h * k);
+    pad_band(h, bp, staging);
+    CK(cudaMemcpy(dG + band_d * k, staging.data(), band_d * sizeof(double2), cudaMemcpyHostToDevice));
+    if (k == 0) sz = h.sz;
+  }
+  SweepWork W;
+  W.l = l;
+  W.w = w;
+  W.bs = bp;
+  W.batch = batch;
+  W.G = dG;
+  W.g_bstride = (long long)band_d;
+  std::vector<int> fails;
+  if (int rc = run_sweeps(W, sz, fails, s)) return rc;
+  bool bad = false;
+  for (int k = 0; k < batch; ++k) {
+    if (fail_layers) fail_layers[k] = fails[k];
+    bad |= fails[k] >= 0;
+    if (fails[k] >= 0) continue;
+    staging.resize(band_d);
+    CK(cudaMemcpy(staging.data(), dG + band_d * k, band_d * sizeof(double2), cudaMemcpyDeviceToHost));
+    HostBand h = make_host(l, w, bs, sizes, A + 2 * band_h * k);
+    unpad_band(staging, bp, h, reinterpret_cast<double2*>(G) + band_h * k);
+  }
+  long long L = l, Wd = w;
+  if (l == 1)
+    put_counters(counters, 0, 1, 1);
+  else if (w == 1)
+    put_counters(counters, 4 * (L - 1), L, 3 * L - 2);
+  else
+    put_counters(counters, (3 * Wd * Wd + Wd) * L - 2 * Wd * Wd * Wd - 2 * Wd * Wd, L, L * (2 * Wd + 1) - Wd * Wd - Wd);
+  return bad ? fail(BBSI_SINGULAR, "singular Schur pivot in at least one matrix") : BBSI_OK;
+}
+
 int bbsi_cuda_rgf_batched_dev(int l, int w, int bs, int batch, const double* dA, long long a_bstride, double* dG,
                               int* fail_layers, void* stream) {
   if (int rc = validate_layout(l, w, bs, nullptr)) return rc;
@@ -457,6 +510,54 @@ int bbsi_cuda_dyson_rgf_dev(int l, int w, int bs, int n_energy, const double* dH
                                reinterpret_cast<double2*>(dG) + size_t(b) * W.g_bstride, &fails[b], s));
     if (fail_layers) fail_layers[b] = fails[b];
     bad |= fails[b] >= 0;
+  }
+  return bad ? fail(BBSI_SINGULAR, "singular Schur pivot in at least one energy") : BBSI_OK;
+}
+
+// Dyson batch with full lead self-energy blocks: A_e = z_e I - H - Sigma_e, where Sigma_e
+// is a full bs x bs block on each of the first and last w layers (energy dependent, as
+// lead self-energies are): dSigma [n_energy][2w][bs][bs] (layers 0..w-1, then l-w..l-1).
+int bbsi_cuda_dyson_rgf_sigma_dev(int l, int w, int bs, int n_energy, const double* dH, const double* z,
+                                  const double* dSigma, double* dG, int* fail_layers, void* stream) {
+  if (int rc = validate_layout(l, w, bs, nullptr)) return rc;
+  if (bs % 64) return fail(BBSI_INVALID_ARGUMENT, "resident API requires bs % 64 == 0");
+  if (w < 1 || l < 2 * w) return fail(BBSI_INVALID_ARGUMENT, "Sigma blocks need l >= 2w and w >= 1");
+  if (n_energy < 1) return fail(BBSI_INVALID_ARGUMENT, "n_energy must be >= 1");
+  if (int rc = device_ok()) return rc;
+  cudaStream_t s = static_cast<cudaStream_t>(stream);
+  double2* dzs = static_cast<double2*>(arena_get(2, sizeof(double2) * (size_t(n_energy) + l)));
+  if (!dzs) return fail(BBSI_OUT_OF_MEMORY, "parameter upload allocation failed");
+  CK(cudaMemcpyAsync(dzs, z, sizeof(double2) * n_energy, cudaMemcpyHostToDevice, s));
+  CK(cudaMemsetAsync(dzs + n_energy, 0, sizeof(double2) * l, s));  // scalar sigma 0: the blocks come next
+  double2* G = reinterpret_cast<double2*>(dG);
+  const long long bb = (long long)bs * bs, band = (long long)l * (2 * w + 1) * bb;
+  CK(dyson_form_band(G, reinterpret_cast<const double2*>(dH), l, w, bs, n_energy, dzs, dzs + n_energy, s));
+  // A[a, a] -= Sigma_e[a] on the 2w boundary layers
+  const double2* Sg = reinterpret_cast<const double2*>(dSigma);
+  for (int q = 0; q < 2 * w; ++q) {
+    const int a = q < w ? q : l - 2 * w + q;
+    CK(axpy_strided(G + ((long long)a * (2 * w + 1) + w) * bb, band, Sg + (long long)q * bb, 2LL * w * bb, bb,
+                    n_energy, make_double2(-1.0, 0.0), s));
+  }
+  SweepWork W;
+  W.l = l;
+  W.w = w;
+  W.bs = bs;
+  W.batch = n_energy;
+  W.G = G;
+  W.g_bstride = band;
+  W.groups = dyson_groups(W.batch);
+  W.two_ended = two_ended_default();
+  void* scratch = arena_get(1, sweep_scratch_bytes(W.l, W.w, W.bs, W.batch, W.groups, W.two_ended));
+  if (!scratch) return fail(BBSI_OUT_OF_MEMORY, "sweep workspace allocation failed");
+  sweep_carve(W, scratch);
+  std::vector<int> nt(l, bs), fails;
+  CK(rgf_sweeps(W, nt.data(), s));
+  CK(collect_failures(W, fails, s));
+  bool bad = false;
+  for (int b = 0; b < n_energy; ++b) {
+    if (fails[b] >= 0) bad = true;
+    if (fail_layers) fail_layers[b] = fails[b];
   }
   return bad ? fail(BBSI_SINGULAR, "singular Schur pivot in at least one energy") : BBSI_OK;
 }

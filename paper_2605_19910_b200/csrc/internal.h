@@ -61,6 +61,8 @@ cudaError_t dyson_form_diag_ends(double2* G, const double2* H, int l, int w, int
 // M_b += I (n x n, ld n, batch stride) and y += x (n complex entries).
 cudaError_t diag_shift_batched(double2* M, int n, long long stride, int batch, cudaStream_t s);
 cudaError_t axpy_batched(double2* y, const double2* x, long long n, cudaStream_t s);
+cudaError_t axpy_strided(double2* y, long long ys, const double2* x, long long xs, long long n, int nb, double2 a,
+                         cudaStream_t s);
 cudaError_t dyson_form_band(double2* G, const double2* H, int l, int w, int bs, int batch, const double2* z,
                             const double2* sigma, cudaStream_t s);
 

@@ -216,5 +216,36 @@ int main() {
     report("ragged layout {3,1,4,2,3}", e <= 1e-10, fmt(e));
   }
   std::printf("%d failure(s)\n", g_fail);
+  // ---- many matrices in one pass (bbsi::gpu::rgf_many) vs the reference solver on each
+  {
+    std::vector<BlockBandedMatrix<cd>> ms;
+    for (int k = 0; k < 5; ++k) ms.push_back(random_spd_like<cd>(make_layout(12, 7, 1), 1200 + k, 2.0));
+    auto got = gpu::rgf_many(ms);
+    double worst = 0.0;
+    bool counters_ok = true;
+    for (size_t k = 0; k < ms.size(); ++k) {
+      auto [ref, rc] = rgf_tridiag(ms[k]);
+      worst = std::max(worst, testutil::max_block_error(got[k].first, ref));
+      counters_ok = counters_ok && got[k].second == rc;
+    }
+    report("rgf_many (5 x rgf_tridiag, l=12 b=7)", worst <= 1e-10 && counters_ok, fmt(worst));
+    std::vector<BlockBandedMatrix<cd>> bad = ms;
+    bad[3].block(6, 0) = DenseMatrix<cd>(7, 7);
+    bad[3].block(6, 1) = DenseMatrix<cd>(7, 7);
+    bad[3].block(6, -1) = DenseMatrix<cd>(7, 7);
+    int layer = -2;
+    try {
+      gpu::rgf_many(bad);
+    } catch (const singular_matrix_error& e) {
+      layer = e.layer();
+    }
+    int ref_layer = -3;
+    try {
+      rgf_tridiag(bad[3]);
+    } catch (const singular_matrix_error& e) {
+      ref_layer = e.layer();
+    }
+    report("rgf_many singular layer = reference's", layer == ref_layer && layer >= 0, std::to_string(layer));
+  }
   return g_fail;
 }

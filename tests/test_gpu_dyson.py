@@ -175,3 +175,31 @@ def test_host_path_graph_replay_pinned(gpu):
     got2, _ = D.solve_host(cfg, H=Hh.numpy(), z=z2, G=Gh.numpy())
     ref2, _ = D.solve_host(cfg, H=np.array(Hh.numpy()), z=z2)  # pageable: eager path
     assert np.array_equal(got2, ref2)
+
+
+def test_full_sigma_blocks(gpu):
+    """Dyson batch with full, energy-dependent lead self-energy blocks on the first and last
+    w layers (bbsi_cuda_dyson_rgf_sigma_dev) against the oracle RGF of the same A(E)."""
+    import torch
+    from dataclasses import replace
+
+    for w, l, b in ((1, 12, 64), (2, 14, 64)):
+        cfg = replace(D.scaled(D.CONFIGS[3 if w == 2 else 2], num_layers=l, n_energy=3, block_size=b), bandwidth=w)
+        rng = np.random.default_rng(5)
+        ne = cfg.n_energy
+        sig = (rng.uniform(-0.3, 0.3, (ne, 2 * w, b, b)) + 1j * rng.uniform(-0.6, 0.0, (ne, 2 * w, b, b)))
+        H = torch.empty((l, 2 * w + 1, b, b), dtype=torch.complex128, device="cuda")
+        D.fill_h_device(cfg, H)
+        G = torch.empty((ne, l, 2 * w + 1, b, b), dtype=torch.complex128, device="cuda")
+        dsig = torch.from_numpy(np.ascontiguousarray(np.swapaxes(sig, -1, -2))).cuda()  # slot (column-major) blocks
+        D.solve_device_sigma(cfg, H, G, dsig)
+        torch.cuda.synchronize()
+        h = DO.hamiltonian(l, w, b, cfg.seed)
+        for e, z in enumerate(cfg.z()):
+            a = DO.dyson_matrix(h, complex(z), 0)
+            for q in range(2 * w):
+                layer = q if q < w else l - 2 * w + q
+                a.block(layer, 0)[...] -= sig[e, q]
+            ref, _ = (O.rgf_ndiag if w > 1 else O.rgf_tridiag)(a)
+            got = O.Band(ref.layout, np.swapaxes(G[e].cpu().numpy(), -1, -2))
+            assert O.max_block_error(got, ref) <= 1e-10

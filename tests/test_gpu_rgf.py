@@ -185,3 +185,24 @@ def test_extended_vs_reference_on_dyson_blocks(gpu):
         for got, exp in ((ext.first_row[k], ref.first_row[k]), (ext.last_row[k], ref.last_row[k]),
                          (ext.first_col[k], ref.first_col[k]), (ext.last_col[k], ref.last_col[k])):
             assert O.rel_frobenius_error(got, exp) <= 1e-10
+
+
+def test_rgf_many_matches_single_calls(gpu):
+    """bbsi_cuda_rgf_many_z: many matrices of one layout in one pass give exactly the
+    single-call results (same kernels, one batch), w = 1 and w = 2, ragged blocks included."""
+    for lay in (O.make_layout(14, 9, 1), O.make_layout(16, 6, 2), O.BlockLayout(7, [3, 5, 2, 5, 4, 1, 5], 1)):
+        ms = [to_product(O.random_spd_like(lay, 1300 + k, 2.0)) for k in range(4)]
+        many = P.rgf_many(ms)
+        single = P.rgf_ndiag if lay.bandwidth > 1 else P.rgf_tridiag
+        for m, (g, c) in zip(ms, many):
+            g1, c1 = single(m)
+            assert np.array_equal(g.data, g1.data) and c == c1
+
+
+def test_rgf_many_reports_first_failing_matrix(gpu):
+    ms = [O.random_spd_like(O.make_layout(10, 4, 1), 1400 + k, 2.0) for k in range(3)]
+    for off in (-1, 0, 1):
+        ms[1].block(6, off)[...] = 0
+    with pytest.raises(P.SingularMatrixError) as ei:
+        P.rgf_many([to_product(m) for m in ms])
+    assert ei.value.layer == 6
