@@ -277,7 +277,8 @@ def measure_traffic(config: int, domains: int, timeout: float = 240.0):
     """DRAM bytes per launch of the dominant kernel, measured in this run: ncu on a child
     process that runs one eager step of the same workload (tools/traffic_probe.py),
     profiling a few sweep-GEMM launches (zgemm_grouped_kernel<0,...>: the non-plain
-    instantiations, i.e. not the Gauss-Jordan updates). None if ncu is unavailable."""
+    instantiations: the TMA kernel, or the cp.async one with BBSI_TMA=0 -- not the
+    Gauss-Jordan updates). None / {"error": ...} if ncu is unavailable or fails."""
     import csv
     import io
     import shutil
@@ -290,7 +291,7 @@ def measure_traffic(config: int, domains: int, timeout: float = 240.0):
         log = Path(td) / "ncu.csv"
         cmd = [ncu, "--metrics", "dram__bytes_read.sum,dram__bytes_write.sum,gpu__time_duration.sum",
                "--clock-control", "none", "--kernel-name-base", "demangled", "--kernel-name",
-               "regex:zgemm_grouped_kernel<0", "--launch-skip", "40", "--launch-count", "6", "--csv",
+               "regex:zgemm_(tma_kernel|grouped_kernel<0)", "--launch-skip", "40", "--launch-count", "6", "--csv",
                "--log-file", str(log), sys.executable, str(ROOT / "tools" / "traffic_probe.py"), "--config",
                str(config)]
         if domains:
@@ -300,27 +301,37 @@ def measure_traffic(config: int, domains: int, timeout: float = 240.0):
             text = log.read_text()
         except Exception as ex:  # the bench line stands without it
             return {"error": f"ncu probe failed: {type(ex).__name__}"}
-    rows = list(csv.reader(io.StringIO(text[text.find('"ID"'):])))
-    if not rows:
-        return None
-    hdr = rows[0]
-    ii, im, iv, iu = hdr.index("ID"), hdr.index("Metric Name"), hdr.index("Metric Value"), hdr.index("Metric Unit")
-    per = {}
-    scale = {"byte": 1, "Kbyte": 1e3, "Mbyte": 1e6, "Gbyte": 1e9, "nsecond": 1e-9, "usecond": 1e-6, "msecond": 1e-3,
-             "second": 1}
-    for r in rows[1:]:
-        if len(r) <= max(ii, im, iv, iu):
-            continue
-        v = float(r[iv].replace(",", "")) * scale.get(r[iu], 1.0)
-        per.setdefault(r[ii], {})[r[im]] = v
-    launches = [d for d in per.values() if "dram__bytes_read.sum" in d]
-    if not launches:
-        return None
-    traffic = statistics.mean(d["dram__bytes_read.sum"] + d["dram__bytes_write.sum"] for d in launches)
-    dur = statistics.mean(d.get("gpu__time_duration.sum", 0.0) for d in launches)
+    try:
+        start = text.find('"ID"')
+        if start < 0:
+            return {"error": "ncu probe matched no launches"}
+        rows = list(csv.reader(io.StringIO(text[start:])))
+        hdr = rows[0]
+        ii, im, iv, iu = hdr.index("ID"), hdr.index("Metric Name"), hdr.index("Metric Value"), hdr.index("Metric Unit")
+        ik = hdr.index("Kernel Name")
+        per, names = {}, {}
+        scale = {"byte": 1, "Kbyte": 1e3, "Mbyte": 1e6, "Gbyte": 1e9, "nsecond": 1e-9, "usecond": 1e-6,
+                 "msecond": 1e-3, "second": 1}
+        for r in rows[1:]:
+            if len(r) <= max(ii, im, iv, iu, ik):
+                continue
+            v = float(r[iv].replace(",", "")) * scale.get(r[iu], 1.0)
+            per.setdefault(r[ii], {})[r[im]] = v
+            names[r[ii]] = r[ik]
+        launches = [d for d in per.values() if "dram__bytes_read.sum" in d]
+        if not launches:
+            return {"error": "ncu probe: no DRAM metrics in the capture"}
+        traffic = statistics.mean(d["dram__bytes_read.sum"] + d["dram__bytes_write.sum"] for d in launches)
+        dur = statistics.mean(d.get("gpu__time_duration.sum", 0.0) for d in launches)
+        import re
+
+        kern = sorted({(re.search(r"zgemm_\w+<[^>]*>", n) or re.search(r"\w+", n)).group(0) for n in names.values()})
+    except Exception as ex:  # the bench line stands without it
+        return {"error": f"ncu probe parse failed: {type(ex).__name__}: {ex}"}
     return {"bytes_per_launch": traffic, "launches_profiled": len(launches), "ncu_mean_duration_us": dur * 1e6,
-            "command": "ncu --metrics dram__bytes_read.sum,dram__bytes_write.sum -k regex:zgemm_grouped_kernel<0 "
-                       f"-s 40 -c 6 python tools/traffic_probe.py --config {config}"}
+            "kernels": kern,
+            "command": "ncu --metrics dram__bytes_read.sum,dram__bytes_write.sum -k regex:zgemm_(tma_kernel|"
+                       f"grouped_kernel<0) -s 40 -c 6 python tools/traffic_probe.py --config {config}"}
 
 
 def roofline_block(cats, peak, traffic, step_tflops, kernel_note):
@@ -459,7 +470,10 @@ def run_ours(args, rank, world, local_rank):
     if rank == 0 and world == 1 and not args.no_traffic:
         torch.cuda.empty_cache()
         L.bbsi_cuda_release_workspace()
-        traffic = measure_traffic(args.config, 0)
+        try:
+            traffic = measure_traffic(args.config, 0)
+        except Exception as ex:  # never lose the bench line to the probe
+            traffic = {"error": f"{type(ex).__name__}: {ex}"}
 
     if rank == 0:
         roofline = roofline_block(cats, peak, traffic, tflops / world,
@@ -609,7 +623,10 @@ def run_ddrgf(args, rank, world, local_rank):
         del A, G, diag  # the probe process needs the device memory (config 5: 154 GB)
         torch.cuda.empty_cache()
         L.bbsi_cuda_release_workspace()
-        traffic = measure_traffic(args.config, P)
+        try:
+            traffic = measure_traffic(args.config, P)
+        except Exception as ex:  # never lose the bench line to the probe
+            traffic = {"error": f"{type(ex).__name__}: {ex}"}
     if rank == 0:
         roofline = roofline_block(cats, peak, traffic, tflops / world,
                                   "zgemm_grouped_kernel (DMMA f64): sweep, corner-chain and interface GEMMs of one "
