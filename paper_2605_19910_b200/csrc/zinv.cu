@@ -72,6 +72,13 @@ int panel_kind() {
 // staging buffers fit next to the static shared memory (n <= 320).
 bool pair_pre2(int n) { return 2 * size_t(kNB) * (n + 2) * sizeof(double2) + 40 * 1024 <= 227 * 1024; }
 
+// V by substitution with the panel's LU factors (default) or by forming Pinv and the
+// DMMA product Pinv * Vs (BBSI_GJ_SUBST=0, round 1).
+int gj_subst() {
+  const char* e = getenv("BBSI_GJ_SUBST");
+  return (e && atoi(e) == 0) ? 0 : 1;
+}
+
 int panel_priority() {
   static int p = [] {
     int lo = 0, hi = 0;
@@ -92,6 +99,7 @@ struct GjScratch {
   double2* wz;    // [batch][n*nb]  (col-major, ld n)
   double2* vbuf;  // [batch][nb*n]  (col-major, ld nb)
   double2* s0;    // [batch][n*n]   working matrix
+  int subst;      // V by per-column LU substitution (1) or Pinv * Vs on DMMA (0)
 };
 
 // Matrix b of a launch lives at base + (b % inner) * bstride + (b / inner) * ostride and
@@ -171,6 +179,42 @@ __device__ __forceinline__ void pivot_block_inverse(const double2 (*lu)[NB + 1],
     pinv[r][c] = acc;
   }
   __syncthreads();
+}
+
+// x <- U^{-1} L^{-1} x for one column held in registers (lu: L \ U of the pivot block in
+// shared memory, read as broadcasts; uinv: 1 / U_jj). Right-looking: once x_j is final,
+// the updates of the later entries are independent, so the dependent chain is NB deep
+// instead of NB^2/2. Replaces forming Pinv (two triangular inverses and their product)
+// and the Pinv * Vs product: V = Pinv Vs column by column, and the identity columns of
+// Vs give Pinv itself.
+// Shared-memory load the compiler may not hoist out of the column loop (the 240 factor
+// entries are loop invariant; hoisting them all spills the register file).
+__device__ __forceinline__ double2 lds_keep(const double2* p) {
+  double2 v;
+  asm volatile("ld.shared.v2.f64 {%0, %1}, [%2];\n"
+               : "=d"(v.x), "=d"(v.y)
+               : "r"((unsigned)__cvta_generic_to_shared(p)));
+  return v;
+}
+
+template <int NB>
+__device__ __forceinline__ void lu_solve_col(const double2 (*lu)[NB + 1], const double2* uinv, double2 (&x)[NB]) {
+#pragma unroll
+  for (int j = 0; j < NB; ++j) {
+    const double2 xj = make_double2(-x[j].x, -x[j].y);
+#pragma unroll
+    for (int i = 0; i < NB; ++i)
+      if (i > j) x[i] = cfma(lds_keep(&lu[i][j]), xj, x[i]);
+  }
+#pragma unroll
+  for (int jj = 0; jj < NB; ++jj) {
+    const int j = NB - 1 - jj;
+    x[j] = cmul(x[j], lds_keep(&uinv[j]));
+    const double2 xj = make_double2(-x[j].x, -x[j].y);
+#pragma unroll
+    for (int i = 0; i < NB; ++i)
+      if (i < j) x[i] = cfma(lds_keep(&lu[i][j]), xj, x[i]);
+  }
 }
 
 // V = Pinv Vs on the tensor cores, Vs (NB x n) staged in shared memory with ld svld.
@@ -289,46 +333,63 @@ __device__ __forceinline__ void panel_tail(const double2* __restrict__ cur, long
     if (c == 0) rowmask[s_src[j]] = -1;
   }
   ZDBG(5)
-  pivot_block_inverse<NB>(lu, s_uinv, s_pinv);
-  ZDBG(6)
-  if (sv) {
-    // V = Pinv Vs on the tensor cores: Vs staged in smem (ld n + 2), each warp takes
-    // 8-column tiles, 2 x 4 complex m8n8k4 steps (4 real DMMAs each) per tile.
-    const int svld = n + 2;
+  if (S.subst) {
+    // V = U^{-1} L^{-1} Vs by substitution, one column per thread (xpre: the first one)
+    __syncthreads();
     for (int col = tid; col < n; col += PT) {
+      double2 x[NB];
       const bool kc = col >= k && col < k + NB;
 #pragma unroll
       for (int j = 0; j < NB; ++j)
-        sv[j * svld + col] = col == tid ? xpre[j]
-                                        : (kc ? make_double2(col - k == j ? 1.0 : 0.0, 0.0)
-                                              : cur[(long long)col * ld + s_src[j]]);
-    }
-    __syncthreads();
-    ZDBG(7)
-    apply_pinv_dmma<NB>(s_pinv, sv, svld, n, vb, NB);
-    ZDBG(8)
-  } else {
-    // V = Pinv Vs, one column per thread (tall panels: no smem left for Vs)
-    for (int col = tid; col < n; col += PT) {
-      double2 x[NB], acc[NB];
-      const bool kc = col >= k && col < k + NB;
-#pragma unroll
-      for (int j = 0; j < NB; ++j) {
         x[j] = col == tid ? xpre[j]
                           : (kc ? make_double2(col - k == j ? 1.0 : 0.0, 0.0) : cur[(long long)col * ld + s_src[j]]);
-        acc[j] = make_double2(0.0, 0.0);
+      lu_solve_col<NB>(lu, s_uinv, x);
+#pragma unroll
+      for (int j = 0; j < NB; ++j) vb[(long long)col * NB + j] = x[j];
+    }
+    ZDBG(8)
+  } else {
+    pivot_block_inverse<NB>(lu, s_uinv, s_pinv);
+    ZDBG(6)
+    if (sv) {
+      // V = Pinv Vs on the tensor cores: Vs staged in smem (ld n + 2), each warp takes
+      // 8-column tiles, 2 x 4 complex m8n8k4 steps (4 real DMMAs each) per tile.
+      const int svld = n + 2;
+      for (int col = tid; col < n; col += PT) {
+        const bool kc = col >= k && col < k + NB;
+  #pragma unroll
+        for (int j = 0; j < NB; ++j)
+          sv[j * svld + col] = col == tid ? xpre[j]
+                                          : (kc ? make_double2(col - k == j ? 1.0 : 0.0, 0.0)
+                                                : cur[(long long)col * ld + s_src[j]]);
       }
-#pragma unroll 1
-      for (int q = 0; q < NB; ++q) {
-        double2 xq = x[0];
-#pragma unroll
-        for (int u = 1; u < NB; ++u)
-          if (u == q) xq = x[u];
-#pragma unroll
-        for (int j = 0; j < NB; ++j) acc[j] = cfma(s_pinv[j][q], xq, acc[j]);
+      __syncthreads();
+      ZDBG(7)
+      apply_pinv_dmma<NB>(s_pinv, sv, svld, n, vb, NB);
+      ZDBG(8)
+    } else {
+      // V = Pinv Vs, one column per thread (tall panels: no smem left for Vs)
+      for (int col = tid; col < n; col += PT) {
+        double2 x[NB], acc[NB];
+        const bool kc = col >= k && col < k + NB;
+  #pragma unroll
+        for (int j = 0; j < NB; ++j) {
+          x[j] = col == tid ? xpre[j]
+                            : (kc ? make_double2(col - k == j ? 1.0 : 0.0, 0.0) : cur[(long long)col * ld + s_src[j]]);
+          acc[j] = make_double2(0.0, 0.0);
+        }
+  #pragma unroll 1
+        for (int q = 0; q < NB; ++q) {
+          double2 xq = x[0];
+  #pragma unroll
+          for (int u = 1; u < NB; ++u)
+            if (u == q) xq = x[u];
+  #pragma unroll
+          for (int j = 0; j < NB; ++j) acc[j] = cfma(s_pinv[j][q], xq, acc[j]);
+        }
+  #pragma unroll
+        for (int j = 0; j < NB; ++j) vb[(long long)col * NB + j] = acc[j];
       }
-#pragma unroll
-      for (int j = 0; j < NB; ++j) vb[(long long)col * NB + j] = acc[j];
     }
   }
   if (last) {  // output scatters: row lmap[i] -> i, column c -> lmap[c]
@@ -753,13 +814,24 @@ __global__ void __launch_bounds__(PT, 1)
       }
     }
     cp_async_commit();
-    pivot_block_inverse<NB>(sm.lu, s_uinv, s_pinv);
+    if (!S.subst) pivot_block_inverse<NB>(sm.lu, s_uinv, s_pinv);
     ZDBG(15 + 10 * ph)
     cp_async_wait<0>();
     __syncthreads();
     if (ph == 1) break;
     ZDBG(16)
-    apply_pinv_dmma<NB>(s_pinv, sv, svld, n, nullptr, 0);  // sv = V1
+    if (S.subst) {  // sv = V1 = U1^{-1} L1^{-1} Vs1, column by column (panel 1's LU is still in sm.lu)
+      for (int col = tid; col < n; col += PT) {
+        double2 x[NB];
+#pragma unroll
+        for (int j = 0; j < NB; ++j) x[j] = sv[j * svld + col];
+        lu_solve_col<NB>(sm.lu, s_uinv, x);
+#pragma unroll
+        for (int j = 0; j < NB; ++j) sv[j * svld + col] = x[j];
+      }
+    } else {
+      apply_pinv_dmma<NB>(s_pinv, sv, svld, n, nullptr, 0);  // sv = V1
+    }
     __syncthreads();
     ZDBG(17)
     // Wz1 (every row) and panel 2's input M2[:,K2] (every row), one row per thread
@@ -821,7 +893,18 @@ __global__ void __launch_bounds__(PT, 1)
   }
   __syncthreads();
   ZDBG(26)
-  apply_pinv_dmma<NB>(s_pinv, sv, svld, n, vb + NB, W2);  // V2 -> vb rows NB..2NB-1
+  if (S.subst) {  // V2 = U2^{-1} L2^{-1} Vs2 -> vb rows NB..2NB-1
+    for (int col = tid; col < n; col += PT) {
+      double2 x[NB];
+#pragma unroll
+      for (int j = 0; j < NB; ++j) x[j] = sv[j * svld + col];
+      lu_solve_col<NB>(sm.lu, s_uinv, x);
+#pragma unroll
+      for (int j = 0; j < NB; ++j) vb[(long long)col * W2 + NB + j] = x[j];
+    }
+  } else {
+    apply_pinv_dmma<NB>(s_pinv, sv, svld, n, vb + NB, W2);  // V2 -> vb rows NB..2NB-1
+  }
   ZDBG(27)
   if (last) {  // output scatters: row lmap[i] -> i, column c -> lmap[c]
     // (gathering the last GEMM's C and Wz rows through lmap instead, so that it writes
@@ -861,6 +944,7 @@ cudaError_t zinv_batched2(double2* M, long long ld, long long bstride, int n, in
   constexpr int nb = kNB;
   GjScratch S;
   carve(S, scratch, n, nb, batch);
+  S.subst = gj_subst();
   const size_t smem = size_t(nb) * (n + 1) * sizeof(double2) + 3 * size_t(n) * sizeof(int);
   cudaError_t e;
   if ((e = set_max_dyn_smem((const void*)gj_panel_kernel<kNB>, smem))) return e;
