@@ -297,7 +297,10 @@ def measure_traffic(config: int, domains: int, timeout: float = 240.0):
         if domains:
             cmd += ["--domains", str(domains)]
         try:
-            subprocess.run(cmd, capture_output=True, timeout=timeout, check=True)
+            # one stream group, as in profile_step: the profiled launches are the same size
+            # (same tiles, same algorithmic bytes) as the ones the roofline divides by
+            env = dict(os.environ, BBSI_GROUPS="1")
+            subprocess.run(cmd, capture_output=True, timeout=timeout, check=True, env=env)
             text = log.read_text()
         except Exception as ex:  # the bench line stands without it
             return {"error": f"ncu probe failed: {type(ex).__name__}"}
@@ -310,8 +313,9 @@ def measure_traffic(config: int, domains: int, timeout: float = 240.0):
         ii, im, iv, iu = hdr.index("ID"), hdr.index("Metric Name"), hdr.index("Metric Value"), hdr.index("Metric Unit")
         ik = hdr.index("Kernel Name")
         per, names = {}, {}
-        scale = {"byte": 1, "Kbyte": 1e3, "Mbyte": 1e6, "Gbyte": 1e9, "nsecond": 1e-9, "usecond": 1e-6,
-                 "msecond": 1e-3, "second": 1}
+        scale = {"byte": 1, "Kbyte": 1e3, "Mbyte": 1e6, "Gbyte": 1e9, "B": 1, "KB": 1e3, "MB": 1e6, "GB": 1e9,
+                 "nsecond": 1e-9, "usecond": 1e-6, "msecond": 1e-3, "second": 1, "ns": 1e-9, "us": 1e-6,
+                 "ms": 1e-3, "s": 1}
         for r in rows[1:]:
             if len(r) <= max(ii, im, iv, iu, ik):
                 continue

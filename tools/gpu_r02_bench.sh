@@ -3,11 +3,13 @@
 # captures of the top kernels at full occupancy (one stream group: 2048-tile launches).
 set -u
 mkdir -p gpurun_out
+nvidia-smi --query-gpu=name,clocks.sm,clocks.max.sm --format=csv > gpurun_out/smi.txt 2>&1
+BBSI_GJ_SUBST=0 python bench.py --no-e2e --no-cpu-baseline --no-traffic > gpurun_out/r02_cfg2_subst0.json 2> gpurun_out/r02_cfg2_subst0.err; echo "subst0 rc=$?"
 python bench.py > gpurun_out/r02_bench_cfg2.json 2> gpurun_out/r02_bench_cfg2.err; echo "cfg2 rc=$?"
 python bench.py --config 3 > gpurun_out/r02_bench_cfg3.json 2> gpurun_out/r02_bench_cfg3.err; echo "cfg3 rc=$?"
 python bench.py --config 4 > gpurun_out/r02_bench_cfg4.json 2> gpurun_out/r02_bench_cfg4.err; echo "cfg4 rc=$?"
-BBSI_DDRGF_TRACE=1 python tools/bench_ddrgf.py --plans 127 127,5 255 63,7 --reps 2 > gpurun_out/r02_ddrgf_plans.log 2>&1; echo "plans rc=$?"
-python bench.py --config 5 --steps 1 --warmup 3 > gpurun_out/r02_bench_cfg5.json 2> gpurun_out/r02_bench_cfg5.err; echo "cfg5 rc=$?"
+BBSI_DDRGF_TRACE=1 timeout 900 python tools/bench_ddrgf.py --plans 127 127,5 255 63,7 --reps 2 > gpurun_out/r02_ddrgf_plans.log 2>&1; echo "plans rc=$?"
+timeout 1800 python bench.py --config 5 --steps 1 --warmup 3 > gpurun_out/r02_bench_cfg5.json 2> gpurun_out/r02_bench_cfg5.err; echo "cfg5 rc=$?"
 python bench.py --impl reference --steps 2 --warmup 1 > gpurun_out/r02_bench_ref.json 2> gpurun_out/r02_bench_ref.err; echo "ref rc=$?"
 export BBSI_GRAPHS=0 BBSI_GROUPS=1
 for spec in "zgemm_tma_kernel 6 2 sweep_tma" "zgemm_grouped_kernel 24 1 gjgemm" "gj_pair_kernel 24 1 pair"; do
