@@ -577,6 +577,10 @@ def run_ddrgf(args, rank, world, local_rank):
         Ah.copy_(A)
         hd_h, sig_h = hd.cpu(), sig.cpu()[:, None]
         dg = Ah[:, 1].diagonal(dim1=-2, dim2=-1)
+        if world == 1:  # the drop-in allocates its own device band (config 5: 2 x 58 GB + scratch)
+            del A, G, diag
+            torch.cuda.empty_cache()
+            L.bbsi_cuda_release_workspace()
 
         def e2e_step():
             for z in e2e_energies:
@@ -624,7 +628,7 @@ def run_ddrgf(args, rank, world, local_rank):
     traffic = None
     comm.close()
     if rank == 0 and world == 1 and not args.no_traffic:
-        del A, G, diag  # the probe process needs the device memory (config 5: 154 GB)
+        A = G = diag = None  # the probe process needs the device memory (config 5: 154 GB)
         torch.cuda.empty_cache()
         L.bbsi_cuda_release_workspace()
         try:

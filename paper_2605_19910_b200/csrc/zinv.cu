@@ -72,11 +72,12 @@ int panel_kind() {
 // staging buffers fit next to the static shared memory (n <= 320).
 bool pair_pre2(int n) { return 2 * size_t(kNB) * (n + 2) * sizeof(double2) + 40 * 1024 <= 227 * 1024; }
 
-// V by substitution with the panel's LU factors (default) or by forming Pinv and the
-// DMMA product Pinv * Vs (BBSI_GJ_SUBST=0, round 1).
+// V by forming Pinv and the DMMA product Pinv * Vs (default) or by substitution with the
+// panel's LU factors (BBSI_GJ_SUBST=1). Measured on B200, config 2: substitution 85 ms of
+// panel time per step against 73 ms (561 vs 549 ms per step), so it stays opt-in.
 int gj_subst() {
   const char* e = getenv("BBSI_GJ_SUBST");
-  return (e && atoi(e) == 0) ? 0 : 1;
+  return (e && atoi(e) == 1) ? 1 : 0;
 }
 
 int panel_priority() {

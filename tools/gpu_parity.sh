@@ -1,7 +1,13 @@
+# Full-size parity of every BASELINE configuration (tools/parity_full.py), one record per
+# solve appended to gpurun_out/r02_parity.jsonl as it is produced; the markdown tables at
+# the end (tools/parity_report.py, with the committed config-5 CPU floors).
 set -u
 mkdir -p gpurun_out
-timeout 1500 python -m pytest tests -x -q -m gpu > gpurun_out/gpu_tests.log 2>&1; echo "tests rc=$?" >> gpurun_out/gpu_tests.log
-tail -2 gpurun_out/gpu_tests.log
-timeout 300 python -c "import __graft_entry__ as g; g.smoke()" > gpurun_out/smoke.log 2>&1; echo "smoke rc=$?" >> gpurun_out/smoke.log; tail -2 gpurun_out/smoke.log
-timeout 900 python bench.py > gpurun_out/bench_full.log 2>&1; tail -1 gpurun_out/bench_full.log
-timeout 3600 python -u tools/parity_full.py --configs 1 5 2 4 > gpurun_out/parity_full.log 2>&1; cat gpurun_out/parity_full.log
+nproc > gpurun_out/r02_parity_host.txt; free -g >> gpurun_out/r02_parity_host.txt
+for k in ${PARITY_CONFIGS:-1 2 3 5 4}; do
+  timeout ${PARITY_TIMEOUT:-5400} python -u tools/parity_full.py --configs $k --out gpurun_out/r02_parity.jsonl \
+    > gpurun_out/r02_parity_cfg$k.log 2>&1
+  echo "config $k rc=$?"
+done
+python tools/parity_report.py gpurun_out/r02_parity.jsonl profiles/r02_cfg5_floor.jsonl > gpurun_out/r02_parity_tables.md
+head -20 gpurun_out/r02_parity_tables.md
