@@ -42,6 +42,9 @@ cudaError_t zinv_batched(double2* M, long long ld, long long bstride, int n, int
 cudaError_t zinv_batched2(double2* M, long long ld, long long bstride, int n, int n_true, int inner, int outer,
                           long long ostride, void* scratch, int* status, long long sostride, cudaStream_t stream);
 size_t zinv_scratch_bytes(int n, int batch);
+// How many inversion batches of this host thread run concurrently (stream groups of a
+// sweep); the pair panel picks its CTAs per matrix from batch x concurrency.
+void zinv_set_concurrency(int groups);
 cudaError_t dyson_fill_h(double2* H, int l, int w, int b, uint64_t seed, cudaStream_t s);
 // Rows [a0, a1) of the same band into H ([a1-a0][2w+1][b][b], local row 0 = layer a0).
 cudaError_t dyson_fill_h_rows(double2* H, int l, int w, int b, uint64_t seed, int a0, int a1, cudaStream_t s);

@@ -675,6 +675,10 @@ cudaError_t rgf_sweeps(const SweepWork& W, const int* n_true, cudaStream_t s) {
     if (!use_two_ended(X)) return rgf_sweeps_one(X, n_true, st, sstride, q);
     return X.w == 1 ? rgf_sweeps_two(X, n_true, st, sstride, q) : rgf_sweeps_two_w(X, n_true, st, sstride, q);
   };
+  zinv_set_concurrency(G);
+  struct ConcReset {
+    ~ConcReset() { zinv_set_concurrency(1); }
+  } conc_reset;
   if (G == 1) return sweep(W, W.status, s, 0);
   // Independent batch groups on side streams: one group's latency-bound pivot
   // inversions overlap the other groups' GEMMs.

@@ -80,6 +80,27 @@ int gj_subst() {
   return (e && atoi(e) == 1) ? 1 : 0;
 }
 
+// Concurrent inversion batches of this host thread (stream groups of the running sweep).
+thread_local int t_conc = 1;
+
+// CTAs per matrix of the pair panel (BBSI_PANEL_SPLIT, else the largest power of two
+// <= 8 that keeps batch x concurrency x split within one wave of the 148 SMs). Only for
+// n <= PT (register rows, one row per thread) and at least 16 columns per CTA.
+int pair_split(int n, int batch) {
+  const char* ev = getenv("BBSI_PANEL_SPLIT");  // read per call: tests compare splits in one process
+  const int env = ev ? atoi(ev) : 0;
+  if (n > PT) return 1;
+  int s = 1;
+  if (env >= 1) {
+    s = env;
+  } else {
+    const int dev_sms = 148;
+    while (s < 8 && (long long)batch * t_conc * s * 2 <= dev_sms) s *= 2;
+  }
+  while (s > 1 && (n % s || (n / s) % 16)) s /= 2;
+  return s;
+}
+
 int panel_priority() {
   static int p = [] {
     int lo = 0, hi = 0;
@@ -222,17 +243,22 @@ __device__ __forceinline__ void lu_solve_col(const double2 (*lu)[NB + 1], const 
 // Each warp takes 8-column tiles (2 x 4 complex m8n8k4 steps, 4 real DMMAs each).
 // dst != nullptr: V[j][col] -> dst[col * dld + j]; otherwise V overwrites Vs in place
 // (a warp reads all of its tile before writing it).
+// Tiles: [t0, t1) (t1 < 0: every tile), plus [x0, x1) when it lies outside that range.
 template <int NB>
 __device__ __forceinline__ void apply_pinv_dmma(const double2 (*pinv)[NB + 1], double2* sv, int svld, int n,
-                                                double2* __restrict__ dst, int dld) {
+                                                double2* __restrict__ dst, int dld, int t0 = 0, int t1 = -1,
+                                                int x0 = 0, int x1 = 0) {
   const int lane = threadIdx.x & 31, warp = threadIdx.x >> 5;
   const int lr = lane >> 2, lc = lane & 3;
+  if (t1 < 0) t1 = n / 8;
+  const int nown = t1 - t0, nx = (x1 > x0 && (x0 >= t1 || x1 <= t0)) ? x1 - x0 : 0;
   double2 af[2][NB / 4];
 #pragma unroll
   for (int mt = 0; mt < 2; ++mt)
 #pragma unroll
     for (int ks = 0; ks < NB / 4; ++ks) af[mt][ks] = pinv[mt * 8 + lr][ks * 4 + lc];
-  for (int nt = warp; nt < n / 8; nt += PT / 32) {
+  for (int it = warp; it < nown + nx; it += PT / 32) {
+    const int nt = it < nown ? t0 + it : x0 + (it - nown);
     double2 bv[NB / 4];
 #pragma unroll
     for (int ks = 0; ks < NB / 4; ++ks) bv[ks] = sv[(ks * 4 + lc) * svld + nt * 8 + lr];
@@ -736,19 +762,32 @@ __global__ void __launch_bounds__(PT, 1)
 // with Wz2 = M2[:,K2] (-I on P2) and V2 = Pinv2 Vs2. Rows <= RPT * PT for both panels.
 // (Capping it at 168 registers -- 12 B of spills -- so that a GEMM CTA of the other
 // stream group can share its SM measured no better on B200: 577-579 vs 575 ms per step.)
+//
+// split > 1 (small batches, n <= PT): `split` CTAs per matrix. Every CTA factors both
+// panels itself (same inputs, same code: identical pivots and LU bits) and keeps its own
+// copies of the active-row lists and of M2 in shared memory; the column-parallel tails
+// (Vs staging, V1, Vs2, V2) and the row-parallel ones (Wz, row mask, output scatters) are
+// split: CTA s owns columns and rows [s n/split, (s+1) n/split). Global scratch is written
+// by its owner only (lmap, piv and the status by CTA 0), so no two CTAs write one word.
 template <int NB, int RPT>
 __global__ void __launch_bounds__(PT, 1)
     gj_pair_kernel(const double2* __restrict__ cur0, long long ld, long long bstride, int n, int n_true, int k,
-                   int last, GjScratch S, int* __restrict__ status0, BatchIdx bi, int pre2) {
+                   int last, GjScratch S, int* __restrict__ status0, BatchIdx bi, int pre2, int split) {
   constexpr int W2 = 2 * NB;
-  extern __shared__ __align__(16) double2 sv[];  // NB x (n + 2): Vs1 / V1, then Vs2 / V2; then sv2
+  // dynamic smem: NB x (n + 2) Vs1 / V1, then Vs2 / V2; then sv2 (pre2); then M2 (split > 1)
+  extern __shared__ __align__(16) double2 sv[];
   double2* const sv2 = pre2 ? sv + NB * (n + 2) : nullptr;  // NB x (n + 2): pivot rows P2 of M
+  double2* const m2s = sv + (pre2 ? 2 : 1) * NB * (n + 2);   // [NB][n] panel 2's input (split > 1)
   __shared__ PanelSmem<NB, RPT> sm;
   __shared__ double2 s_pinv[NB][NB + 1];
   __shared__ double2 s_uinv[NB];
   __shared__ double2 s_wz1p2[NB][NB + 1];  // Wz1 on the rows P2
   __shared__ int s_src1[NB], s_src2[NB];
-  const int tid = threadIdx.x, b = blockIdx.x;
+  __shared__ int s_next[RPT * PT];  // panel 1's new active list (lmap[k .. n)), as seen by this CTA
+  __shared__ int s_lmap[RPT * PT];  // last step: the final row map lmap[0 .. n)
+  const int tid = threadIdx.x, b = blockIdx.x / split, part = blockIdx.x % split;
+  const bool own_all = split == 1, lead = part == 0;
+  const int cw = n / split, c0 = part * cw, c1 = c0 + cw;  // this CTA's columns and rows
   const double2* __restrict__ cur = cur0 + (k == 0 ? bi.off(b) : (long long)b * bstride);
   int* __restrict__ status = status0 + bi.sidx(b);
   const int k2 = k + NB, svld = n + 2;
@@ -756,7 +795,9 @@ __global__ void __launch_bounds__(PT, 1)
   int* __restrict__ rowmask = S.rowmask + (long long)b * n;
   double2* __restrict__ wz = S.wz + (long long)b * n * W2;  // [W2][n], ld n
   double2* __restrict__ vb = S.vbuf + (long long)b * W2 * n;  // [n][W2], ld W2
-  if (k == 0 && tid == 0) S.amax[b] = 0ull;  // the first GJ GEMM accumulates max |a|^2
+  if (k == 0 && tid == 0 && lead) S.amax[b] = 0ull;  // the first GJ GEMM accumulates max |a|^2
+  if (last && !own_all)
+    for (int i = tid; i < k; i += PT) s_lmap[i] = lmap[i];
   ZDBG(10)
 
   // Both panels run through the same loop body (one copy of the unrolled elimination
@@ -766,14 +807,15 @@ __global__ void __launch_bounds__(PT, 1)
     const int kk = ph ? k2 : k, rows = n - kk;
     int* s_src = ph ? s_src2 : s_src1;
     // panel 1 reads M[:,K1]; panel 2 reads its input M2[:,K2], computed into wz[NB..2NB)
-    const double2* src = ph ? wz + (long long)NB * n : cur + (long long)k * ld;
+    // (or this CTA's shared copy)
+    const double2* src = ph ? (own_all ? wz + (long long)NB * n : m2s) : cur + (long long)k * ld;
     const long long sld = ph ? n : ld;
     double2 a[RPT][NB];
 #pragma unroll
     for (int i = 0; i < RPT; ++i) {
       const int t = tid + i * PT;
       const bool ok = t < rows;
-      const int phys = ok ? active_row(lmap, kk, t) : 0;
+      const int phys = ok ? (ph && !own_all ? s_next[NB + t] : active_row(lmap, kk, t)) : 0;
       if (ok) sm.act[t] = phys;
 #pragma unroll
       for (int c = 0; c < NB; ++c) a[i][c] = ok ? src[(long long)c * sld + phys] : make_double2(0.0, 0.0);
@@ -783,28 +825,40 @@ __global__ void __launch_bounds__(PT, 1)
     ZDBG(12 + 10 * ph)
     if (tid < NB) {
       const double2 d = sm.lu[tid][tid];
-      S.piv[(long long)b * n + kk + tid] = hypot(d.x, d.y);  // kernels.hpp:149-158, tested at the end
+      if (lead) S.piv[(long long)b * n + kk + tid] = hypot(d.x, d.y);  // kernels.hpp:149-158, tested at the end
       s_uinv[tid] = crcp_fast(d);
       s_src[tid] = sm.act[sm.map[tid]];
     }
-    for (int r = tid; r < rows; r += PT) lmap[kk + r] = sm.act[sm.map[r]];
+    for (int r = tid; r < rows; r += PT) {
+      const int p = sm.act[sm.map[r]];
+      if (lead) lmap[kk + r] = p;
+      if (!own_all) {
+        if (ph == 0) s_next[r] = p;
+        if (last) s_lmap[kk + r] = p;
+      }
+    }
     __syncthreads();
     ZDBG(13 + 10 * ph)
     if (ph == 1) {
-      for (int e = tid; e < NB * NB; e += PT) s_wz1p2[e / NB][e % NB] = wz[(long long)(e % NB) * n + s_src2[e / NB]];
+      // Wz1 on P2 = M[P2, K1] (P2 holds no P1 row)
+      for (int e = tid; e < NB * NB; e += PT) s_wz1p2[e / NB][e % NB] = cur[(long long)(k + e % NB) * ld + s_src2[e / NB]];
       __syncthreads();
-      for (int e = tid; e < NB * NB; e += PT) {  // rows P2: 0 in Wz1, -I in Wz2, 0 in C
-        const int j = e / NB, c = e % NB;
-        wz[(long long)c * n + s_src2[j]] = make_double2(0.0, 0.0);
-        wz[(long long)(NB + c) * n + s_src2[j]] = make_double2(j == c ? -1.0 : 0.0, 0.0);
-        if (c == 0) rowmask[s_src2[j]] = -1;
+      for (int e = tid; e < NB * NB; e += PT) {  // rows P2: 0 in Wz1, -I in Wz2, 0 in C (by the row's owner)
+        const int j = e / NB, c = e % NB, r = s_src2[j];
+        if (r < c0 || r >= c1) continue;
+        wz[(long long)c * n + r] = make_double2(0.0, 0.0);
+        wz[(long long)(NB + c) * n + r] = make_double2(j == c ? -1.0 : 0.0, 0.0);
+        if (c == 0) rowmask[r] = -1;
       }
     }
     ZDBG(14 + 10 * ph)
-    // the pivot rows of M this panel needs (Vs1 into sv; panel 2's raw rows into sv2)
-    // are copied asynchronously so that the loads overlap the pivot-block inverse
+    // the pivot rows of M this panel needs (Vs1 into sv: this CTA's columns and K2; panel
+    // 2's raw rows into sv2: this CTA's columns) are copied asynchronously so that the
+    // loads overlap the pivot-block inverse
     for (int col = tid; col < n; col += PT) {
       const bool k1c = col >= k && col < k2, k2c = col >= k2 && col < k2 + NB;
+      const bool mine = col >= c0 && col < c1;
+      if (!(mine || (ph == 0 && k2c))) continue;
       double2* dst = ph ? sv2 : sv;
 #pragma unroll
       for (int j = 0; j < NB; ++j) {
@@ -823,6 +877,7 @@ __global__ void __launch_bounds__(PT, 1)
     ZDBG(16)
     if (S.subst) {  // sv = V1 = U1^{-1} L1^{-1} Vs1, column by column (panel 1's LU is still in sm.lu)
       for (int col = tid; col < n; col += PT) {
+        if (!((col >= c0 && col < c1) || (col >= k2 && col < k2 + NB))) continue;
         double2 x[NB];
 #pragma unroll
         for (int j = 0; j < NB; ++j) x[j] = sv[j * svld + col];
@@ -831,24 +886,28 @@ __global__ void __launch_bounds__(PT, 1)
         for (int j = 0; j < NB; ++j) sv[j * svld + col] = x[j];
       }
     } else {
-      apply_pinv_dmma<NB>(s_pinv, sv, svld, n, nullptr, 0);  // sv = V1
+      apply_pinv_dmma<NB>(s_pinv, sv, svld, n, nullptr, 0, c0 / 8, c1 / 8, k2 / 8, (k2 + NB) / 8);  // sv = V1
     }
     __syncthreads();
     ZDBG(17)
-    // Wz1 (every row) and panel 2's input M2[:,K2] (every row), one row per thread
+    // Wz1 and panel 2's input M2[:,K2], one row per thread: every row for this CTA's
+    // panel-2 factorisation, the global copies (the GEMM's operands) for its own rows
     for (int r = tid; r < n; r += PT) {
       int j1 = -1;
 #pragma unroll
       for (int q = 0; q < NB; ++q)
         if (s_src1[q] == r) j1 = q;
+      const bool mine = r >= c0 && r < c1;
       double2 w[NB], m2[NB];
 #pragma unroll
       for (int c = 0; c < NB; ++c) {
         w[c] = j1 >= 0 ? make_double2(j1 == c ? -1.0 : 0.0, 0.0) : cur[(long long)(k + c) * ld + r];
         m2[c] = j1 >= 0 ? make_double2(0.0, 0.0) : cur[(long long)(k2 + c) * ld + r];
       }
+      if (mine) {
 #pragma unroll
-      for (int c = 0; c < NB; ++c) wz[(long long)c * n + r] = w[c];
+        for (int c = 0; c < NB; ++c) wz[(long long)c * n + r] = w[c];
+      }
 #pragma unroll 1
       for (int q = 0; q < NB; ++q) {
         double2 wq = w[0];
@@ -859,23 +918,29 @@ __global__ void __launch_bounds__(PT, 1)
 #pragma unroll
         for (int c = 0; c < NB; ++c) m2[c] = cfma(nq, sv[q * svld + k2 + c], m2[c]);
       }
+      if (mine) {
 #pragma unroll
-      for (int c = 0; c < NB; ++c) wz[(long long)(NB + c) * n + r] = m2[c];
-      rowmask[r] = j1 >= 0 ? -1 : r;
+        for (int c = 0; c < NB; ++c) wz[(long long)(NB + c) * n + r] = m2[c];
+        rowmask[r] = j1 >= 0 ? -1 : r;
+      }
+      if (!own_all) {
+#pragma unroll
+        for (int c = 0; c < NB; ++c) m2s[(long long)c * n + r] = m2[c];
+      }
     }
     __syncthreads();
     ZDBG(18)
   }
-  // per column: V1 (0 on K2) -> vb rows 0..NB-1; Vs2 replaces V1 in sv
-  for (int col = tid; col < n; col += PT) {
+  // per column of this CTA: V1 (0 on K2) -> vb rows 0..NB-1; Vs2 replaces V1 in sv
+  for (int col = c0 + tid; col < c1; col += PT) {
     double2 v1[NB], x[NB];
-    const bool c1 = col >= k && col < k2, c2 = col >= k2 && col < k2 + NB;
+    const bool c1c = col >= k && col < k2, c2 = col >= k2 && col < k2 + NB;
 #pragma unroll
     for (int j = 0; j < NB; ++j) {
       v1[j] = sv[j * svld + col];
       vb[(long long)col * W2 + j] = c2 ? make_double2(0.0, 0.0) : v1[j];
       x[j] = c2 ? make_double2(col - k2 == j ? 1.0 : 0.0, 0.0)
-                : (c1 ? make_double2(0.0, 0.0) : (pre2 ? sv2[j * svld + col] : cur[(long long)col * ld + s_src2[j]]));
+                : (c1c ? make_double2(0.0, 0.0) : (pre2 ? sv2[j * svld + col] : cur[(long long)col * ld + s_src2[j]]));
     }
     if (!c2) {
 #pragma unroll 1
@@ -895,7 +960,7 @@ __global__ void __launch_bounds__(PT, 1)
   __syncthreads();
   ZDBG(26)
   if (S.subst) {  // V2 = U2^{-1} L2^{-1} Vs2 -> vb rows NB..2NB-1
-    for (int col = tid; col < n; col += PT) {
+    for (int col = c0 + tid; col < c1; col += PT) {
       double2 x[NB];
 #pragma unroll
       for (int j = 0; j < NB; ++j) x[j] = sv[j * svld + col];
@@ -904,26 +969,29 @@ __global__ void __launch_bounds__(PT, 1)
       for (int j = 0; j < NB; ++j) vb[(long long)col * W2 + NB + j] = x[j];
     }
   } else {
-    apply_pinv_dmma<NB>(s_pinv, sv, svld, n, vb + NB, W2);  // V2 -> vb rows NB..2NB-1
+    apply_pinv_dmma<NB>(s_pinv, sv, svld, n, vb + NB, W2, c0 / 8, c1 / 8);  // V2 -> vb rows NB..2NB-1
   }
   ZDBG(27)
-  if (last) {  // output scatters: row lmap[i] -> i, column c -> lmap[c]
+  if (last) {  // output scatters: row lmap[i] -> i, column c -> lmap[c] (this CTA's i)
     // (gathering the last GEMM's C and Wz rows through lmap instead, so that it writes
     // whole rows in order, measured slower on B200: 101 vs 87 us per launch)
     int* __restrict__ rowscat = S.rowscat + (long long)b * n;
     int* __restrict__ colmap = S.colmap + (long long)b * n;
-    for (int i = tid; i < n; i += PT) {
-      const int p = lmap[i];
+    if (!own_all) __syncthreads();  // s_lmap complete
+    for (int i = c0 + tid; i < c1; i += PT) {
+      const int p = own_all ? lmap[i] : s_lmap[i];
       rowscat[p] = i;
       colmap[i] = p;
     }
   }
   __syncthreads();
-  if (last) final_status(S, b, n, n_true, status);
+  if (last && lead) final_status(S, b, n, n_true, status);
   ZDBG(28)
 }
 
 }  // namespace
+
+void zinv_set_concurrency(int groups) { t_conc = groups < 1 ? 1 : groups; }
 
 extern "C" int bbsi_debug_zinv(long long* out) { return (int)cudaMemcpyFromSymbol(out, g_zinv_dbg, sizeof(long long) * 64); }
 
@@ -950,11 +1018,14 @@ cudaError_t zinv_batched2(double2* M, long long ld, long long bstride, int n, in
   cudaError_t e;
   if ((e = set_max_dyn_smem((const void*)gj_panel_kernel<kNB>, smem))) return e;
   const size_t rows_smem = size_t(nb) * (n + 2) * sizeof(double2);  // Vs staging of the tail
+  const int split = pair_split(n, batch);
+  const size_t m2_smem = split > 1 ? size_t(nb) * n * sizeof(double2) : 0;  // per-CTA M2 (split pair)
   {
     const void* fns[4] = {(const void*)gj_panel_rows_kernel<kNB, 1>, (const void*)gj_panel_rows_kernel<kNB, 2>,
                           (const void*)gj_pair_kernel<kNB, 1>, (const void*)gj_pair_kernel<kNB, 2>};
     for (int i = 0; i < 4; ++i)
-      if ((e = set_max_dyn_smem(fns[i], (i >= 2 && pair_pre2(n) ? 2 : 1) * rows_smem))) return e;
+      if ((e = set_max_dyn_smem(fns[i], (i >= 2 && pair_pre2(n) ? 2 : 1) * rows_smem + (i >= 2 ? m2_smem : 0))))
+        return e;
   }
   const long long nn = (long long)n * n;
   // panel steps: two panels per step (pair kernel, one rank-2nb GEMM) wherever both
@@ -985,9 +1056,13 @@ cudaError_t zinv_batched2(double2* M, long long ld, long long bstride, int n, in
       const int pre2 = pair_pre2(n) ? 1 : 0;
       if (pair && pre2) cfg.dynamicSmemBytes = 2 * rows_smem;  // Vs staging + panel 2's pivot rows
       if (pair && rows <= PT) {
-        e = cudaLaunchKernelEx(&cfg, gj_pair_kernel<kNB, 1>, cur, cld, cbs, n, n_true, k, last, S, status, bi, pre2);
+        cfg.gridDim = dim3(batch * split);
+        cfg.dynamicSmemBytes += m2_smem;
+        e = cudaLaunchKernelEx(&cfg, gj_pair_kernel<kNB, 1>, cur, cld, cbs, n, n_true, k, last, S, status, bi, pre2,
+                               split);
       } else if (pair) {
-        e = cudaLaunchKernelEx(&cfg, gj_pair_kernel<kNB, 2>, cur, cld, cbs, n, n_true, k, last, S, status, bi, pre2);
+        e = cudaLaunchKernelEx(&cfg, gj_pair_kernel<kNB, 2>, cur, cld, cbs, n, n_true, k, last, S, status, bi, pre2,
+                               1);
       } else if (kind != 2 && rows <= PT) {
         e = cudaLaunchKernelEx(&cfg, gj_panel_rows_kernel<kNB, 1>, cur, cld, cbs, n, n_true, k, last, S, status, bi);
       } else if (kind != 2 && rows <= 2 * PT) {

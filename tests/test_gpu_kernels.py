@@ -78,6 +78,33 @@ def test_zinv_matches_numpy(gpu, n, n_true, batch):
         assert res <= 1e-11, res
 
 
+@pytest.mark.parametrize("n,batch", [(128, 3), (256, 5)])
+def test_zinv_split_pair_bit_identical(gpu, n, batch, monkeypatch):
+    """The pair panel with several CTAs per matrix (BBSI_PANEL_SPLIT; the default for small
+    batches) factors every panel redundantly and splits only the V / Wz tails: the result,
+    the row interchanges and the singular-pivot status are bit-identical to one CTA."""
+    from paper_2605_19910_b200._native import lib
+
+    torch = _torch()
+    rng = np.random.default_rng(7 * n + batch)
+    a = _rand(rng, batch, n, n)
+    a[batch - 1, :, 17] = 0  # exactly singular last matrix
+    outs = {}
+    for split in (1, 2, 4, 8):
+        monkeypatch.setenv("BBSI_PANEL_SPLIT", str(split))
+        da = _dev(a)
+        st = np.zeros(batch, dtype=np.int32)
+        rc = lib().bbsi_cuda_zinv_dev(n, n, batch, C.c_void_p(da.data_ptr()), n, n * n,
+                                      st.ctypes.data_as(C.c_void_p), C.c_void_p(0))
+        assert rc == 0
+        torch.cuda.synchronize()
+        outs[split] = (da.cpu().numpy(), st.copy())
+    for split in (2, 4, 8):
+        assert np.array_equal(outs[split][1], outs[1][1])
+        assert np.array_equal(outs[split][0][: batch - 1].view(np.uint64), outs[1][0][: batch - 1].view(np.uint64))
+    assert (outs[1][1][: batch - 1] == -1).all() and outs[1][1][batch - 1] >= 0
+
+
 def test_zinv_flags_singular(gpu):
     from paper_2605_19910_b200._native import lib
 
