@@ -52,6 +52,9 @@ def parse():
     p.add_argument("--no-cpu-baseline", action="store_true")
     p.add_argument("--domains", type=int, default=0, help="configs 4/5: DDRGF domains (0 = 32 / 8, at least world)")
     p.add_argument("--no-traffic", action="store_true", help="skip the ncu DRAM-traffic probe of the dominant kernel")
+    p.add_argument("--levels", type=int, nargs="*", default=None,
+                   help="configs 4/5: the DomainPlan's later levels s2_levels[1..] (nested interface system; "
+                        "default: DDRGF_LEVELS[config])")
     p.add_argument("--chunk", type=int, default=0, help="energy chunk of the e2e path (0 = library default: ~32 energies per chunk from 48 energies up)")
     return p.parse_args()
 
@@ -183,6 +186,8 @@ def workload_config(cfg, n_energies: int) -> dict:
                    "L2-resident workload (below the 126 MB L2; not flushed)")}
 
 
+# DomainPlan levels above the first (ddrgf.hpp:18-32, 363-369) the DDRGF arm uses by default
+DDRGF_LEVELS = {4: (), 5: ()}
 SUBCHAIN = {4: 1024, 5: 48}  # leading layers of the reference's bounded single-energy sample (DDRGF configs)
 
 
@@ -548,9 +553,11 @@ def run_ddrgf(args, rank, world, local_rank):
     comm = Dd.NcclComm()
     diag = A[:, 1].diagonal(dim1=-2, dim2=-1)
 
+    levels = tuple(args.levels) if args.levels is not None else DDRGF_LEVELS[args.config]
+
     def solve_energy(z):
         diag.copy_((complex(z) - hd) - sig[:, None])  # (z - h) - sigma: the generator's order
-        Dd.ddrgf_nccl(comm, A, G, l, b, s2)
+        Dd.ddrgf_nccl(comm, A, G, l, b, s2, levels)
 
     def step():
         for z in zs:
@@ -588,10 +595,10 @@ def run_ddrgf(args, rank, world, local_rank):
                 if world == 1:
                     from paper_2605_19910_b200 import bbsi as B
 
-                    B.ddrgf_slots(Ah.numpy(), Gh.numpy(), l, b, [s2])
+                    B.ddrgf_slots(Ah.numpy(), Gh.numpy(), l, b, [s2, *levels])
                 else:
                     A.copy_(Ah, non_blocking=True)
-                    Dd.ddrgf_nccl(comm, A, G, l, b, s2)
+                    Dd.ddrgf_nccl(comm, A, G, l, b, s2, levels)
                     Gh.copy_(G, non_blocking=True)
                     torch.cuda.synchronize()
 
@@ -646,7 +653,8 @@ def run_ddrgf(args, rank, world, local_rank):
                 "higher_is_better": True, "scaling": "strong", "vs_baseline": None, "dtype": "c128 (f64)",
                 "data": "synthetic (seeded Dyson generator, csrc/dyson_gen.h)",
                 "config": workload_config(cfg, n_e),
-                "solver": f"stabilised ddrgf, {len(Dd.partition(l, s2))} domains (s2 = {s2}), NCCL inside the library",
+                "solver": f"stabilised ddrgf, {len(Dd.partition(l, s2))} domains (DomainPlan s2_levels = "
+                          f"{[s2, *levels]}), NCCL inside the library",
                 "parallelism": f"ddrgf domains over {world} rank(s)",
                 "energies_per_s": n_e / (ms_step * 1e-3), "tflops_rgf_equivalent": tflops,
                 "gpu_launches": int(launches), "clocks": clocks, "roofline": roofline, "e2e": e2e,

@@ -175,6 +175,11 @@ int bbsi_cuda_ddrgf_rank_layers(int l, int s2, int nranks, int rank, int* t0, in
  * status (a singular pivot anywhere is reported on all ranks). */
 int bbsi_cuda_ddrgf_rank_dev(void* comm, int l, int bs, int s2, const double* dA_loc, double* dG_loc,
                              int* fail_layer, void* stream);
+/* The same with a multi-level DomainPlan (ddrgf.hpp:18-32, 363-369): ranks own level-0
+ * tasks of s2_levels[0]; the interface system every rank solves redundantly after the
+ * packet all-gather is nested over s2_levels[1..]. */
+int bbsi_cuda_ddrgf_rank_plan_dev(void* comm, int l, int bs, const int* s2_levels, int n_levels, const double* dA_loc,
+                                  double* dG_loc, int* fail_layer, void* stream);
 /* bbsi::ddrgf (ddrgf.hpp:420-428) over ngpu GPUs of this process (devices: NULL = 0..ngpu-1):
  * ncclCommInitAll, one host thread per GPU, domains sharded as above. Same arguments and
  * results as bbsi_cuda_ddrgf_z. */

@@ -50,6 +50,7 @@ SIGNATURES = {
     "bbsi_cuda_nccl_comm_destroy": (None, [_vp]),
     "bbsi_cuda_ddrgf_rank_layers": (_i, [_i, _i, _i, _i, _ip, _ip, _ip, _ip]),
     "bbsi_cuda_ddrgf_rank_dev": (_i, [_vp, _i, _i, _i, _vp, _vp, _vp, _vp]),
+    "bbsi_cuda_ddrgf_rank_plan_dev": (_i, [_vp, _i, _i, _vp, _i, _vp, _vp, _vp, _vp]),
     "bbsi_cuda_ddrgf_multi_z": (_i, [_i, _i, _i, _vp, _vp, _vp, _i, _i, _i, _i, _vp, _vp, _vp, _vp]),
     "bbsi_cuda_dyson_rgf_multi_z": (_i, [_i, _i, _i, _i, _vp, _vp, _vp, _vp, _vp, _i, _i, _vp]),
     "bbsi_cuda_rgf_many_z": (_i, [_i, _i, _i, _vp, _i, _vp, _vp, _vp, _vp]),

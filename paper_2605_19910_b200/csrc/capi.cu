@@ -1347,9 +1347,14 @@ int bbsi_cuda_ddrgf_rank_layers(int l, int s2, int nranks, int rank, int* t0, in
 
 int bbsi_cuda_ddrgf_rank_dev(void* comm, int l, int bs, int s2, const double* dA_loc, double* dG_loc, int* fail_layer,
                              void* stream) {
+  return bbsi_cuda_ddrgf_rank_plan_dev(comm, l, bs, &s2, 1, dA_loc, dG_loc, fail_layer, stream);
+}
+
+int bbsi_cuda_ddrgf_rank_plan_dev(void* comm, int l, int bs, const int* s2_levels, int n_levels, const double* dA_loc,
+                                  double* dG_loc, int* fail_layer, void* stream) {
   if (fail_layer) *fail_layer = -1;
-  int one = s2;
-  if (int rc = validate_ddrgf(l, 1, bs, nullptr, &one, 1, 1, 1)) return rc;
+  if (int rc = validate_ddrgf(l, 1, bs, nullptr, s2_levels, n_levels, 1, 1)) return rc;
+  const int s2 = s2_levels[0];
   if (bs % 64) return fail(BBSI_INVALID_ARGUMENT, "resident API requires bs % 64 == 0");
   if (int rc = device_ok()) return rc;
   std::string err;
@@ -1364,7 +1369,7 @@ int bbsi_cuda_ddrgf_rank_dev(void* comm, int l, int bs, int s2, const double* dA
   int fl = -1;
   cudaStream_t s = static_cast<cudaStream_t>(stream);
   cudaError_t e = ddrgf_rank(reinterpret_cast<const double2*>(dA_loc), reinterpret_cast<double2*>(dG_loc), l, bs,
-                             nullptr, s2, t0, t1, ddrgf_gamma0(), x, scr, sb, &fl, s);
+                             nullptr, s2, t0, t1, ddrgf_gamma0(), x, scr, sb, &fl, s, s2_levels + 1, n_levels - 1);
   if (e != cudaSuccess) return err.empty() ? cuda_fail(e, "ddrgf rank") : fail(BBSI_CUDA_ERROR, err);
   CK(cudaStreamSynchronize(s));
   if (fl >= 0) {

@@ -224,10 +224,19 @@ def rank_layers(l: int, s2: int, world: int, rank: int) -> tuple[int, int, int, 
     return tuple(x.value for x in v)
 
 
-def ddrgf_nccl(comm: NcclComm, A_loc, G_loc, l: int, b: int, s2: int):
+def ddrgf_nccl(comm: NcclComm, A_loc, G_loc, l: int, b: int, s2: int, levels_above=()):
     """This rank's part of the domain-sharded DDRGF with NCCL inside the library
-    (bbsi_cuda_ddrgf_rank_dev): A_loc / G_loc are the rank's band rows (rank_layers)."""
+    (bbsi_cuda_ddrgf_rank_dev): A_loc / G_loc are the rank's band rows (rank_layers).
+    levels_above: the DomainPlan's later levels s2_levels[1..] (ddrgf.hpp:363-369), which
+    nest the interface system every rank solves (bbsi_cuda_ddrgf_rank_plan_dev)."""
     fail = C.c_int(-1)
-    rc = lib().bbsi_cuda_ddrgf_rank_dev(comm.comm, l, b, s2, _ptr(A_loc), _ptr(G_loc), C.byref(fail), _stream())
+    if levels_above:
+        import numpy as np
+
+        lv = np.array([s2, *levels_above], dtype=np.int32)
+        rc = lib().bbsi_cuda_ddrgf_rank_plan_dev(comm.comm, l, b, lv.ctypes.data_as(C.c_void_p), len(lv),
+                                                 _ptr(A_loc), _ptr(G_loc), C.byref(fail), _stream())
+    else:
+        rc = lib().bbsi_cuda_ddrgf_rank_dev(comm.comm, l, b, s2, _ptr(A_loc), _ptr(G_loc), C.byref(fail), _stream())
     _raise(rc, fail.value)
     return G_loc

@@ -52,6 +52,31 @@ def test_nccl_rank_path_one_rank(gpu):
     assert O.max_block_error(got, O.rgf_tridiag(a)[0]) <= 1e-10
 
 
+def test_nccl_rank_plan_one_rank(gpu):
+    """bbsi_cuda_ddrgf_rank_plan_dev (nested interface levels) through a one-rank NCCL
+    communicator equals the resident multi-level plan entry bit for bit."""
+    import torch
+
+    l, b = 90, 64
+    a = DO.dyson_matrix(DO.hamiltonian(l, 1, b, 9), complex(-0.25, 1e-4), 1)
+    full = torch.from_numpy(np.ascontiguousarray(a.data.transpose(0, 1, 3, 2))).cuda()
+    comm = Dd.NcclComm()
+    try:
+        G = torch.empty_like(full)
+        Dd.ddrgf_nccl(comm, full, G, l, b, 4, levels_above=(3,))
+    finally:
+        comm.close()
+    Gd = torch.empty_like(full)
+    lv = np.array([4, 3], dtype=np.int32)
+    fail = C.c_int(-1)
+    assert lib().bbsi_cuda_ddrgf_plan_dev(l, b, lv.ctypes.data_as(C.c_void_p), 2, C.c_void_p(full.data_ptr()),
+                                          C.c_void_p(Gd.data_ptr()), C.byref(fail), _stream()) == 0
+    torch.cuda.synchronize()
+    assert torch.equal(G, Gd)
+    got = O.Band(a.layout, np.ascontiguousarray(G.cpu().numpy().transpose(0, 1, 3, 2)))
+    assert O.max_block_error(got, O.rgf_tridiag(a)[0]) <= 1e-10
+
+
 def test_ddrgf_multi_one_gpu(gpu):
     """bbsi_cuda_ddrgf_multi_z (one host thread per GPU) with ngpu = 1 == bbsi_cuda_ddrgf_z."""
     m = to_product(DO.dyson_matrix(DO.hamiltonian(40, 1, 48, 8), complex(-0.3, 1e-4), 1))
