@@ -80,6 +80,15 @@ int gj_subst() {
   return (e && atoi(e) == 1) ? 1 : 0;
 }
 
+// Register-resident Gauss-Jordan panels (gj_rows_kernel, n <= 4 PT): the default;
+// BBSI_GJ_ROWS=0 keeps the LU + Pinv pair / tall panels (A/B).
+// Largest cluster (CTAs per matrix) gj_rows_kernel may use: BBSI_GJ_ROWS = 0 (never) .. 4 (n <= 1024, default).
+int gj_rows_max_cl() {
+  const char* e = getenv("BBSI_GJ_ROWS");  // read per call: tests compare both in one process
+  const int v = e ? atoi(e) : 4;
+  return v < 0 ? 0 : (v > 4 ? 4 : v);
+}
+
 // Concurrent inversion batches of this host thread (stream groups of the running sweep).
 thread_local int t_conc = 1;
 
@@ -989,6 +998,298 @@ __global__ void __launch_bounds__(PT, 1)
   ZDBG(28)
 }
 
+
+// ---------------------------------------------------------------------------------------
+// Register-resident Gauss-Jordan panels (round 2, the default for n <= PT).
+//
+// Thread t owns PHYSICAL row t of the matrix for the whole kernel (rows never move, so the
+// panel columns load coalesced with no row map), and instead of factoring the panel
+// (L \ U), forming Pinv from two triangular inverses and multiplying V = Pinv Vs, the
+// elimination itself runs as in-place Gauss-Jordan on all n rows of the n x NB panel:
+//   column j, pivot row p (largest |re|+|im| among the rows not yet used as pivots):
+//     row p:   a[p][j] <- 1/a[p][j],  a[p][c] <- a[p][c] / a[p][j]         (c != j)
+//     row r:   l = a[r][j] / a[p][j], a[r][j] <- -l, a[r][c] <- a[r][c] - l a[p][c]
+// After NB columns the registers hold W = E[:, P], the columns of the accumulated row
+// operation E (E M[:, K] = unit columns at the pivot rows): W[P] = Pinv and
+// W[R] = -M[R, K] Pinv, which are exactly the new panel columns of the blocked step
+// (see the header of this file), and for the other columns
+//   M <- M (0 on rows P / cols K) + W Vs,   Vs = M[P, :] with the identity in columns K,
+// so the GEMM operands are W (from registers) and the RAW pivot rows: no Pinv, no V
+// product. The active rows see the same operations in the same order as in the LU panel,
+// so pivots are chosen from the same values. The pivot rows are fetched with cp.async as
+// each pivot is resolved (their latency hides behind the remaining columns).
+// Two panels per launch, one rank-2NB update, as in gj_pair_kernel:
+//   M2[:, K2] = M[:, K2] (0 on P1) + W1 Vs1[:, K2]      (per thread: its own row)
+//   Vs2       = M[P2, :] (0 on K1) + W1[P2] Vs1, I on K2
+//   M <- M (0 on rows P1, P2 / cols K1, K2) + [W1 (0 on P2) | W2] [Vs1 (0 on K2); Vs2]
+// Several CTAs per matrix (n > PT): a thread-block cluster of CL CTAs, CTA `rank` owns
+// rows and columns [rank PT, (rank + 1) PT). Every warp pushes its pivot candidate (key,
+// reciprocal, row) into the same slot of EVERY CTA's shared memory (DSMEM stores), the
+// per-column barrier becomes a cluster barrier (release / acquire), and every CTA then
+// resolves the same pivot from the CL * 8 slots. Everything else is local to the owner.
+template <int CL>
+__device__ __forceinline__ void gj_sync() {
+  if constexpr (CL == 1)
+    __syncthreads();
+  else
+    asm volatile("barrier.cluster.arrive.release.aligned;\n\tbarrier.cluster.wait.acquire.aligned;\n" ::: "memory");
+}
+__device__ __forceinline__ unsigned dsmem_addr(const void* p, unsigned rank) {
+  const unsigned a = (unsigned)__cvta_generic_to_shared(p);
+  unsigned r;
+  asm volatile("mapa.shared::cluster.u32 %0, %1, %2;\n" : "=r"(r) : "r"(a), "r"(rank));
+  return r;
+}
+__device__ __forceinline__ void st_cluster(unsigned addr, double2 v) {
+  asm volatile("st.shared::cluster.v2.f64 [%0], {%1, %2};\n" ::"r"(addr), "d"(v.x), "d"(v.y) : "memory");
+}
+__device__ __forceinline__ void st_cluster(unsigned addr, unsigned v) {
+  asm volatile("st.shared::cluster.u32 [%0], %1;\n" ::"r"(addr), "r"(v) : "memory");
+}
+__device__ __forceinline__ double2 ld_cluster(unsigned addr) {
+  double2 v;
+  asm volatile("ld.shared::cluster.v2.f64 {%0, %1}, [%2];\n" : "=d"(v.x), "=d"(v.y) : "r"(addr) : "memory");
+  return v;
+}
+
+template <int NB, int CL>
+struct GjRowSmem {
+  static constexpr int NC = CL * (PT / 32);  // candidate slots: one per warp of the cluster
+  __align__(16) unsigned cand_k[2][NC];
+  double2 cand_r[2][NC];              // reciprocal of the candidate
+  double2 cand_p[2][NC];              // the candidate itself (deferred negligible-pivot test)
+  __align__(16) double2 cand_row[2][NC][NB];
+  double2 w1p2[NB][NB + 1];           // W1 on the rows P2
+  __align__(16) double2 vk2[NB][NB];  // Vs1[:, K2]
+  double2 pv[2][NB];                  // the pivots
+  int src[2][NB];                     // physical pivot rows of the two panels
+  unsigned char used[PT];             // own rows used as pivots by earlier steps
+};
+
+template <int NB, int CL>
+__global__ void __launch_bounds__(PT, 1)
+    gj_rows_kernel(const double2* __restrict__ cur0, long long ld, long long bstride, int n, int n_true, int k, int last,
+                   GjScratch S, int* __restrict__ status0, BatchIdx bi) {
+  static_assert(PT == NB * NB, "one thread per entry of the NB x NB blocks");
+  static_assert(CL * PT <= int(KEY_IMASK) + 1, "row numbers must fit the pivot key");
+  constexpr int W2 = 2 * NB;
+  constexpr int svld = PT + 2;
+  extern __shared__ __align__(16) double2 sv[];  // own columns of Vs1 [NB][svld]; of the raw rows P2; W1 [NB][PT]
+  double2* const sv2 = sv + NB * svld;
+  double2* const w1s = sv2 + NB * svld;  // W1 of the own rows (panel 1's result, kept out of the registers)
+  __shared__ GjRowSmem<NB, CL> sm;
+  const int tid = threadIdx.x, lane = tid & 31, warp = tid >> 5;
+  const int b = blockIdx.x / CL, rank = blockIdx.x % CL;
+  const int grow = rank * PT + tid;  // this thread's row (and column) of the matrix
+  const int slot = rank * (PT / 32) + warp;
+  const double2* __restrict__ cur = cur0 + (k == 0 ? bi.off(b) : (long long)b * bstride);
+  int* __restrict__ status = status0 + bi.sidx(b);
+  const int k2 = k + NB;
+  int* __restrict__ lmap = S.lmap + (long long)b * n;
+  int* __restrict__ rowmask = S.rowmask + (long long)b * n;
+  double2* __restrict__ wz = S.wz + (long long)b * n * W2;    // [W2][n], ld n
+  double2* __restrict__ vb = S.vbuf + (long long)b * W2 * n;  // [n][W2], ld W2
+  if (k == 0 && tid == 0 && rank == 0) S.amax[b] = 0ull;  // the first GJ GEMM accumulates max |a|^2
+  sm.used[tid] = 0;
+  __syncthreads();
+  for (int i = tid; i < k; i += PT) {
+    const int p = lmap[i] - rank * PT;
+    if (p >= 0 && p < PT) sm.used[p] = 1;
+  }
+  gj_sync<CL>();  // (CL > 1: every CTA of the cluster is resident before the first remote store)
+  const bool inrow = grow < n;
+  bool cand = inrow && !sm.used[tid];
+  bool piv1 = false, piv2 = false;
+  double2 a[NB];
+#pragma unroll
+  for (int c = 0; c < NB; ++c) a[c] = inrow ? cur[(long long)(k + c) * ld + grow] : make_double2(0.0, 0.0);
+
+  // Both panels run through one loop body (the kernel executes its code once per SM).
+#pragma unroll 1
+  for (int ph = 0; ph < 2; ++ph) {
+    const int kk = ph ? k2 : k;
+    double2* const dst = ph ? sv2 : sv;
+    const bool kcol = ph == 0 && grow >= kk && grow < kk + NB;  // identity columns of Vs1
+    auto publish_key = [&](int par, int J) -> bool {
+      const unsigned key = cand ? piv_key(a[J], grow) : 0u;
+      const unsigned wk = __reduce_max_sync(0xffffffffu, key);
+      if (lane == 0) {
+        if constexpr (CL == 1) {
+          sm.cand_k[par][slot] = wk;
+        } else {
+#pragma unroll
+          for (int r = 0; r < CL; ++r) st_cluster(dsmem_addr(&sm.cand_k[par][slot], r), wk);
+        }
+      }
+      const bool win = wk != 0 && key == wk;
+      if (win) {
+        const double2 rc = crcp_fast(a[J]);
+        if constexpr (CL == 1) {
+          sm.cand_r[par][slot] = rc;
+          sm.cand_p[par][slot] = a[J];
+        } else {
+#pragma unroll
+          for (int r = 0; r < CL; ++r) {
+            st_cluster(dsmem_addr(&sm.cand_r[par][slot], r), rc);
+            st_cluster(dsmem_addr(&sm.cand_p[par][slot], r), a[J]);
+          }
+        }
+      }
+      return win;
+    };
+    auto publish_row = [&](int par) {
+      if constexpr (CL == 1) {
+#pragma unroll
+        for (int c = 0; c < NB; ++c) sm.cand_row[par][slot][c] = a[c];
+      } else {
+#pragma unroll
+        for (int r = 0; r < CL; ++r) {
+          const unsigned base = dsmem_addr(&sm.cand_row[par][slot][0], r);
+#pragma unroll
+          for (int c = 0; c < NB; ++c) st_cluster(base + c * (unsigned)sizeof(double2), a[c]);
+        }
+      }
+    };
+    if (publish_key(0, 0)) publish_row(0);
+#pragma unroll
+    for (int j = 0; j < NB; ++j) {
+      const int par = j & 1;
+      gj_sync<CL>();
+      unsigned best = 0;
+#pragma unroll
+      for (int q = 0; q < GjRowSmem<NB, CL>::NC / 4; ++q) {
+        const uint4 kq = reinterpret_cast<const uint4*>(sm.cand_k[par])[q];
+        best = max(max(best, max(kq.x, kq.y)), max(kq.z, kq.w));
+      }
+      const int tj = int(KEY_IMASK - (best & KEY_IMASK));  // the pivot's row of the matrix
+      const int qw = tj >> 5;                               // and its candidate slot
+      const double2 rcp = sm.cand_r[par][qw];
+      const bool isp = grow == tj;
+      if (isp) {  // this row is pivot j of the panel
+        cand = false;
+        if (ph)
+          piv2 = true;
+        else
+          piv1 = true;
+      }
+      if (tid == 0) {
+        sm.src[ph][j] = tj;
+        sm.pv[ph][j] = sm.cand_p[par][qw];
+      }
+      if (inrow && !kcol) cp_async16(&dst[j * svld + tid], &cur[(long long)grow * ld + tj]);
+      if (ph == 0 && tid < NB) cp_async16(&sm.vk2[j][tid], &cur[(long long)(k2 + tid) * ld + tj]);
+      double2 l = cmul(a[j], rcp);
+      if (isp) l = make_double2(-rcp.x, -rcp.y);
+      a[j] = make_double2(-l.x, -l.y);
+      auto update = [&](int c) {
+        const double2 u = sm.cand_row[par][qw][c];
+        double2 x = isp ? make_double2(0.0, 0.0) : a[c];
+        x.x = fma(-l.x, u.x, fma(l.y, u.y, x.x));
+        x.y = fma(-l.x, u.y, fma(-l.y, u.x, x.y));
+        a[c] = x;
+      };
+      if (j + 1 < NB) {
+        update(j + 1);
+        const bool win = publish_key(par ^ 1, j + 1);
+#pragma unroll
+        for (int c = 0; c < NB; ++c)
+          if (c != j && c != j + 1) update(c);
+        if (win) publish_row(par ^ 1);
+      } else {
+#pragma unroll
+        for (int c = 0; c < NB; ++c)
+          if (c != j) update(c);
+      }
+    }
+    cp_async_commit();
+    if (kcol) {
+#pragma unroll
+      for (int j = 0; j < NB; ++j) sv[j * svld + tid] = make_double2(grow - kk == j ? 1.0 : 0.0, 0.0);
+    }
+    if (ph == 1) break;
+    // panel 2's input, this thread's row: M2[r, K2] = M[r, K2] (0 on P1) + W1[r] Vs1[:, K2]
+    double2 a1[NB];
+#pragma unroll
+    for (int c = 0; c < NB; ++c) {
+      a1[c] = a[c];
+      w1s[c * PT + tid] = a[c];
+      a[c] = (inrow && !piv1) ? cur[(long long)(k2 + c) * ld + grow] : make_double2(0.0, 0.0);
+    }
+    cp_async_wait<0>();
+    __syncthreads();
+#pragma unroll 1
+    for (int q = 0; q < NB; ++q) {
+      double2 wq = a1[0];
+#pragma unroll
+      for (int u = 1; u < NB; ++u)
+        if (u == q) wq = a1[u];
+#pragma unroll
+      for (int c = 0; c < NB; ++c) a[c] = cfma(wq, sm.vk2[q][c], a[c]);
+    }
+  }
+  // ---- the GEMM operands and the bookkeeping
+  if (inrow) {
+#pragma unroll
+    for (int c = 0; c < NB; ++c) {
+      wz[(long long)c * n + grow] = piv2 ? make_double2(0.0, 0.0) : w1s[c * PT + tid];
+      wz[(long long)(NB + c) * n + grow] = a[c];
+    }
+    rowmask[grow] = (piv1 || piv2) ? -1 : grow;
+  }
+  cp_async_wait<0>();
+  __syncthreads();
+  {  // W1 on the rows P2, from the rows' owners
+    const int j = tid / NB, c = tid % NB, r = sm.src[1][j];
+    if constexpr (CL == 1)
+      sm.w1p2[j][c] = w1s[c * PT + r];
+    else
+      sm.w1p2[j][c] = ld_cluster(dsmem_addr(&w1s[c * PT + (r % PT)], unsigned(r / PT)));
+  }
+  gj_sync<CL>();  // (CL > 1: no CTA leaves while a peer still reads its shared memory)
+  if (rank == 0 && tid < W2) {
+    const int ph = tid / NB, j = tid % NB;
+    const double2 d = sm.pv[ph][j];
+    S.piv[(long long)b * n + k + tid] = hypot(d.x, d.y);  // kernels.hpp:149-158, tested at the end
+    lmap[k + tid] = sm.src[ph][j];
+  }
+  if (inrow) {  // this thread's column: Vs1 (0 on K2) and Vs2 = M[P2, col] (0 on K1) + W1[P2] Vs1[:, col], I on K2
+    const int col = grow;
+    const bool c1c = col >= k && col < k2, c2 = col >= k2 && col < k2 + NB;
+    double2 v1[NB], x[NB];
+#pragma unroll
+    for (int j = 0; j < NB; ++j) {
+      v1[j] = sv[j * svld + tid];
+      x[j] = c2 ? make_double2(col - k2 == j ? 1.0 : 0.0, 0.0) : (c1c ? make_double2(0.0, 0.0) : sv2[j * svld + tid]);
+    }
+    if (!c2) {
+#pragma unroll 1
+      for (int q = 0; q < NB; ++q) {
+        double2 vq = v1[0];
+#pragma unroll
+        for (int u = 1; u < NB; ++u)
+          if (u == q) vq = v1[u];
+#pragma unroll
+        for (int j = 0; j < NB; ++j) x[j] = cfma(sm.w1p2[j][q], vq, x[j]);
+      }
+    }
+#pragma unroll
+    for (int j = 0; j < NB; ++j) {
+      vb[(long long)col * W2 + j] = c2 ? make_double2(0.0, 0.0) : v1[j];
+      vb[(long long)col * W2 + NB + j] = x[j];
+    }
+  }
+  if (last && inrow) {  // output scatters: row lmap[i] -> i, column c -> lmap[c]
+    int* __restrict__ rowscat = S.rowscat + (long long)b * n;
+    int* __restrict__ colmap = S.colmap + (long long)b * n;
+    const int i = grow;
+    const int p = i < k ? lmap[i] : (i < k2 ? sm.src[0][i - k] : sm.src[1][i - k2]);
+    rowscat[p] = i;
+    colmap[i] = p;
+  }
+  __syncthreads();
+  if (last && rank == 0) final_status(S, b, n, n_true, status);
+}
+
 }  // namespace
 
 void zinv_set_concurrency(int groups) { t_conc = groups < 1 ? 1 : groups; }
@@ -1031,6 +1332,16 @@ cudaError_t zinv_batched2(double2* M, long long ld, long long bstride, int n, in
   // panel steps: two panels per step (pair kernel, one rank-2nb GEMM) wherever both
   // fit the register kernel; single panels otherwise (tall panels, BBSI_PANEL=2/3)
   const int kind = panel_kind();
+  // gj_rows_kernel: one thread per row, CL = ceil(n / PT) CTAs (a cluster) per matrix; n % 64 == 0, so every
+  // step is a pair of panels
+  const int cl = (n + PT - 1) / PT;
+  const bool rowsgj = kind == 1 && cl <= gj_rows_max_cl();
+  const size_t gjr_smem = (2 * size_t(nb) * (PT + 2) + size_t(nb) * PT) * sizeof(double2);  // Vs1, raw rows P2, W1
+  const void* gjr_fn = cl == 1   ? (const void*)gj_rows_kernel<kNB, 1>
+                       : cl == 2 ? (const void*)gj_rows_kernel<kNB, 2>
+                       : cl == 3 ? (const void*)gj_rows_kernel<kNB, 3>
+                                 : (const void*)gj_rows_kernel<kNB, 4>;
+  if (rowsgj && (e = set_max_dyn_smem(gjr_fn, gjr_smem))) return e;
   for (int k = 0; k < n;) {
     const int rows = n - k;
     const bool pair = kind == 1 && rows <= 2 * PT && k + 2 * nb <= n;
@@ -1055,7 +1366,22 @@ cudaError_t zinv_batched2(double2* M, long long ld, long long bstride, int n, in
       cfg.numAttrs = 1;
       const int pre2 = pair_pre2(n) ? 1 : 0;
       if (pair && pre2) cfg.dynamicSmemBytes = 2 * rows_smem;  // Vs staging + panel 2's pivot rows
-      if (pair && rows <= PT) {
+      if (rowsgj) {
+        cfg.dynamicSmemBytes = gjr_smem;
+        cfg.gridDim = dim3(batch * cl);
+        cudaLaunchAttribute attr2[2];
+        attr2[0] = attr_[0];
+        attr2[1].id = cudaLaunchAttributeClusterDimension;
+        attr2[1].val.clusterDim.x = cl;
+        attr2[1].val.clusterDim.y = 1;
+        attr2[1].val.clusterDim.z = 1;
+        cfg.attrs = attr2;
+        cfg.numAttrs = cl > 1 ? 2 : 1;
+        int kl = last;
+        void* args[] = {(void*)&cur, (void*)&cld, (void*)&cbs, (void*)&n, (void*)&n_true, (void*)&k, (void*)&kl,
+                        (void*)&S, (void*)&status, (void*)&bi};
+        e = cudaLaunchKernelExC(&cfg, gjr_fn, args);
+      } else if (pair && rows <= PT) {
         cfg.gridDim = dim3(batch * split);
         cfg.dynamicSmemBytes += m2_smem;
         e = cudaLaunchKernelEx(&cfg, gj_pair_kernel<kNB, 1>, cur, cld, cbs, n, n_true, k, last, S, status, bi, pre2,
@@ -1086,7 +1412,7 @@ cudaError_t zinv_batched2(double2* M, long long ld, long long bstride, int n, in
       p.M = n;
       p.N = n;
       p.K = kw;
-      p.alpha = make_double2(-1.0, 0.0);
+      p.alpha = make_double2(rowsgj ? 1.0 : -1.0, 0.0);  // gj_rows_kernel: M + W Vs; LU panels: M - Wz V
       p.beta = make_double2(1.0, 0.0);
       p.A = ZOp{S.wz + so * n * kw, n, 64, 64LL * n, (long long)n * kw};
       p.B = ZOp{S.vbuf + so * kw * n, kw, 64, 64LL * kw, (long long)kw * n};

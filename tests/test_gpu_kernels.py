@@ -90,6 +90,7 @@ def test_zinv_split_pair_bit_identical(gpu, n, batch, monkeypatch):
     a = _rand(rng, batch, n, n)
     a[batch - 1, :, 17] = 0  # exactly singular last matrix
     outs = {}
+    monkeypatch.setenv("BBSI_GJ_ROWS", "0")  # the LU + Pinv pair panel (gj_rows_kernel has no split)
     for split in (1, 2, 4, 8):
         monkeypatch.setenv("BBSI_PANEL_SPLIT", str(split))
         da = _dev(a)
@@ -103,6 +104,44 @@ def test_zinv_split_pair_bit_identical(gpu, n, batch, monkeypatch):
         assert np.array_equal(outs[split][1], outs[1][1])
         assert np.array_equal(outs[split][0][: batch - 1].view(np.uint64), outs[1][0][: batch - 1].view(np.uint64))
     assert (outs[1][1][: batch - 1] == -1).all() and outs[1][1][batch - 1] >= 0
+
+
+@pytest.mark.parametrize("n,n_true,batch", [(64, 64, 3), (128, 100, 3), (192, 192, 2), (256, 256, 5), (320, 300, 2), (512, 512, 3),
+                                            (768, 768, 2), (1024, 1000, 2)])
+def test_zinv_rows_panel_vs_lu_panel(gpu, n, n_true, batch, monkeypatch):
+    """gj_rows_kernel (in-place Gauss-Jordan on register rows, raw pivot rows as the GEMM
+    operand; one CTA for n <= 256, a cluster of ceil(n / 256) CTAs up to n = 1024) against the LU + Pinv pair panel (BBSI_GJ_ROWS=0)
+    and numpy: same inverse to rounding (inverse <= 1e-12 as tests/test_dense_kernels.cpp:
+    97-134), same singular-pivot status."""
+    from paper_2605_19910_b200._native import lib
+
+    torch = _torch()
+    rng = np.random.default_rng(11 * n + batch)
+    a = _rand(rng, batch, n, n)
+    a[:, n_true:, :] = 0
+    a[:, :, n_true:] = 0
+    for i in range(batch):
+        a[i, n_true:, n_true:] = np.eye(n - n_true)
+    a[batch - 1, :, 9] = 0  # exactly singular last matrix
+    outs = {}
+    for mode in ("1", "0"):
+        monkeypatch.setenv("BBSI_GJ_ROWS", mode)
+        da = _dev(a)
+        st = np.zeros(batch, dtype=np.int32)
+        rc = lib().bbsi_cuda_zinv_dev(n, n_true, batch, C.c_void_p(da.data_ptr()), n, n * n,
+                                      st.ctypes.data_as(C.c_void_p), C.c_void_p(0))
+        assert rc == 0
+        torch.cuda.synchronize()
+        outs[mode] = (_host(da), st.copy())
+    assert np.array_equal(outs["1"][1], outs["0"][1])
+    assert (outs["1"][1][: batch - 1] == -1).all() and outs["1"][1][batch - 1] == 9
+    for i in range(batch - 1):
+        ref = np.linalg.inv(a[i])
+        for mode in ("1", "0"):
+            err = np.linalg.norm(outs[mode][0][i] - ref) / np.linalg.norm(ref)
+            assert err <= 1e-12, (mode, err)
+        res = np.linalg.norm(a[i] @ outs["1"][0][i] - np.eye(n)) / np.sqrt(n)
+        assert res <= 1e-11, res
 
 
 def test_zinv_flags_singular(gpu):
