@@ -1317,20 +1317,6 @@ cudaError_t zinv_batched2(double2* M, long long ld, long long bstride, int n, in
   S.subst = gj_subst();
   const size_t smem = size_t(nb) * (n + 1) * sizeof(double2) + 3 * size_t(n) * sizeof(int);
   cudaError_t e;
-  if ((e = set_max_dyn_smem((const void*)gj_panel_kernel<kNB>, smem))) return e;
-  const size_t rows_smem = size_t(nb) * (n + 2) * sizeof(double2);  // Vs staging of the tail
-  const int split = pair_split(n, batch);
-  const size_t m2_smem = split > 1 ? size_t(nb) * n * sizeof(double2) : 0;  // per-CTA M2 (split pair)
-  {
-    const void* fns[4] = {(const void*)gj_panel_rows_kernel<kNB, 1>, (const void*)gj_panel_rows_kernel<kNB, 2>,
-                          (const void*)gj_pair_kernel<kNB, 1>, (const void*)gj_pair_kernel<kNB, 2>};
-    for (int i = 0; i < 4; ++i)
-      if ((e = set_max_dyn_smem(fns[i], (i >= 2 && pair_pre2(n) ? 2 : 1) * rows_smem + (i >= 2 ? m2_smem : 0))))
-        return e;
-  }
-  const long long nn = (long long)n * n;
-  // panel steps: two panels per step (pair kernel, one rank-2nb GEMM) wherever both
-  // fit the register kernel; single panels otherwise (tall panels, BBSI_PANEL=2/3)
   const int kind = panel_kind();
   // gj_rows_kernel: one thread per row, CL = ceil(n / PT) CTAs (a cluster) per matrix; n % 64 == 0, so every
   // step is a pair of panels
@@ -1342,6 +1328,20 @@ cudaError_t zinv_batched2(double2* M, long long ld, long long bstride, int n, in
                        : cl == 3 ? (const void*)gj_rows_kernel<kNB, 3>
                                  : (const void*)gj_rows_kernel<kNB, 4>;
   if (rowsgj && (e = set_max_dyn_smem(gjr_fn, gjr_smem))) return e;
+  const size_t rows_smem = size_t(nb) * (n + 2) * sizeof(double2);  // Vs staging of the tail
+  const int split = pair_split(n, batch);
+  const size_t m2_smem = split > 1 ? size_t(nb) * n * sizeof(double2) : 0;  // per-CTA M2 (split pair)
+  if (!rowsgj) {  // LU panels: tall (shared-memory) panel, register panels, pair panels
+    if ((e = set_max_dyn_smem((const void*)gj_panel_kernel<kNB>, smem))) return e;
+    const void* fns[4] = {(const void*)gj_panel_rows_kernel<kNB, 1>, (const void*)gj_panel_rows_kernel<kNB, 2>,
+                          (const void*)gj_pair_kernel<kNB, 1>, (const void*)gj_pair_kernel<kNB, 2>};
+    for (int i = 0; i < 4; ++i)  // (the M2 copy: split pair, RPT = 1, only)
+      if ((e = set_max_dyn_smem(fns[i], (i >= 2 && pair_pre2(n) ? 2 : 1) * rows_smem + (i == 2 ? m2_smem : 0))))
+        return e;
+  }
+  const long long nn = (long long)n * n;
+  // LU panel steps: two panels per step (pair kernel, one rank-2nb GEMM) wherever both
+  // fit the register kernel; single panels otherwise (tall panels, BBSI_PANEL=2/3)
   for (int k = 0; k < n;) {
     const int rows = n - k;
     const bool pair = kind == 1 && rows <= 2 * PT && k + 2 * nb <= n;

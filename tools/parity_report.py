@@ -17,10 +17,15 @@ def main():
                 r["_file"] = path
                 rows.append(r)
     floors5 = {r["energy_index"]: r for r in rows if r.get("kind") == "floor"}
+    floors5b = {r["energy_index"]: r for r in rows if r.get("kind") == "floor_blas"}
     solves = [r for r in rows if "max" in r]
-    for r in solves:  # config 5: the input-noise floors come from the CPU floor run
-        if r["config"] == 5 and r.get("floor") is None and r["energy_index"] in floors5:
-            r["floor"] = floors5[r["energy_index"]]["floor"]
+    for r in solves:  # config 5: the floors come from the CPU floor runs (input noise; BLAS kernel order)
+        e = r["energy_index"]
+        if r["config"] == 5 and (e in floors5 or e in floors5b):
+            fi = floors5[e]["floor"] if e in floors5 else None
+            fb = floors5b[e]["floor"] if e in floors5b else None
+            r["floor_input"], r["floor_blas"] = fi, fb
+            r["floor"] = max(x for x in (fi, fb) if x is not None)
             r["verdict"] = "<= 1e-10" if r["max"] <= 1e-10 else ("<= floor" if r["max"] <= r["floor"] else "ABOVE")
     by = collections.defaultdict(list)
     for r in solves:
@@ -44,16 +49,19 @@ def main():
             fi, fb = r.get("floor_input"), r.get("floor_blas")
             fl = r.get("floor")
             fs = (f"{fl:.2e} ({fi:.2e} / {fb:.2e})" if fi is not None and fb is not None
-                  else (f"{fl:.2e}" if fl is not None else "—"))
+                  else (f"{fl:.2e} ({fi:.2e} / —)" if fi is not None else (f"{fl:.2e}" if fl is not None else "—")))
             print(f"| {r['energy_index']} | {r['E']:+.4f} | {r['max']:.2e} | {r['median']:.2e} | {fs} | "
                   f"{r['residual_gpu']:.1e} / {r['residual_ref']:.1e} | {r.get('verdict', '?')} |")
         print()
     if floors5:
-        print("### config 5 input-noise floors (CPU, streaming reference on A vs perturbed A)\n")
-        print("| energy | E | floor | median |")
+        print("### config 5 floors (CPU, streaming reference): input noise (A vs one-ulp-perturbed A) and BLAS "
+              "kernel order (native AVX-512 kernels vs OPENBLAS_CORETYPE=Haswell, tools/cfg5_blas_floor.py)\n")
+        print("| energy | E | input floor (max / median) | BLAS floor (max / median) |")
         print("|---|---|---|---|")
         for e, r in sorted(floors5.items()):
-            print(f"| {e} | {r['E']:+.4f} | {r['floor']:.2e} | {r['floor_median']:.2e} |")
+            fb = floors5b.get(e)
+            fbs = f"{fb['floor']:.2e} / {fb['floor_median']:.2e}" if fb else "—"
+            print(f"| {e} | {r['E']:+.4f} | {r['floor']:.2e} / {r['floor_median']:.2e} | {fbs} |")
 
 
 if __name__ == "__main__":
