@@ -107,6 +107,20 @@ __device__ __forceinline__ double2 crcp_fast(double2 a) {
   return make_double2(xr * inv, -xi * inv);
 }
 
+// crcp_fast without branches or library calls (every lane of a warp can run it next to
+// independent work): the power-of-two scale comes from the exponent bits of max(|re|, |im|)
+// (scaled to [1, 2) instead of frexp's [0.5, 1): both scalings are exact, so the result has
+// the same bits as crcp_fast for normal inputs). Zero maps to zero.
+__device__ __forceinline__ double2 crcp_lanes(double2 a) {
+  const double m = fmax(fabs(a.x), fabs(a.y));
+  const long long e = (__double_as_longlong(m) >> 52) & 0x7ff;
+  const double sc = __longlong_as_double((0x7feLL - e) << 52);
+  const double xr = a.x * sc, xi = a.y * sc;
+  const double inv = rcp_nr(fma(xr, xr, xi * xi)) * sc;
+  const bool z = m == 0.0;
+  return make_double2(z ? 0.0 : xr * inv, z ? 0.0 : -xi * inv);
+}
+
 // DMMA: D(8x8) += A(8x4, row) * B(4x8, col), FP64. One lane holds A[l/4][l%4],
 // B[l%4][l/4] and C[l/4][2*(l%4) + {0,1}].
 __device__ __forceinline__ void dmma884(double (&c)[2], double a, double b) {

@@ -1073,7 +1073,7 @@ __global__ void __launch_bounds__(PT, 1)
   static_assert(PT == NB * NB, "one thread per entry of the NB x NB blocks");
   static_assert(CL * PT <= int(KEY_IMASK) + 1, "row numbers must fit the pivot key");
   constexpr int W2 = 2 * NB;
-  constexpr int svld = PT + 2;
+  constexpr int svld = PT + 1;  // odd: a warp reading one column of the [NB][svld] tiles hits 32 distinct bank groups
   extern __shared__ __align__(16) double2 sv[];  // own columns of Vs1 [NB][svld]; of the raw rows P2; W1 [NB][PT]
   double2* const sv2 = sv + NB * svld;
   double2* const w1s = sv2 + NB * svld;  // W1 of the own rows (panel 1's result, kept out of the registers)
@@ -1090,6 +1090,7 @@ __global__ void __launch_bounds__(PT, 1)
   double2* __restrict__ wz = S.wz + (long long)b * n * W2;    // [W2][n], ld n
   double2* __restrict__ vb = S.vbuf + (long long)b * W2 * n;  // [n][W2], ld W2
   if (k == 0 && tid == 0 && rank == 0) S.amax[b] = 0ull;  // the first GJ GEMM accumulates max |a|^2
+  ZDBG(30)
   sm.used[tid] = 0;
   __syncthreads();
   for (int i = tid; i < k; i += PT) {
@@ -1103,6 +1104,7 @@ __global__ void __launch_bounds__(PT, 1)
   double2 a[NB];
 #pragma unroll
   for (int c = 0; c < NB; ++c) a[c] = inrow ? cur[(long long)(k + c) * ld + grow] : make_double2(0.0, 0.0);
+  ZDBG(31)
 
   // Both panels run through one loop body (the kernel executes its code once per SM).
 #pragma unroll 1
@@ -1110,8 +1112,12 @@ __global__ void __launch_bounds__(PT, 1)
     const int kk = ph ? k2 : k;
     double2* const dst = ph ? sv2 : sv;
     const bool kcol = ph == 0 && grow >= kk && grow < kk + NB;  // identity columns of Vs1
-    auto publish_key = [&](int par, int J) -> bool {
+    // this warp's best candidate for column J: the key now (lane 0); from the winning lane its
+    // reciprocal, the pivot itself and the row once the row is fully updated. Every lane forms the
+    // reciprocal of its own entry (branch-free), so its dependent chain overlaps the other updates
+    auto publish_key = [&](int par, int J, double2& rc) -> bool {
       const unsigned key = cand ? piv_key(a[J], grow) : 0u;
+      rc = crcp_lanes(a[J]);
       const unsigned wk = __reduce_max_sync(0xffffffffu, key);
       if (lane == 0) {
         if constexpr (CL == 1) {
@@ -1121,21 +1127,19 @@ __global__ void __launch_bounds__(PT, 1)
           for (int r = 0; r < CL; ++r) st_cluster(dsmem_addr(&sm.cand_k[par][slot], r), wk);
         }
       }
-      const bool win = wk != 0 && key == wk;
-      if (win) {
-        const double2 rc = crcp_fast(a[J]);
-        if constexpr (CL == 1) {
-          sm.cand_r[par][slot] = rc;
-          sm.cand_p[par][slot] = a[J];
-        } else {
+      return wk != 0 && key == wk;
+    };
+    auto publish_rcp = [&](int par, int J, double2 rc) {
+      if constexpr (CL == 1) {
+        sm.cand_r[par][slot] = rc;
+        sm.cand_p[par][slot] = a[J];
+      } else {
 #pragma unroll
-          for (int r = 0; r < CL; ++r) {
-            st_cluster(dsmem_addr(&sm.cand_r[par][slot], r), rc);
-            st_cluster(dsmem_addr(&sm.cand_p[par][slot], r), a[J]);
-          }
+        for (int r = 0; r < CL; ++r) {
+          st_cluster(dsmem_addr(&sm.cand_r[par][slot], r), rc);
+          st_cluster(dsmem_addr(&sm.cand_p[par][slot], r), a[J]);
         }
       }
-      return win;
     };
     auto publish_row = [&](int par) {
       if constexpr (CL == 1) {
@@ -1150,7 +1154,14 @@ __global__ void __launch_bounds__(PT, 1)
         }
       }
     };
-    if (publish_key(0, 0)) publish_row(0);
+    {
+      double2 rc;
+      if (publish_key(0, 0, rc)) {
+        publish_rcp(0, 0, rc);
+        publish_row(0);
+      }
+    }
+  ZDBG(32 + 8 * ph)
 #pragma unroll
     for (int j = 0; j < NB; ++j) {
       const int par = j & 1;
@@ -1165,12 +1176,14 @@ __global__ void __launch_bounds__(PT, 1)
       const int qw = tj >> 5;                               // and its candidate slot
       const double2 rcp = sm.cand_r[par][qw];
       const bool isp = grow == tj;
-      if (isp) {  // this row is pivot j of the panel
+      if (isp) {  // this row is pivot j of the panel: its own row comes back from cand_row scaled by 1/p
         cand = false;
         if (ph)
           piv2 = true;
         else
           piv1 = true;
+#pragma unroll
+        for (int c = 0; c < NB; ++c) a[c] = make_double2(0.0, 0.0);
       }
       if (tid == 0) {
         sm.src[ph][j] = tj;
@@ -1183,18 +1196,22 @@ __global__ void __launch_bounds__(PT, 1)
       a[j] = make_double2(-l.x, -l.y);
       auto update = [&](int c) {
         const double2 u = sm.cand_row[par][qw][c];
-        double2 x = isp ? make_double2(0.0, 0.0) : a[c];
+        double2 x = a[c];
         x.x = fma(-l.x, u.x, fma(l.y, u.y, x.x));
         x.y = fma(-l.x, u.y, fma(-l.y, u.x, x.y));
         a[c] = x;
       };
       if (j + 1 < NB) {
         update(j + 1);
-        const bool win = publish_key(par ^ 1, j + 1);
+        double2 rc;
+        const bool win = publish_key(par ^ 1, j + 1, rc);
 #pragma unroll
         for (int c = 0; c < NB; ++c)
           if (c != j && c != j + 1) update(c);
-        if (win) publish_row(par ^ 1);
+        if (win) {
+          publish_rcp(par ^ 1, j + 1, rc);
+          publish_row(par ^ 1);
+        }
       } else {
 #pragma unroll
         for (int c = 0; c < NB; ++c)
@@ -1202,30 +1219,28 @@ __global__ void __launch_bounds__(PT, 1)
       }
     }
     cp_async_commit();
+  ZDBG(33 + 8 * ph)
     if (kcol) {
 #pragma unroll
       for (int j = 0; j < NB; ++j) sv[j * svld + tid] = make_double2(grow - kk == j ? 1.0 : 0.0, 0.0);
     }
     if (ph == 1) break;
     // panel 2's input, this thread's row: M2[r, K2] = M[r, K2] (0 on P1) + W1[r] Vs1[:, K2]
-    double2 a1[NB];
 #pragma unroll
     for (int c = 0; c < NB; ++c) {
-      a1[c] = a[c];
       w1s[c * PT + tid] = a[c];
       a[c] = (inrow && !piv1) ? cur[(long long)(k2 + c) * ld + grow] : make_double2(0.0, 0.0);
     }
     cp_async_wait<0>();
     __syncthreads();
+  ZDBG(34)
 #pragma unroll 1
     for (int q = 0; q < NB; ++q) {
-      double2 wq = a1[0];
-#pragma unroll
-      for (int u = 1; u < NB; ++u)
-        if (u == q) wq = a1[u];
+      const double2 wq = w1s[q * PT + tid];
 #pragma unroll
       for (int c = 0; c < NB; ++c) a[c] = cfma(wq, sm.vk2[q][c], a[c]);
     }
+  ZDBG(35)
   }
   // ---- the GEMM operands and the bookkeeping
   if (inrow) {
@@ -1236,6 +1251,7 @@ __global__ void __launch_bounds__(PT, 1)
     }
     rowmask[grow] = (piv1 || piv2) ? -1 : grow;
   }
+  ZDBG(44)
   cp_async_wait<0>();
   __syncthreads();
   {  // W1 on the rows P2, from the rows' owners
@@ -1246,38 +1262,42 @@ __global__ void __launch_bounds__(PT, 1)
       sm.w1p2[j][c] = ld_cluster(dsmem_addr(&w1s[c * PT + (r % PT)], unsigned(r / PT)));
   }
   gj_sync<CL>();  // (CL > 1: no CTA leaves while a peer still reads its shared memory)
+  ZDBG(45)
   if (rank == 0 && tid < W2) {
     const int ph = tid / NB, j = tid % NB;
     const double2 d = sm.pv[ph][j];
     S.piv[(long long)b * n + k + tid] = hypot(d.x, d.y);  // kernels.hpp:149-158, tested at the end
     lmap[k + tid] = sm.src[ph][j];
   }
-  if (inrow) {  // this thread's column: Vs1 (0 on K2) and Vs2 = M[P2, col] (0 on K1) + W1[P2] Vs1[:, col], I on K2
+  {  // this thread's column: Vs2 = M[P2, col] (0 on K1) + W1[P2] Vs1[:, col], I on K2; it replaces the raw rows in sv2
     const int col = grow;
     const bool c1c = col >= k && col < k2, c2 = col >= k2 && col < k2 + NB;
-    double2 v1[NB], x[NB];
+    double2 x[NB];
 #pragma unroll
-    for (int j = 0; j < NB; ++j) {
-      v1[j] = sv[j * svld + tid];
-      x[j] = c2 ? make_double2(col - k2 == j ? 1.0 : 0.0, 0.0) : (c1c ? make_double2(0.0, 0.0) : sv2[j * svld + tid]);
-    }
-    if (!c2) {
+    for (int j = 0; j < NB; ++j)
+      x[j] = c2 ? make_double2(col - k2 == j ? 1.0 : 0.0, 0.0) : ((c1c || !inrow) ? make_double2(0.0, 0.0) : sv2[j * svld + tid]);
+    if (!c2 && inrow) {
 #pragma unroll 1
       for (int q = 0; q < NB; ++q) {
-        double2 vq = v1[0];
-#pragma unroll
-        for (int u = 1; u < NB; ++u)
-          if (u == q) vq = v1[u];
+        const double2 vq = sv[q * svld + tid];
 #pragma unroll
         for (int j = 0; j < NB; ++j) x[j] = cfma(sm.w1p2[j][q], vq, x[j]);
       }
     }
 #pragma unroll
     for (int j = 0; j < NB; ++j) {
-      vb[(long long)col * W2 + j] = c2 ? make_double2(0.0, 0.0) : v1[j];
-      vb[(long long)col * W2 + NB + j] = x[j];
+      sv2[j * svld + tid] = x[j];
+      if (c2) sv[j * svld + tid] = make_double2(0.0, 0.0);  // Vs1 is 0 on K2 in the combined update
     }
   }
+  __syncthreads();
+  // [Vs1; Vs2] of the own columns -> vb, one warp per column (32 consecutive entries: coalesced)
+#pragma unroll 4
+  for (int i = 0; i < PT / 8; ++i) {
+    const int cl_ = warp + (PT / 32) * i, col = rank * PT + cl_;
+    if (col < n) vb[(long long)col * W2 + lane] = lane < NB ? sv[lane * svld + cl_] : sv2[(lane - NB) * svld + cl_];
+  }
+  ZDBG(46)
   if (last && inrow) {  // output scatters: row lmap[i] -> i, column c -> lmap[c]
     int* __restrict__ rowscat = S.rowscat + (long long)b * n;
     int* __restrict__ colmap = S.colmap + (long long)b * n;
@@ -1288,6 +1308,7 @@ __global__ void __launch_bounds__(PT, 1)
   }
   __syncthreads();
   if (last && rank == 0) final_status(S, b, n, n_true, status);
+  ZDBG(47)
 }
 
 }  // namespace
@@ -1322,7 +1343,7 @@ cudaError_t zinv_batched2(double2* M, long long ld, long long bstride, int n, in
   // step is a pair of panels
   const int cl = (n + PT - 1) / PT;
   const bool rowsgj = kind == 1 && cl <= gj_rows_max_cl();
-  const size_t gjr_smem = (2 * size_t(nb) * (PT + 2) + size_t(nb) * PT) * sizeof(double2);  // Vs1, raw rows P2, W1
+  const size_t gjr_smem = (2 * size_t(nb) * (PT + 1) + size_t(nb) * PT) * sizeof(double2);  // Vs1, raw rows P2, W1
   const void* gjr_fn = cl == 1   ? (const void*)gj_rows_kernel<kNB, 1>
                        : cl == 2 ? (const void*)gj_rows_kernel<kNB, 2>
                        : cl == 3 ? (const void*)gj_rows_kernel<kNB, 3>
@@ -1344,7 +1365,7 @@ cudaError_t zinv_batched2(double2* M, long long ld, long long bstride, int n, in
   // fit the register kernel; single panels otherwise (tall panels, BBSI_PANEL=2/3)
   for (int k = 0; k < n;) {
     const int rows = n - k;
-    const bool pair = kind == 1 && rows <= 2 * PT && k + 2 * nb <= n;
+    const bool pair = rowsgj || (kind == 1 && rows <= 2 * PT && k + 2 * nb <= n);
     const int kw = pair ? 2 * nb : nb;
     const int last = k + kw == n;
     // the first step reads the input block; the working matrix s0 is updated in place
