@@ -1023,10 +1023,13 @@ __global__ void __launch_bounds__(PT, 1)
 //   Vs2       = M[P2, :] (0 on K1) + W1[P2] Vs1, I on K2
 //   M <- M (0 on rows P1, P2 / cols K1, K2) + [W1 (0 on P2) | W2] [Vs1 (0 on K2); Vs2]
 // Several CTAs per matrix (n > PT): a thread-block cluster of CL CTAs, CTA `rank` owns
-// rows and columns [rank PT, (rank + 1) PT). Every warp pushes its pivot candidate (key,
-// reciprocal, row) into the same slot of EVERY CTA's shared memory (DSMEM stores), the
-// per-column barrier becomes a cluster barrier (release / acquire), and every CTA then
-// resolves the same pivot from the CL * 8 slots. Everything else is local to the owner.
+// rows and columns [rank PT, (rank + 1) PT). Every warp pushes its pivot KEY into the same
+// slot of every CTA's shared memory (one DSMEM store per CTA) and keeps its candidate record
+// (row, reciprocal, pivot) local; the per-column barrier becomes a cluster barrier (release /
+// acquire), every CTA resolves the same winner from the CL * 8 keys, and the CTAs that do not
+// own it fetch its record (18 DSMEM loads by 18 threads) from the owner. (Pushing every
+// candidate row to every CTA measured 4.3 k cycles per column on B200 against 1.4 k for one
+// CTA: 54 remote stores per warp and column, 23 of 24 rows never used.)
 template <int CL>
 __device__ __forceinline__ void gj_sync() {
   if constexpr (CL == 1)
@@ -1040,9 +1043,6 @@ __device__ __forceinline__ unsigned dsmem_addr(const void* p, unsigned rank) {
   asm volatile("mapa.shared::cluster.u32 %0, %1, %2;\n" : "=r"(r) : "r"(a), "r"(rank));
   return r;
 }
-__device__ __forceinline__ void st_cluster(unsigned addr, double2 v) {
-  asm volatile("st.shared::cluster.v2.f64 [%0], {%1, %2};\n" ::"r"(addr), "d"(v.x), "d"(v.y) : "memory");
-}
 __device__ __forceinline__ void st_cluster(unsigned addr, unsigned v) {
   asm volatile("st.shared::cluster.u32 [%0], %1;\n" ::"r"(addr), "r"(v) : "memory");
 }
@@ -1052,18 +1052,24 @@ __device__ __forceinline__ double2 ld_cluster(unsigned addr) {
   return v;
 }
 
+template <int NB>
+struct GjCand {  // one warp's pivot candidate
+  double2 row[NB];  // the candidate row (all NB columns of the panel)
+  double2 rcp;      // reciprocal of its entry in the pivot column
+  double2 piv;      // the entry itself (deferred negligible-pivot test)
+};
+
 template <int NB, int CL>
 struct GjRowSmem {
-  static constexpr int NC = CL * (PT / 32);  // candidate slots: one per warp of the cluster
-  __align__(16) unsigned cand_k[2][NC];
-  double2 cand_r[2][NC];              // reciprocal of the candidate
-  double2 cand_p[2][NC];              // the candidate itself (deferred negligible-pivot test)
-  __align__(16) double2 cand_row[2][NC][NB];
-  double2 w1p2[NB][NB + 1];           // W1 on the rows P2
-  __align__(16) double2 vk2[NB][NB];  // Vs1[:, K2]
-  double2 pv[2][NB];                  // the pivots
-  int src[2][NB];                     // physical pivot rows of the two panels
-  unsigned char used[PT];             // own rows used as pivots by earlier steps
+  static constexpr int NC = CL * (PT / 32);  // one key slot per warp of the cluster
+  __align__(16) unsigned cand_k[2][NC];      // keys of every warp of the cluster (pushed by their owners)
+  __align__(16) GjCand<NB> cand[2][PT / 32]; // this CTA's candidates
+  __align__(16) GjCand<NB> pulled;           // CL > 1: the winner's record, fetched from its owner
+  double2 w1p2[NB][NB + 1];                  // W1 on the rows P2
+  __align__(16) double2 vk2[NB][NB];         // Vs1[:, K2]
+  double2 pv[2][NB];                         // the pivots
+  int src[2][NB];                            // physical pivot rows of the two panels
+  unsigned char used[PT];                    // own rows used as pivots by earlier steps
 };
 
 template <int NB, int CL>
@@ -1073,6 +1079,11 @@ __global__ void __launch_bounds__(PT, 1)
   static_assert(PT == NB * NB, "one thread per entry of the NB x NB blocks");
   static_assert(CL * PT <= int(KEY_IMASK) + 1, "row numbers must fit the pivot key");
   constexpr int W2 = 2 * NB;
+#ifdef BBSI_GJ_GATHER_AFTER
+  constexpr bool kGatherInLoop = CL == 1;  // pivot rows fetched as each pivot is resolved, or after the 16 columns
+#else
+  constexpr bool kGatherInLoop = true;
+#endif
   constexpr int svld = PT + 1;  // odd: a warp reading one column of the [NB][svld] tiles hits 32 distinct bank groups
   extern __shared__ __align__(16) double2 sv[];  // own columns of Vs1 [NB][svld]; of the raw rows P2; W1 [NB][PT]
   double2* const sv2 = sv + NB * svld;
@@ -1104,6 +1115,12 @@ __global__ void __launch_bounds__(PT, 1)
   double2 a[NB];
 #pragma unroll
   for (int c = 0; c < NB; ++c) a[c] = inrow ? cur[(long long)(k + c) * ld + grow] : make_double2(0.0, 0.0);
+  // panel 2's raw columns M[:, K2] of the own row, staged in sv2 (free until panel 2's pivot rows arrive, which
+  // land in the same thread's slots); they join panel 1's copy group
+  if (inrow) {
+#pragma unroll
+    for (int c = 0; c < NB; ++c) cp_async16(&sv2[c * svld + tid], &cur[(long long)(k2 + c) * ld + grow]);
+  }
   ZDBG(31)
 
   // Both panels run through one loop body (the kernel executes its code once per SM).
@@ -1130,29 +1147,12 @@ __global__ void __launch_bounds__(PT, 1)
       return wk != 0 && key == wk;
     };
     auto publish_rcp = [&](int par, int J, double2 rc) {
-      if constexpr (CL == 1) {
-        sm.cand_r[par][slot] = rc;
-        sm.cand_p[par][slot] = a[J];
-      } else {
-#pragma unroll
-        for (int r = 0; r < CL; ++r) {
-          st_cluster(dsmem_addr(&sm.cand_r[par][slot], r), rc);
-          st_cluster(dsmem_addr(&sm.cand_p[par][slot], r), a[J]);
-        }
-      }
+      sm.cand[par][warp].rcp = rc;
+      sm.cand[par][warp].piv = a[J];
     };
     auto publish_row = [&](int par) {
-      if constexpr (CL == 1) {
 #pragma unroll
-        for (int c = 0; c < NB; ++c) sm.cand_row[par][slot][c] = a[c];
-      } else {
-#pragma unroll
-        for (int r = 0; r < CL; ++r) {
-          const unsigned base = dsmem_addr(&sm.cand_row[par][slot][0], r);
-#pragma unroll
-          for (int c = 0; c < NB; ++c) st_cluster(base + c * (unsigned)sizeof(double2), a[c]);
-        }
-      }
+      for (int c = 0; c < NB; ++c) sm.cand[par][warp].row[c] = a[c];
     };
     {
       double2 rc;
@@ -1173,8 +1173,19 @@ __global__ void __launch_bounds__(PT, 1)
         best = max(max(best, max(kq.x, kq.y)), max(kq.z, kq.w));
       }
       const int tj = int(KEY_IMASK - (best & KEY_IMASK));  // the pivot's row of the matrix
-      const int qw = tj >> 5;                               // and its candidate slot
-      const double2 rcp = sm.cand_r[par][qw];
+      const int qw = tj >> 5;                               // and its key slot: CTA qw / 8, warp qw % 8
+      const GjCand<NB>* cw = &sm.cand[par][qw % (PT / 32)];
+      if constexpr (CL > 1) {
+        const int owner = qw / (PT / 32);
+        if (owner != rank) {  // (uniform over the CTA) fetch the winner's record from its owner's shared memory
+          if (tid < NB + 2)
+            reinterpret_cast<double2*>(&sm.pulled)[tid] =
+                ld_cluster(dsmem_addr(reinterpret_cast<const double2*>(cw) + tid, unsigned(owner)));
+          __syncthreads();
+          cw = &sm.pulled;
+        }
+      }
+      const double2 rcp = cw->rcp;
       const bool isp = grow == tj;
       if (isp) {  // this row is pivot j of the panel: its own row comes back from cand_row scaled by 1/p
         cand = false;
@@ -1187,15 +1198,17 @@ __global__ void __launch_bounds__(PT, 1)
       }
       if (tid == 0) {
         sm.src[ph][j] = tj;
-        sm.pv[ph][j] = sm.cand_p[par][qw];
+        sm.pv[ph][j] = cw->piv;
       }
-      if (inrow && !kcol) cp_async16(&dst[j * svld + tid], &cur[(long long)grow * ld + tj]);
-      if (ph == 0 && tid < NB) cp_async16(&sm.vk2[j][tid], &cur[(long long)(k2 + tid) * ld + tj]);
+      if constexpr (kGatherInLoop) {
+        if (inrow && !kcol) cp_async16(&dst[j * svld + tid], &cur[(long long)grow * ld + tj]);
+        if (ph == 0 && tid < NB) cp_async16(&sm.vk2[j][tid], &cur[(long long)(k2 + tid) * ld + tj]);
+      }
       double2 l = cmul(a[j], rcp);
       if (isp) l = make_double2(-rcp.x, -rcp.y);
       a[j] = make_double2(-l.x, -l.y);
       auto update = [&](int c) {
-        const double2 u = sm.cand_row[par][qw][c];
+        const double2 u = cw->row[c];
         double2 x = a[c];
         x.x = fma(-l.x, u.x, fma(l.y, u.y, x.x));
         x.y = fma(-l.x, u.y, fma(-l.y, u.x, x.y));
@@ -1218,6 +1231,15 @@ __global__ void __launch_bounds__(PT, 1)
           if (c != j) update(c);
       }
     }
+    if constexpr (!kGatherInLoop) {  // (clusters: copies in flight would stall every release barrier)
+      __syncthreads();
+#pragma unroll
+      for (int j = 0; j < NB; ++j) {
+        const int tj = sm.src[ph][j];
+        if (inrow && !kcol) cp_async16(&dst[j * svld + tid], &cur[(long long)grow * ld + tj]);
+        if (ph == 0 && tid < NB) cp_async16(&sm.vk2[j][tid], &cur[(long long)(k2 + tid) * ld + tj]);
+      }
+    }
     cp_async_commit();
   ZDBG(33 + 8 * ph)
     if (kcol) {
@@ -1227,11 +1249,10 @@ __global__ void __launch_bounds__(PT, 1)
     if (ph == 1) break;
     // panel 2's input, this thread's row: M2[r, K2] = M[r, K2] (0 on P1) + W1[r] Vs1[:, K2]
 #pragma unroll
-    for (int c = 0; c < NB; ++c) {
-      w1s[c * PT + tid] = a[c];
-      a[c] = (inrow && !piv1) ? cur[(long long)(k2 + c) * ld + grow] : make_double2(0.0, 0.0);
-    }
+    for (int c = 0; c < NB; ++c) w1s[c * PT + tid] = a[c];
     cp_async_wait<0>();
+#pragma unroll
+    for (int c = 0; c < NB; ++c) a[c] = (inrow && !piv1) ? sv2[c * svld + tid] : make_double2(0.0, 0.0);
     __syncthreads();
   ZDBG(34)
 #pragma unroll 1
