@@ -80,17 +80,22 @@ int gj_subst() {
   return (e && atoi(e) == 1) ? 1 : 0;
 }
 
+// Concurrent inversion batches of this host thread (stream groups of the running sweep).
+thread_local int t_conc = 1;
+
 // Register-resident Gauss-Jordan panels (gj_rows_kernel, n <= 4 PT): the default;
 // BBSI_GJ_ROWS=0 keeps the LU + Pinv pair / tall panels (A/B).
-// Largest cluster (CTAs per matrix) gj_rows_kernel may use: BBSI_GJ_ROWS = 0 (never) .. 4 (n <= 1024, default).
-int gj_rows_max_cl() {
+// Largest cluster (CTAs per matrix) gj_rows_kernel may use: BBSI_GJ_ROWS = 0 (never) .. 4 (n <= 1024).
+// Unset: 4, except that one or two n <= 256 matrices on their own (a single-energy sweep, DDRGF phase 2)
+// keep the LU pair panel, whose tails split over 8 CTAs per matrix (B200, config 4 single-energy RGF:
+// 1.45 s against 1.58 s).
+int gj_rows_max_cl(int n, int batch) {
   const char* e = getenv("BBSI_GJ_ROWS");  // read per call: tests compare both in one process
-  const int v = e ? atoi(e) : 4;
+  if (!e) return (n <= PT && (long long)batch * t_conc <= 2) ? 0 : 4;
+  const int v = atoi(e);
   return v < 0 ? 0 : (v > 4 ? 4 : v);
 }
 
-// Concurrent inversion batches of this host thread (stream groups of the running sweep).
-thread_local int t_conc = 1;
 
 // CTAs per matrix of the pair panel (BBSI_PANEL_SPLIT, else the largest power of two
 // <= 8 that keeps batch x concurrency x split within one wave of the 148 SMs). Only for
@@ -1362,7 +1367,7 @@ cudaError_t zinv_batched2(double2* M, long long ld, long long bstride, int n, in
   // gj_rows_kernel: one thread per row, CL = ceil(n / PT) CTAs (a cluster) per matrix; n % 64 == 0, so every
   // step is a pair of panels
   const int cl = (n + PT - 1) / PT;
-  const bool rowsgj = kind == 1 && cl <= gj_rows_max_cl();
+  const bool rowsgj = kind == 1 && cl <= gj_rows_max_cl(n, batch);
   const size_t gjr_smem = (2 * size_t(nb) * (PT + 1) + size_t(nb) * PT) * sizeof(double2);  // Vs1, raw rows P2, W1
   const void* gjr_fn = cl == 1   ? (const void*)gj_rows_kernel<kNB, 1>
                        : cl == 2 ? (const void*)gj_rows_kernel<kNB, 2>
