@@ -85,17 +85,18 @@ thread_local int t_conc = 1;
 
 // Register-resident Gauss-Jordan panels (gj_rows_kernel, n <= 4 PT): the default;
 // BBSI_GJ_ROWS=0 keeps the LU + Pinv pair / tall panels (A/B).
-// Largest cluster (CTAs per matrix) gj_rows_kernel may use: BBSI_GJ_ROWS = 0 (never) .. 4 (n <= 1024).
-// Unset: 4, except that one or two n <= 256 matrices on their own (a single-energy sweep, DDRGF phase 2)
-// keep the LU pair panel, whose tails split over 8 CTAs per matrix (B200, config 4 single-energy RGF:
-// 1.45 s against 1.58 s).
+// Largest cluster (CTAs per matrix) gj_rows_kernel may use: BBSI_GJ_ROWS = 0 (never) .. 4 (n <= 1024,
+// default). The choice never depends on the batch: the two panel families round differently, and a
+// solve must give the same bits however its matrices are grouped into launches (stream groups, ranks).
+// (One or two n = 256 matrices on their own are 9 % faster on the LU pair panel, whose tails split over
+// 8 CTAs per matrix: B200, config 4 single-energy RGF, 1.45 s against 1.58 s.)
 int gj_rows_max_cl(int n, int batch) {
+  (void)n;
+  (void)batch;
   const char* e = getenv("BBSI_GJ_ROWS");  // read per call: tests compare both in one process
-  if (!e) return (n <= PT && (long long)batch * t_conc <= 2) ? 0 : 4;
-  const int v = atoi(e);
+  const int v = e ? atoi(e) : 4;
   return v < 0 ? 0 : (v > 4 ? 4 : v);
 }
-
 
 // CTAs per matrix of the pair panel (BBSI_PANEL_SPLIT, else the largest power of two
 // <= 8 that keeps batch x concurrency x split within one wave of the 148 SMs). Only for
