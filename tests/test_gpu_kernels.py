@@ -145,6 +145,29 @@ def test_zinv_rows_panel_vs_lu_panel(gpu, n, n_true, batch, monkeypatch):
         assert res <= 1e-11, res
 
 
+@pytest.mark.parametrize("n", [128, 256, 512, 768])
+def test_zinv_bits_independent_of_batch(gpu, n):
+    """A matrix inverts to the same bits alone and inside a larger launch (the panel family
+    and the cluster size depend on n only): a solve gives the same result however its
+    matrices are grouped into launches (stream groups, ranks, domains)."""
+    from paper_2605_19910_b200._native import lib
+
+    torch = _torch()
+    rng = np.random.default_rng(n + 1)
+    a = _rand(rng, 5, n, n)
+    outs = []
+    for sel in ([0], [0, 1], [0, 1, 2, 3, 4]):
+        da = _dev(a[sel])
+        st = np.zeros(len(sel), dtype=np.int32)
+        rc = lib().bbsi_cuda_zinv_dev(n, n, len(sel), C.c_void_p(da.data_ptr()), n, n * n,
+                                      st.ctypes.data_as(C.c_void_p), C.c_void_p(0))
+        assert rc == 0 and (st == -1).all()
+        torch.cuda.synchronize()
+        outs.append(da.cpu().numpy()[0])
+    assert np.array_equal(outs[0].view(np.uint64), outs[1].view(np.uint64))
+    assert np.array_equal(outs[0].view(np.uint64), outs[2].view(np.uint64))
+
+
 def test_zinv_flags_singular(gpu):
     from paper_2605_19910_b200._native import lib
 
