@@ -1078,8 +1078,19 @@ struct GjRowSmem {
   unsigned char used[PT];                    // own rows used as pivots by earlier steps
 };
 
+// BBSI_GJ_SHARE_SM (build flag, A/B): 168 registers and two staging tiles only (W1 goes through the
+// global Wz operand and, for the panel-2 input, through the free sv2 slots), so that one 128-thread GEMM
+// CTA of another stream group fits next to a panel CTA on the same SM.
+#ifdef BBSI_GJ_SHARE_SM
+#define GJ_ROWS_BOUNDS __maxnreg__(168)
+constexpr bool kW1Smem = false;
+#else
+#define GJ_ROWS_BOUNDS __launch_bounds__(PT, 1)
+constexpr bool kW1Smem = true;
+#endif
+
 template <int NB, int CL>
-__global__ void __launch_bounds__(PT, 1)
+__global__ void GJ_ROWS_BOUNDS
     gj_rows_kernel(const double2* __restrict__ cur0, long long ld, long long bstride, int n, int n_true, int k, int last,
                    GjScratch S, int* __restrict__ status0, BatchIdx bi) {
   static_assert(PT == NB * NB, "one thread per entry of the NB x NB blocks");
@@ -1253,16 +1264,27 @@ __global__ void __launch_bounds__(PT, 1)
     }
     if (ph == 1) break;
     // panel 2's input, this thread's row: M2[r, K2] = M[r, K2] (0 on P1) + W1[r] Vs1[:, K2]
+    if constexpr (kW1Smem) {
 #pragma unroll
-    for (int c = 0; c < NB; ++c) w1s[c * PT + tid] = a[c];
-    cp_async_wait<0>();
+      for (int c = 0; c < NB; ++c) w1s[c * PT + tid] = a[c];
+      cp_async_wait<0>();
 #pragma unroll
-    for (int c = 0; c < NB; ++c) a[c] = (inrow && !piv1) ? sv2[c * svld + tid] : make_double2(0.0, 0.0);
+      for (int c = 0; c < NB; ++c) a[c] = (inrow && !piv1) ? sv2[c * svld + tid] : make_double2(0.0, 0.0);
+    } else {  // W1 -> the Wz operand (global) and, for the loop below, this thread's slots of sv2
+      cp_async_wait<0>();
+#pragma unroll
+      for (int c = 0; c < NB; ++c) {
+        const double2 raw = (inrow && !piv1) ? sv2[c * svld + tid] : make_double2(0.0, 0.0);
+        if (inrow) wz[(long long)c * n + grow] = a[c];
+        sv2[c * svld + tid] = a[c];
+        a[c] = raw;
+      }
+    }
     __syncthreads();
   ZDBG(34)
 #pragma unroll 1
     for (int q = 0; q < NB; ++q) {
-      const double2 wq = w1s[q * PT + tid];
+      const double2 wq = kW1Smem ? w1s[q * PT + tid] : sv2[q * svld + tid];
 #pragma unroll
       for (int c = 0; c < NB; ++c) a[c] = cfma(wq, sm.vk2[q][c], a[c]);
     }
@@ -1272,7 +1294,7 @@ __global__ void __launch_bounds__(PT, 1)
   if (inrow) {
 #pragma unroll
     for (int c = 0; c < NB; ++c) {
-      wz[(long long)c * n + grow] = piv2 ? make_double2(0.0, 0.0) : w1s[c * PT + tid];
+      if constexpr (kW1Smem) wz[(long long)c * n + grow] = piv2 ? make_double2(0.0, 0.0) : w1s[c * PT + tid];
       wz[(long long)(NB + c) * n + grow] = a[c];
     }
     rowmask[grow] = (piv1 || piv2) ? -1 : grow;
@@ -1282,12 +1304,20 @@ __global__ void __launch_bounds__(PT, 1)
   __syncthreads();
   {  // W1 on the rows P2, from the rows' owners
     const int j = tid / NB, c = tid % NB, r = sm.src[1][j];
-    if constexpr (CL == 1)
+    if constexpr (!kW1Smem)
+      sm.w1p2[j][c] = __ldcg(&wz[(long long)c * n + r]);  // written before the last 16 (cluster) barriers
+    else if constexpr (CL == 1)
       sm.w1p2[j][c] = w1s[c * PT + r];
     else
       sm.w1p2[j][c] = ld_cluster(dsmem_addr(&w1s[c * PT + (r % PT)], unsigned(r / PT)));
   }
   gj_sync<CL>();  // (CL > 1: no CTA leaves while a peer still reads its shared memory)
+  if constexpr (!kW1Smem) {  // W1 is 0 on the rows P2 in the combined update (after every read of those rows)
+    if (inrow && piv2) {
+#pragma unroll
+      for (int c = 0; c < NB; ++c) wz[(long long)c * n + grow] = make_double2(0.0, 0.0);
+    }
+  }
   ZDBG(45)
   if (rank == 0 && tid < W2) {
     const int ph = tid / NB, j = tid % NB;
@@ -1369,7 +1399,7 @@ cudaError_t zinv_batched2(double2* M, long long ld, long long bstride, int n, in
   // step is a pair of panels
   const int cl = (n + PT - 1) / PT;
   const bool rowsgj = kind == 1 && cl <= gj_rows_max_cl(n, batch);
-  const size_t gjr_smem = (2 * size_t(nb) * (PT + 1) + size_t(nb) * PT) * sizeof(double2);  // Vs1, raw rows P2, W1
+  const size_t gjr_smem = (2 * size_t(nb) * (PT + 1) + (kW1Smem ? size_t(nb) * PT : 0)) * sizeof(double2);  // Vs1, raw rows P2, W1
   const void* gjr_fn = cl == 1   ? (const void*)gj_rows_kernel<kNB, 1>
                        : cl == 2 ? (const void*)gj_rows_kernel<kNB, 2>
                        : cl == 3 ? (const void*)gj_rows_kernel<kNB, 3>
