@@ -361,7 +361,9 @@ int bbsi_cuda_rgf_many_z(int l, int w, int bs, const int* sizes, int batch, cons
   for (int k = 0; k < batch; ++k) {
     HostBand h = make_host(l, w, bs, sizes, A + 2 * band_h * k);
     pad_band(h, bp, staging);
-    CK(cudaMemcpy(dG + band_d * k, staging.data(), band_d * sizeof(double2), cudaMemcpyHostToDevice));
+    // on the sweep's own (non-blocking) stream: a synchronous cudaMemcpy from pageable memory returns once
+    // the data is staged, before the DMA lands, and orders nothing against a non-blocking stream
+    CK(cudaMemcpyAsync(dG + band_d * k, staging.data(), band_d * sizeof(double2), cudaMemcpyHostToDevice, s));
     if (k == 0) sz = h.sz;
   }
   SweepWork W;

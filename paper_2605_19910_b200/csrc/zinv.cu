@@ -1078,10 +1078,14 @@ struct GjRowSmem {
   unsigned char used[PT];                    // own rows used as pivots by earlier steps
 };
 
-// BBSI_GJ_SHARE_SM (build flag, A/B): 168 registers and two staging tiles only (W1 goes through the
-// global Wz operand and, for the panel-2 input, through the free sv2 slots), so that one 128-thread GEMM
-// CTA of another stream group fits next to a panel CTA on the same SM.
-#ifdef BBSI_GJ_SHARE_SM
+// Resources sized so that one 128-thread GEMM CTA of another stream group fits next to a panel CTA on the
+// same SM: 168 registers (no spills worth naming: 8-24 bytes) and two staging tiles only -- W1 goes
+// through the global Wz operand and, for the panel-2 input, through this thread's free sv2 slots
+// (146 KB of shared memory with the static part; the sweep GEMM CTA needs 64-75 KB and 21.5 K registers).
+// B200, config 2: 535.8 -> 514.1 ms per step (the panels no longer hold ~half of the SMs to themselves);
+// 8-energy shards 103.7 -> 108.2 ms (the shared FP64 pipe lengthens the panels' chain). -DBBSI_GJ_EXCLUSIVE_SM
+// builds the exclusive variant (W1 in a third shared-memory tile, one CTA per SM).
+#ifndef BBSI_GJ_EXCLUSIVE_SM
 #define GJ_ROWS_BOUNDS __maxnreg__(168)
 constexpr bool kW1Smem = false;
 #else
