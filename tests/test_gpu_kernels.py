@@ -168,6 +168,37 @@ def test_zinv_bits_independent_of_batch(gpu, n):
     assert np.array_equal(outs[0].view(np.uint64), outs[2].view(np.uint64))
 
 
+@pytest.mark.parametrize("n,batch", [(256, 6), (512, 3), (768, 2)])
+def test_zinv_deterministic_under_load(gpu, n, batch):
+    """Repeated inversions of one batch give the same bits every time, alone and while another
+    stream keeps the SMs busy with FP64 GEMMs (the panel CTA shares its SM with other CTAs; the
+    cluster variant exchanges pivots through DSMEM): a data race would show as run-to-run noise."""
+    from paper_2605_19910_b200._native import lib
+
+    torch = _torch()
+    rng = np.random.default_rng(3 * n + batch)
+    a = _rand(rng, batch, n, n)
+    side = torch.cuda.Stream()
+    x = torch.randn(2048, 2048, dtype=torch.float64, device="cuda")
+    first = None
+    for rep in range(12):
+        if rep >= 4:  # background load on another stream from the fifth repetition on
+            with torch.cuda.stream(side):
+                for _ in range(4):
+                    x = (x @ x) * 1e-3
+        da = _dev(a)
+        st = np.zeros(batch, dtype=np.int32)
+        rc = lib().bbsi_cuda_zinv_dev(n, n, batch, C.c_void_p(da.data_ptr()), n, n * n,
+                                      st.ctypes.data_as(C.c_void_p), C.c_void_p(0))
+        assert rc == 0 and (st == -1).all()
+        torch.cuda.synchronize()
+        out = da.cpu().numpy().view(np.uint64)
+        if first is None:
+            first = out
+        else:
+            assert np.array_equal(out, first), rep
+
+
 def test_zinv_flags_singular(gpu):
     from paper_2605_19910_b200._native import lib
 
